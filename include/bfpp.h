@@ -1,0 +1,122 @@
+/*
+ * bfpp.h — C ABI of the B200-native breadth-first pipeline executor.
+ *
+ * Schedule section: drop-in replacement for the reference's schedule/stage API
+ * (pipesim; C++ signatures in proj/include/pipesim/schedule.hpp and
+ * simulate.hpp). Exceptions cannot cross a C ABI, so every function returns a
+ * status code (BFPP_OK, BFPP_SPEC_ERROR = the CLI's exit code 2 for SpecError,
+ * BFPP_EXEC_ERROR = exit code 4 for SimError / execution failures;
+ * reference tools/pipesim.cpp:214-226) and the message is available from
+ * bfpp_last_error() (thread-local).
+ *
+ * Enum integer values are the reference's declaration order (wire format):
+ *   DpVariant  DP0=0 DP_PS=1 DP_FS=2                       (types.hpp:14)
+ *   Schedule   NoPipeline=0 GPipe=1 OneFOneB=2 DepthFirst=3 BreadthFirst=4 (types.hpp:15)
+ *   Lane       Compute=0 DpNet=1 PpNet=2                   (schedule.hpp:41)
+ *   TaskKind   Fwd=0 Bwd=1 Reduce=2 Reconstruct=3 Transfer=4 (schedule.hpp:42)
+ */
+#ifndef BFPP_H
+#define BFPP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BFPP_OK 0
+#define BFPP_SPEC_ERROR 2
+#define BFPP_EXEC_ERROR 4
+
+/* ---- value types (POD mirrors of the reference structs) ------------------ */
+
+/* mirrors pipesim::ModelSpec (types.hpp:29-43) */
+typedef struct bfpp_model_spec {
+    int64_t n_layers, s_hidden, n_heads, s_head, s_mlp, s_seq, s_voc;
+} bfpp_model_spec;
+
+/* mirrors pipesim::ParallelConfig (types.hpp:64-84) */
+typedef struct bfpp_parallel_config {
+    int64_t n_dp, n_tp, n_pp, n_mb, s_mb, n_loop;
+    int32_t dp_variant, schedule;
+} bfpp_parallel_config;
+
+/* mirrors pipesim::ClusterSpec (types.hpp:47-59) */
+typedef struct bfpp_cluster_spec {
+    int64_t n_node, s_node;
+    double peak_flops, bw_intra, bw_inter, pp_latency, mem_capacity, kernel_efficiency;
+} bfpp_cluster_spec;
+
+/* mirrors pipesim::TimingModel (schedule.hpp:24-39) */
+typedef struct bfpp_timing_model {
+    double t_fwd_stage, bwd_ratio, t_pp_transfer, pp_latency, t_dp_reduce_stage, t_dp_reconstruct_stage;
+} bfpp_timing_model;
+
+/* mirrors pipesim::Task (schedule.hpp:46-56) without deps (CSR accessors) */
+typedef struct bfpp_task {
+    int32_t id, lane, kind, priority;
+    int64_t device, peer_device, micro_batch, stage;
+} bfpp_task;
+
+typedef struct bfpp_graph bfpp_graph;       /* pipesim::TaskGraph */
+typedef struct bfpp_timeline bfpp_timeline; /* pipesim::Timeline  */
+typedef struct bfpp_exec bfpp_exec;         /* per-rank executor   */
+
+const char* bfpp_last_error(void);
+
+/* ---- schedule API ---------------------------------------------------------- */
+
+/* replaces ParallelConfig::validate(model[, cluster]) (types.cpp:92-130); cluster may be NULL */
+int bfpp_validate(const bfpp_model_spec* m, const bfpp_parallel_config* c, const bfpp_cluster_spec* cl);
+
+/* replaces place_stages (schedule.hpp:20, schedule.cpp:23-33). assignment_out
+ * receives n_stage entries (cap must be >= n_pp*n_loop). */
+int bfpp_place_stages(const bfpp_model_spec* m, const bfpp_parallel_config* c, int64_t* assignment_out,
+                      int64_t cap, int64_t* n_stage, int64_t* layers_per_stage);
+
+/* replaces build_tasks (schedule.hpp:73-74, schedule.cpp:422-452); the
+ * placement is recomputed from (m, c) exactly as place_stages does. */
+int bfpp_build_tasks(const bfpp_model_spec* m, const bfpp_parallel_config* c, bfpp_graph** out);
+
+/* replaces build_accumulation_tasks (schedule.hpp:80-81, schedule.cpp:454-500); order 0 = DF, 1 = BF */
+int bfpp_build_accumulation_tasks(const bfpp_model_spec* m, int32_t dp_variant, int32_t order, int64_t n_mb,
+                                  bfpp_graph** out);
+
+/* Builds a graph from raw arrays (deadlock / malformed-program tests; ref test_schedule.cpp:393-406). */
+int bfpp_graph_from_arrays(int64_t n_devices, int64_t n_tasks, const bfpp_task* tasks, const int32_t* dep_offsets,
+                           const int32_t* dep_ids, const int32_t* prog_offsets, const int32_t* prog_ids,
+                           bfpp_graph** out);
+
+int64_t bfpp_graph_n_devices(const bfpp_graph* g);
+int64_t bfpp_graph_n_tasks(const bfpp_graph* g);
+int64_t bfpp_graph_n_deps(const bfpp_graph* g);
+int64_t bfpp_graph_n_program_steps(const bfpp_graph* g);
+/* copy-out: tasks[n_tasks]; dep CSR (offsets[n_tasks+1], ids[n_deps]); program CSR (offsets[n_devices+1], ids[...]) */
+int bfpp_graph_tasks(const bfpp_graph* g, bfpp_task* out, int64_t cap);
+int bfpp_graph_deps(const bfpp_graph* g, int32_t* offsets, int32_t* ids);
+int bfpp_graph_programs(const bfpp_graph* g, int32_t* offsets, int32_t* ids);
+void bfpp_graph_destroy(bfpp_graph* g);
+
+/* replaces simulate (simulate.hpp:28, simulate.cpp:41-158) */
+int bfpp_simulate(const bfpp_graph* g, const bfpp_timing_model* t, bfpp_timeline** out);
+int64_t bfpp_timeline_n_events(const bfpp_timeline* tl);
+int64_t bfpp_timeline_n_devices(const bfpp_timeline* tl);
+double bfpp_timeline_makespan(const bfpp_timeline* tl);
+/* start/end[n_events] (seconds), lane_busy[n_devices*3] */
+int bfpp_timeline_events(const bfpp_timeline* tl, double* start, double* end, double* lane_busy);
+/* Builds a timeline from measured per-task intervals (executor output, or tests). */
+int bfpp_timeline_from_arrays(const bfpp_graph* g, const double* start, const double* end, bfpp_timeline** out);
+void bfpp_timeline_destroy(bfpp_timeline* tl);
+
+/* replaces bubble_fraction (simulate.cpp:160-164) */
+double bfpp_bubble_fraction(const bfpp_timeline* tl);
+/* replaces peak_inflight (simulate.cpp:166-191); out[n_devices] */
+int bfpp_peak_inflight(const bfpp_timeline* tl, const bfpp_graph* g, int64_t layers_per_stage, int64_t* out);
+/* replaces compute_per_gpu (types.cpp:136-146; Eq. 11) */
+double bfpp_compute_per_gpu(const bfpp_model_spec* m, const bfpp_parallel_config* c);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BFPP_H */

@@ -1,0 +1,373 @@
+"""Host-side mirror of the reference's ``pipesim`` Python module for the hot path.
+
+Same names, argument meaning and error behaviour as the reference's pybind
+module (proj/bindings/module.cpp:28-379) for the schedule/stage API:
+``ModelSpec``, ``ParallelConfig``, ``ClusterSpec``, ``TimingModel``,
+``place_stages``, ``build_tasks``, ``build_accumulation_tasks``, ``simulate``,
+``simulate_config``, ``bubble_fraction``, ``peak_inflight``,
+``accumulation_timeline``, ``compute_per_gpu``, ``param_count``,
+``throughput``; ``SpecError``/``SimError`` exceptions. Everything computes in
+libbfpp.so (C ABI, include/bfpp.h); this file only marshals. Unlike the
+reference binding, ``Task.priority`` is exposed (module.cpp:185-193 omits it).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import List
+
+from . import _native as N
+
+
+class SpecError(ValueError):
+    """Invalid model/cluster/config (reference error.hpp:8-12; exit code 2)."""
+
+
+class SimError(RuntimeError):
+    """Wedged program / execution failure (reference error.hpp:14-18; exit code 4)."""
+
+
+class DpVariant(enum.IntEnum):
+    DP0 = 0
+    DP_PS = 1
+    DP_FS = 2
+
+
+class Schedule(enum.IntEnum):
+    NoPipeline = 0
+    GPipe = 1
+    OneFOneB = 2
+    DepthFirst = 3
+    BreadthFirst = 4
+
+
+class Lane(enum.IntEnum):
+    Compute = 0
+    DpNet = 1
+    PpNet = 2
+
+
+class TaskKind(enum.IntEnum):
+    Fwd = 0
+    Bwd = 1
+    Reduce = 2
+    Reconstruct = 3
+    Transfer = 4
+
+
+class AccumulationOrder(enum.IntEnum):
+    DepthFirst = 0
+    BreadthFirst = 1
+
+
+def _check(status: int):
+    if status == 0:
+        return
+    msg = N.lib().bfpp_last_error().decode()
+    if status == 2:
+        raise SpecError(msg)
+    raise SimError(msg)
+
+
+@dataclass(frozen=True)
+class ModelSpec:
+    """pipesim::ModelSpec; constructor validates like ModelSpec::make (types.cpp:57-68)."""
+    n_layers: int
+    s_hidden: int
+    n_heads: int
+    s_seq: int
+    s_voc: int
+    s_mlp: int = -1
+    s_head: int = -1
+
+    def __post_init__(self):
+        if self.s_head <= 0:
+            object.__setattr__(self, "s_head", self.s_hidden // self.n_heads if self.n_heads > 0 else 0)
+        if self.s_mlp <= 0:
+            object.__setattr__(self, "s_mlp", 4 * self.s_hidden)
+        _check(_validate_model(self))
+
+    def _c(self) -> N.ModelSpecC:
+        return N.ModelSpecC(self.n_layers, self.s_hidden, self.n_heads, self.s_head, self.s_mlp,
+                            self.s_seq, self.s_voc)
+
+
+def _validate_model(m: ModelSpec) -> int:
+    # A 1-stage, 1-micro-batch config only checks the model fields.
+    one = N.ParallelConfigC(1, 1, 1, 1, 1, 1, 0, 0)
+    mc = N.ModelSpecC(m.n_layers, m.s_hidden, m.n_heads, m.s_head, m.s_mlp, m.s_seq, m.s_voc)
+    return N.lib().bfpp_validate(C.byref(mc), C.byref(one), None)
+
+
+@dataclass(frozen=True)
+class ClusterSpec:
+    n_node: int
+    s_node: int
+    peak_flops: float
+    bw_intra: float
+    bw_inter: float
+    pp_latency: float = 0.0
+    mem_capacity: float = 0.0
+    kernel_efficiency: float = 0.6
+
+    def n_gpu(self) -> int:
+        return self.n_node * self.s_node
+
+    def _c(self) -> N.ClusterSpecC:
+        return N.ClusterSpecC(self.n_node, self.s_node, self.peak_flops, self.bw_intra, self.bw_inter,
+                              self.pp_latency, self.mem_capacity, self.kernel_efficiency)
+
+
+@dataclass(frozen=True)
+class ParallelConfig:
+    """pipesim::ParallelConfig; internal consistency checked on construction
+    (pybind ctor, module.cpp:114-121; types.cpp:92-108)."""
+    n_dp: int = 1
+    n_tp: int = 1
+    n_pp: int = 1
+    n_mb: int = 1
+    s_mb: int = 1
+    n_loop: int = 1
+    dp_variant: DpVariant = DpVariant.DP0
+    schedule: Schedule = Schedule.NoPipeline
+
+    def __post_init__(self):
+        # Model-independent checks: use a model whose layer count every stage count divides.
+        big = N.ModelSpecC(max(1, self.n_pp * self.n_loop), 1, 1, 1, 4, 1, 1)
+        _check(N.lib().bfpp_validate(C.byref(big), C.byref(self._c()), None))
+
+    def n_stage(self) -> int:
+        return self.n_pp * self.n_loop
+
+    def batch_size(self) -> int:
+        return self.n_dp * self.n_mb * self.s_mb
+
+    def validate(self, model: ModelSpec, cluster: ClusterSpec | None = None):
+        _check(N.lib().bfpp_validate(C.byref(model._c()), C.byref(self._c()),
+                                     C.byref(cluster._c()) if cluster is not None else None))
+
+    def _c(self) -> N.ParallelConfigC:
+        return N.ParallelConfigC(self.n_dp, self.n_tp, self.n_pp, self.n_mb, self.s_mb, self.n_loop,
+                                 int(self.dp_variant), int(self.schedule))
+
+
+@dataclass
+class TimingModel:
+    t_fwd_stage: float = 1.0
+    bwd_ratio: float = 2.0
+    t_pp_transfer: float = 0.0
+    pp_latency: float = 0.0
+    t_dp_reduce_stage: float = 0.0
+    t_dp_reconstruct_stage: float = 0.0
+
+    def _c(self) -> N.TimingModelC:
+        return N.TimingModelC(self.t_fwd_stage, self.bwd_ratio, self.t_pp_transfer, self.pp_latency,
+                              self.t_dp_reduce_stage, self.t_dp_reconstruct_stage)
+
+
+@dataclass(frozen=True)
+class StagePlacement:
+    n_stage: int
+    n_pp: int
+    layers_per_stage: int
+    assignment: List[int]
+
+    def device_of(self, stage: int) -> int:
+        return self.assignment[stage]
+
+    def layers_of(self, stage: int) -> range:
+        """Explicit layer range of a stage: [s*lps, (s+1)*lps)."""
+        return range(stage * self.layers_per_stage, (stage + 1) * self.layers_per_stage)
+
+
+@dataclass
+class Task:
+    id: int
+    device: int
+    peer_device: int
+    lane: Lane
+    kind: TaskKind
+    micro_batch: int
+    stage: int
+    priority: int
+    deps: List[int] = field(default_factory=list)
+
+
+class TaskGraph:
+    """pipesim::TaskGraph backed by a native handle (passed to the executor)."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+        L = N.lib()
+        n = L.bfpp_graph_n_tasks(self._h)
+        nd = L.bfpp_graph_n_devices(self._h)
+        raw = (N.TaskC * max(n, 1))()
+        _check(L.bfpp_graph_tasks(self._h, raw, n))
+        doff = (C.c_int32 * (n + 1))()
+        dids = (C.c_int32 * max(1, L.bfpp_graph_n_deps(self._h)))()
+        _check(L.bfpp_graph_deps(self._h, doff, dids))
+        poff = (C.c_int32 * (nd + 1))()
+        pids = (C.c_int32 * max(1, L.bfpp_graph_n_program_steps(self._h)))()
+        _check(L.bfpp_graph_programs(self._h, poff, pids))
+        self.n_devices = int(nd)
+        self.tasks = [Task(t.id, t.device, t.peer_device, Lane(t.lane), TaskKind(t.kind), t.micro_batch,
+                           t.stage, t.priority, list(dids[doff[i]:doff[i + 1]]))
+                      for i, t in enumerate(raw[:n])]
+        self.compute_program = [list(pids[poff[d]:poff[d + 1]]) for d in range(nd)]
+
+    def tasks_of_kind(self, kind: TaskKind) -> List[int]:
+        return [t.id for t in self.tasks if t.kind == kind]
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        try:
+            if self._h:
+                N.lib().bfpp_graph_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    @staticmethod
+    def from_tasks(n_devices: int, tasks: List[Task], compute_program: List[List[int]]) -> "TaskGraph":
+        n = len(tasks)
+        raw = (N.TaskC * max(n, 1))(*[N.TaskC(t.id, int(t.lane), int(t.kind), t.priority, t.device,
+                                              t.peer_device, t.micro_batch, t.stage) for t in tasks])
+        offs, ids = [0], []
+        for t in tasks:
+            ids += t.deps
+            offs.append(len(ids))
+        poffs, pids = [0], []
+        for p in compute_program:
+            pids += p
+            poffs.append(len(pids))
+        h = C.c_void_p()
+        arr = lambda xs: (C.c_int32 * max(1, len(xs)))(*xs)  # noqa: E731
+        _check(N.lib().bfpp_graph_from_arrays(n_devices, n, raw, arr(offs), arr(ids), arr(poffs), arr(pids),
+                                              C.byref(h)))
+        return TaskGraph(h.value)
+
+
+@dataclass
+class TimelineEvent:
+    task: int
+    start: float
+    end: float
+
+
+class Timeline:
+    """pipesim::Timeline (simulated or measured), backed by a native handle."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+        L = N.lib()
+        n = L.bfpp_timeline_n_events(self._h)
+        nd = L.bfpp_timeline_n_devices(self._h)
+        st = (C.c_double * max(n, 1))()
+        en = (C.c_double * max(n, 1))()
+        lb = (C.c_double * (3 * nd))()
+        _check(L.bfpp_timeline_events(self._h, st, en, lb))
+        self.n_devices = int(nd)
+        self.events = [TimelineEvent(i, st[i], en[i]) for i in range(n)]
+        self.makespan = float(L.bfpp_timeline_makespan(self._h))
+        self.lane_busy = [[lb[3 * d + l] for l in range(3)] for d in range(nd)]
+
+    def compute_busy_max(self) -> float:
+        return max([lb[0] for lb in self.lane_busy] + [0.0])
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        try:
+            if self._h:
+                N.lib().bfpp_timeline_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    @staticmethod
+    def from_intervals(graph: TaskGraph, start: List[float], end: List[float]) -> "Timeline":
+        n = len(graph.tasks)
+        h = C.c_void_p()
+        _check(N.lib().bfpp_timeline_from_arrays(graph.handle, (C.c_double * max(n, 1))(*start),
+                                                 (C.c_double * max(n, 1))(*end), C.byref(h)))
+        return Timeline(h.value)
+
+
+@dataclass
+class PerfPoint:
+    beta: float = 0.0
+    throughput: float = 0.0
+    utilization: float = 0.0
+    config: ParallelConfig | None = None
+
+
+def place_stages(model: ModelSpec, config: ParallelConfig) -> StagePlacement:
+    ns = config.n_pp * config.n_loop
+    out = (C.c_int64 * max(ns, 1))()
+    n_stage, lps = C.c_int64(), C.c_int64()
+    _check(N.lib().bfpp_place_stages(C.byref(model._c()), C.byref(config._c()), out, ns, C.byref(n_stage),
+                                     C.byref(lps)))
+    return StagePlacement(n_stage.value, config.n_pp, lps.value, list(out[:n_stage.value]))
+
+
+def build_tasks(model: ModelSpec, config: ParallelConfig, placement: StagePlacement | None = None) -> TaskGraph:
+    if placement is not None and (placement.n_stage != config.n_stage() or placement.n_pp != config.n_pp):
+        raise SpecError("error[invalid-spec]: schedule: placement does not match the configuration")
+    h = C.c_void_p()
+    _check(N.lib().bfpp_build_tasks(C.byref(model._c()), C.byref(config._c()), C.byref(h)))
+    return TaskGraph(h.value)
+
+
+def build_accumulation_tasks(model: ModelSpec, dp_variant: DpVariant, order: AccumulationOrder,
+                             n_mb: int) -> TaskGraph:
+    h = C.c_void_p()
+    _check(N.lib().bfpp_build_accumulation_tasks(C.byref(model._c()), int(dp_variant), int(order), n_mb,
+                                                 C.byref(h)))
+    return TaskGraph(h.value)
+
+
+def simulate(graph: TaskGraph, timing: TimingModel) -> Timeline:
+    h = C.c_void_p()
+    _check(N.lib().bfpp_simulate(graph.handle, C.byref(timing._c()), C.byref(h)))
+    return Timeline(h.value)
+
+
+def simulate_config(model: ModelSpec, config: ParallelConfig, timing: TimingModel) -> Timeline:
+    return simulate(build_tasks(model, config, place_stages(model, config)), timing)
+
+
+def accumulation_timeline(model, dp_variant, order, n_mb, timing) -> Timeline:
+    return simulate(build_accumulation_tasks(model, dp_variant, order, n_mb), timing)
+
+
+def bubble_fraction(timeline: Timeline) -> float:
+    return float(N.lib().bfpp_bubble_fraction(timeline.handle))
+
+
+def peak_inflight(timeline: Timeline, graph: TaskGraph, placement: StagePlacement) -> List[int]:
+    out = (C.c_int64 * timeline.n_devices)()
+    _check(N.lib().bfpp_peak_inflight(timeline.handle, graph.handle, placement.layers_per_stage, out))
+    return list(out)
+
+
+def compute_per_gpu(model: ModelSpec, config: ParallelConfig) -> float:
+    return float(N.lib().bfpp_compute_per_gpu(C.byref(model._c()), C.byref(config._c())))
+
+
+def param_count(model: ModelSpec) -> int:
+    return 12 * model.n_layers * model.s_hidden * model.s_hidden
+
+
+def throughput(model: ModelSpec, config: ParallelConfig, timeline: Timeline, cluster: ClusterSpec) -> PerfPoint:
+    """Eq. 11 flop/s per GPU over the (simulated or measured) makespan (perf.cpp:8-20)."""
+    config.validate(model, cluster)
+    if timeline.makespan <= 0:
+        raise SpecError("error[invalid-spec]: throughput: timeline has no extent")
+    tput = compute_per_gpu(model, config) / timeline.makespan
+    return PerfPoint(config.batch_size() / cluster.n_gpu(), tput, tput / cluster.peak_flops, config)
