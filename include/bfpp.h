@@ -116,6 +116,31 @@ int bfpp_peak_inflight(const bfpp_timeline* tl, const bfpp_graph* g, int64_t lay
 /* replaces compute_per_gpu (types.cpp:136-146; Eq. 11) */
 double bfpp_compute_per_gpu(const bfpp_model_spec* m, const bfpp_parallel_config* c);
 
+/* ---- device kernels (device pointers; stream is a cudaStream_t, NULL = default) --------
+ * The reference has no kernels (stage compute is the scalar
+ * TimingModel::t_fwd_stage, schedule.hpp:25-26); these are the stage executor's
+ * building blocks, exported for parity tests and micro-benchmarks. */
+
+/* epilogues of bfpp_gemm_bf16 */
+#define BFPP_EPI_BF16 0  /* D = acc (bf16)                                   */
+#define BFPP_EPI_GELU 1  /* aux_out = acc (bf16), D = gelu(aux_out) (bf16)   */
+#define BFPP_EPI_RESID 2 /* D = acc + aux (bf16)                             */
+#define BFPP_EPI_DGELU 3 /* D = acc * gelu'(aux) (bf16)                      */
+#define BFPP_EPI_F32 4   /* D (+)= acc (f32, accumulate flag)                */
+
+typedef struct bfpp_gemm_args {
+    int64_t M, N, K;
+    const void* A; int64_t lda; int32_t a_mn_major; /* 0: A[M][lda]; 1: A stored as [K][lda] */
+    const void* B; int64_t ldb; int32_t b_mn_major; /* 0: B[N][ldb]; 1: B stored as [K][ldb] */
+    void* D; int64_t ldd;
+    const void* aux; int64_t ldaux;
+    void* aux_out; int64_t ldaux_out;
+    int32_t epilogue, accumulate;
+} bfpp_gemm_args;
+
+/* D[M,N] = sum_k A[m,k] B[n,k] on tcgen05 (TMA + TMEM), bf16 in, f32 accumulate */
+int bfpp_gemm_bf16(const bfpp_gemm_args* args, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -3,7 +3,24 @@ from __future__ import annotations
 
 import ctypes as C
 
-PROTOS: dict = {}
+_P = C.c_void_p
+_I64 = C.c_int64
+_I32 = C.c_int32
+
+
+class GemmArgsC(C.Structure):
+    _fields_ = [("M", _I64), ("N", _I64), ("K", _I64),
+                ("A", _P), ("lda", _I64), ("a_mn_major", _I32),
+                ("B", _P), ("ldb", _I64), ("b_mn_major", _I32),
+                ("D", _P), ("ldd", _I64),
+                ("aux", _P), ("ldaux", _I64),
+                ("aux_out", _P), ("ldaux_out", _I64),
+                ("epilogue", _I32), ("accumulate", _I32)]
+
+
+PROTOS: dict = {
+    "bfpp_gemm_bf16": (C.c_int, [C.POINTER(GemmArgsC), _P]),
+}
 
 
 def bind(L):

@@ -1,0 +1,37 @@
+// Host interface of the sm_100a bf16 GEMM (gemm_sm100.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace bfpp {
+
+enum GemmEpilogue : int {
+    GEMM_EPI_BF16 = 0,   // D = acc                                (bf16)
+    GEMM_EPI_GELU = 1,   // aux_out = acc (bf16), D = gelu(aux_out) (bf16)
+    GEMM_EPI_RESID = 2,  // D = acc + aux                          (bf16)
+    GEMM_EPI_DGELU = 3,  // D = acc * gelu'(aux)                   (bf16)
+    GEMM_EPI_F32 = 4,    // D (+)= acc                             (f32; accumulate flag)
+};
+
+struct GemmArgs {
+    int64_t M = 0, N = 0, K = 0;
+    const void* A = nullptr;  // bf16
+    int64_t lda = 0;
+    int a_mn_major = 0;       // 0: A is [M][lda] (K contiguous); 1: A is [K][lda] (M contiguous)
+    const void* B = nullptr;  // bf16
+    int64_t ldb = 0;
+    int b_mn_major = 0;       // 0: B is [N][ldb]; 1: B is [K][ldb]
+    void* D = nullptr;
+    int64_t ldd = 0;
+    const void* aux = nullptr;
+    int64_t ldaux = 0;
+    void* aux_out = nullptr;
+    int64_t ldaux_out = 0;
+    int epilogue = GEMM_EPI_BF16;
+    int accumulate = 0;
+};
+
+void gemm_bf16(const GemmArgs& g, cudaStream_t stream);
+
+}  // namespace bfpp

@@ -1,0 +1,356 @@
+// Persistent warp-specialised bf16 GEMM for sm_100a: TMA -> SMEM (SWIZZLE_128B)
+// -> tcgen05.mma (accumulator in TMEM, double-buffered) -> fused epilogue.
+//
+//   D[M,N] = sum_k A[m,k] * B[n,k]      (f32 accumulate)
+//
+// A is either K-major (row-major [M][lda]) or MN-major (row-major [K][lda], i.e.
+// A^T stored); likewise B ([N][ldb] or [K][ldb]). The three transformer GEMM
+// forms are then: forward X.W^T (K,K), data-grad dY.W (K,MN) and weight-grad
+// dY^T.X (MN,MN), with no explicit transposes.
+//
+// Warp roles (192 threads): warp 0 = TMA producer, warp 1 = MMA issuer (+ TMEM
+// owner), warps 2..5 = epilogue (TMEM lane quarter = warp % 4).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+#include "gemm.hpp"
+#include "sm100_ptx.cuh"
+
+namespace bfpp {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int kStages = 4;
+constexpr int kThreads = 192;
+
+__device__ __forceinline__ float gelu_f(float x) {
+    const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+    return 0.5f * x * (1.f + tanhf(k0 * (x + k1 * x * x * x)));
+}
+__device__ __forceinline__ float dgelu_f(float x) {
+    const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+    const float u = k0 * (x + k1 * x * x * x);
+    const float t = tanhf(u);
+    return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x * x);
+}
+
+struct EpiArgs {
+    void* d;
+    int64_t ldd;
+    const __nv_bfloat16* aux;  // residual / gelu pre-activation input
+    int64_t ldaux;
+    __nv_bfloat16* aux_out;    // gelu pre-activation output
+    int64_t ldaux_out;
+    int epi;
+    int accumulate;
+};
+
+template <int BN>
+struct Smem {
+    static constexpr int kABytes = BM * BK * 2;
+    static constexpr int kBBytes = BN * BK * 2;
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kBarOffset = kStages * kStageBytes;
+    static constexpr int kBytes = kBarOffset + 256 + 1024;  // barriers + alignment slack
+};
+
+template <int BN, int A_MN, int B_MN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
+                EpiArgs ep) {
+    using S = Smem<BN>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kBarOffset);
+    uint64_t* empty = full + kStages;
+    uint64_t* tfull = empty + kStages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    const int m_tiles = (M + BM - 1) / BM;
+    const int n_tiles = (N + BN - 1) / BN;
+    const int num_tiles = m_tiles * n_tiles;
+    const int nk = (K + BK - 1) / BK;
+
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch(&tmA);
+        ptx::tma_prefetch(&tmB);
+        for (int s = 0; s < kStages; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            ptx::mbar_init(&tfull[b], 1);
+            ptx::mbar_init(&tempty[b], 4);
+        }
+        ptx::fence_barrier_init();
+    }
+    if (warp == 1) ptx::tmem_alloc<2 * BN>(tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ===== TMA producer =====
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+                const int m0 = (t % m_tiles) * BM, n0 = (t / m_tiles) * BN;
+                for (int kb = 0; kb < nk; ++kb) {
+                    ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t* sa = smem + stage * S::kStageBytes;
+                    uint8_t* sb = sa + S::kABytes;
+                    ptx::mbar_expect_tx(&full[stage], S::kStageBytes);
+                    const int k0 = kb * BK;
+                    if (A_MN) {
+#pragma unroll
+                        for (int i = 0; i < BM / 64; ++i) ptx::tma_load_2d(sa + i * 64 * BK * 2, &tmA, &full[stage], m0 + 64 * i, k0);
+                    } else {
+                        ptx::tma_load_2d(sa, &tmA, &full[stage], k0, m0);
+                    }
+                    if (B_MN) {
+#pragma unroll
+                        for (int i = 0; i < BN / 64; ++i) ptx::tma_load_2d(sb + i * 64 * BK * 2, &tmB, &full[stage], n0 + 64 * i, k0);
+                    } else {
+                        ptx::tma_load_2d(sb, &tmB, &full[stage], k0, n0);
+                    }
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ===== MMA issuer =====
+            constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM, BN, A_MN, B_MN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int it = 0;
+            for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+                const int acc = it & 1;
+                const uint32_t acc_phase = (it >> 1) & 1;
+                ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * BN;
+                for (int kb = 0; kb < nk; ++kb) {
+                    ptx::mbar_wait(&full[stage], phase);
+                    ptx::tc_fence_after();
+                    const uint32_t sa = ptx::smem_u32(smem + stage * S::kStageBytes);
+                    const uint32_t sb = sa + S::kABytes;
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k) {
+                        // K-major: advance 32 B inside the 128 B swizzle row; MN-major: 16 K-rows of 128 B.
+                        const uint64_t ad = A_MN ? ptx::sdesc_sw128(sa + k * 2048, 64 * BK * 2, 1024)
+                                                 : ptx::sdesc_sw128(sa + k * 32, 16, 1024);
+                        const uint64_t bd = B_MN ? ptx::sdesc_sw128(sb + k * 2048, 64 * BK * 2, 1024)
+                                                 : ptx::sdesc_sw128(sb + k * 32, 16, 1024);
+                        ptx::umma_f16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+                    }
+                    ptx::umma_commit(&empty[stage]);
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                ptx::umma_commit(&tfull[acc]);
+            }
+        }
+    } else {
+        // ===== epilogue: TMEM -> registers -> fused op -> global =====
+        const int q = warp & 3;
+        int it = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+            const int acc = it & 1;
+            const uint32_t acc_phase = (it >> 1) & 1;
+            const int m0 = (t % m_tiles) * BM, n0 = (t / m_tiles) * BN;
+            ptx::mbar_wait(&tfull[acc], acc_phase);
+            ptx::tc_fence_after();
+            const int row = m0 + q * 32 + lane;
+            const bool row_ok = row < M;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t r[32];
+                ptx::tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + acc * BN + c * 32, r);
+                ptx::tmem_ld_wait();
+                const int col0 = n0 + c * 32;
+                if (!row_ok || col0 >= N) continue;
+                const bool full_chunk = col0 + 32 <= N;
+                float v[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+                if (ep.epi == GEMM_EPI_F32) {
+                    float* d = static_cast<float*>(ep.d) + static_cast<int64_t>(row) * ep.ldd + col0;
+                    if (full_chunk) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 4) {
+                            float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                            if (ep.accumulate) {
+                                float4 p = *reinterpret_cast<const float4*>(d + j);
+                                o.x += p.x;
+                                o.y += p.y;
+                                o.z += p.z;
+                                o.w += p.w;
+                            }
+                            *reinterpret_cast<float4*>(d + j) = o;
+                        }
+                    } else {
+                        for (int j = 0; j < 32 && col0 + j < N; ++j) d[j] = ep.accumulate ? d[j] + v[j] : v[j];
+                    }
+                    continue;
+                }
+                __nv_bfloat16* d = static_cast<__nv_bfloat16*>(ep.d) + static_cast<int64_t>(row) * ep.ldd + col0;
+                if (ep.epi == GEMM_EPI_RESID || ep.epi == GEMM_EPI_DGELU) {
+                    const __nv_bfloat16* a = ep.aux + static_cast<int64_t>(row) * ep.ldaux + col0;
+                    if (full_chunk) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 8) {
+                            uint4 raw = *reinterpret_cast<const uint4*>(a + j);
+                            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                float2 f = __bfloat1622float2(h[u]);
+                                if (ep.epi == GEMM_EPI_RESID) {
+                                    v[j + 2 * u] += f.x;
+                                    v[j + 2 * u + 1] += f.y;
+                                } else {
+                                    v[j + 2 * u] *= dgelu_f(f.x);
+                                    v[j + 2 * u + 1] *= dgelu_f(f.y);
+                                }
+                            }
+                        }
+                    } else {
+                        for (int j = 0; j < 32 && col0 + j < N; ++j) {
+                            float f = __bfloat162float(a[j]);
+                            v[j] = ep.epi == GEMM_EPI_RESID ? v[j] + f : v[j] * dgelu_f(f);
+                        }
+                    }
+                }
+                if (ep.epi == GEMM_EPI_GELU) {
+                    __nv_bfloat16* pre = ep.aux_out + static_cast<int64_t>(row) * ep.ldaux_out + col0;
+                    // keep the pre-activation exactly as stored (bf16) so dgelu sees the same value
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        __nv_bfloat16 b = __float2bfloat16_rn(v[j]);
+                        if (full_chunk || col0 + j < N) pre[j] = b;
+                        v[j] = gelu_f(__bfloat162float(b));
+                    }
+                }
+                if (full_chunk) {
+#pragma unroll
+                    for (int j = 0; j < 32; j += 8) {
+                        uint4 o;
+                        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) h[u] = __floats2bfloat162_rn(v[j + 2 * u], v[j + 2 * u + 1]);
+                        *reinterpret_cast<uint4*>(d + j) = o;
+                    }
+                } else {
+                    for (int j = 0; j < 32 && col0 + j < N; ++j) d[j] = __float2bfloat16_rn(v[j]);
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+        }
+    }
+    __syncthreads();
+    if (warp == 1) ptx::tmem_dealloc<2 * BN>(tmem_base);
+}
+
+// ---- host side -----------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    if (!fn) throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+// 2-D bf16 tensor map over a row-major [rows][ld] matrix with `inner` valid
+// columns; box = {64 (inner), box_rows}, SWIZZLE_128B, OOB -> zero.
+CUtensorMap make_map(const void* ptr, int64_t inner, int64_t rows, int64_t ld, int box_rows) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+    return m;
+}
+
+int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return n;
+}
+
+template <int BN, int A_MN, int B_MN>
+void launch(const GemmArgs& g, cudaStream_t st) {
+    CUtensorMap ta = A_MN ? make_map(g.A, g.M, g.K, g.lda, BK) : make_map(g.A, g.K, g.M, g.lda, BM);
+    CUtensorMap tb = B_MN ? make_map(g.B, g.N, g.K, g.ldb, BK) : make_map(g.B, g.K, g.N, g.ldb, BN);
+    EpiArgs ep{g.D, g.ldd, static_cast<const __nv_bfloat16*>(g.aux), g.ldaux,
+               static_cast<__nv_bfloat16*>(g.aux_out), g.ldaux_out, g.epilogue, g.accumulate};
+    auto kern = gemm_kernel<BN, A_MN, B_MN>;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<BN>::kBytes);
+        configured = true;
+    }
+    const int tiles = static_cast<int>(((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN));
+    const int grid = tiles < num_sms() ? tiles : num_sms();
+    kern<<<grid, kThreads, Smem<BN>::kBytes, st>>>(ta, tb, static_cast<int>(g.M), static_cast<int>(g.N),
+                                                   static_cast<int>(g.K), ep);
+}
+
+}  // namespace
+
+void gemm_bf16(const GemmArgs& g, cudaStream_t st) {
+    if (g.M <= 0 || g.N <= 0 || g.K <= 0) throw std::runtime_error("gemm: empty problem");
+    if (g.K % 8 || g.lda % 8 || g.ldb % 8 || g.ldd % 8) throw std::runtime_error("gemm: K and leading dims must be multiples of 8");
+    const bool small_n = g.N <= 128;
+    const int a = g.a_mn_major ? 1 : 0, b = g.b_mn_major ? 1 : 0;
+#define BFPP_GEMM_CASE(BN_, A_, B_) \
+    if (a == A_ && b == B_) return launch<BN_, A_, B_>(g, st);
+    if (small_n) {
+        BFPP_GEMM_CASE(128, 0, 0)
+        BFPP_GEMM_CASE(128, 0, 1)
+        BFPP_GEMM_CASE(128, 1, 0)
+        BFPP_GEMM_CASE(128, 1, 1)
+    } else {
+        BFPP_GEMM_CASE(256, 0, 0)
+        BFPP_GEMM_CASE(256, 0, 1)
+        BFPP_GEMM_CASE(256, 1, 0)
+        BFPP_GEMM_CASE(256, 1, 1)
+    }
+#undef BFPP_GEMM_CASE
+}
+
+}  // namespace bfpp

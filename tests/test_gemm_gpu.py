@@ -1,0 +1,77 @@
+"""tcgen05 GEMM vs a plain PyTorch fp32 reference (bf16 inputs, f32 accumulate).
+
+Tolerance: bf16 outputs -> max |err| <= 1e-2 * max|ref|; f32 outputs ->
+1e-4 * max|ref| (accumulation-order differences only).
+"""
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _ops():
+    from paper_2211_05953_b200 import ops
+    return ops
+
+
+def _close(got, ref, rtol):
+    err = (got.float() - ref).abs().max().item()
+    scale = ref.abs().max().item() + 1e-6
+    assert err <= rtol * scale, (err, scale)
+
+
+@pytest.mark.parametrize("a_mn", [False, True])
+@pytest.mark.parametrize("b_mn", [False, True])
+@pytest.mark.parametrize("shape", [(256, 512, 128), (128, 256, 64), (384, 768, 320), (64, 1000, 128),
+                                   (2048, 2048, 2048), (200, 136, 72)])
+def test_gemm_layouts(cuda_device, a_mn, b_mn, shape):
+    ops = _ops()
+    M, N, K = shape
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    B = torch.randn(N, K, device="cuda", generator=g).bfloat16()
+    ref = A.float() @ B.float().t()
+    a_in = A.t().contiguous() if a_mn else A
+    b_in = B.t().contiguous() if b_mn else B
+    out = ops.gemm(a_in, b_in, a_mn_major=a_mn, b_mn_major=b_mn)
+    torch.cuda.synchronize()
+    _close(out, ref, 1e-2)
+    out32 = ops.gemm(a_in, b_in, a_mn_major=a_mn, b_mn_major=b_mn, epilogue=ops.EPI_F32)
+    torch.cuda.synchronize()
+    _close(out32, ref, 1e-4)
+
+
+def test_gemm_epilogues(cuda_device):
+    ops = _ops()
+    M, N, K = 256, 768, 192
+    A = torch.randn(M, K, device="cuda").bfloat16()
+    B = (0.1 * torch.randn(N, K, device="cuda")).bfloat16()
+    ref = A.float() @ B.float().t()
+    pre = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    out = ops.gemm(A, B, epilogue=ops.EPI_GELU, aux_out=pre)
+    _close(pre, ref, 1e-2)
+    _close(out, torch.nn.functional.gelu(pre.float(), approximate="tanh"), 1e-2)
+    R = torch.randn(M, N, device="cuda").bfloat16()
+    out = ops.gemm(A, B, epilogue=ops.EPI_RESID, aux=R)
+    _close(out, ref + R.float(), 1e-2)
+    x = pre.float().requires_grad_()
+    y = torch.nn.functional.gelu(x, approximate="tanh")
+    (dg,) = torch.autograd.grad(y, x, torch.ones_like(y))
+    out = ops.gemm(A, B, epilogue=ops.EPI_DGELU, aux=pre)
+    _close(out, ref * dg, 1e-2)
+    acc = torch.randn(M, N, device="cuda")
+    base = acc.clone()
+    ops.gemm(A, B, epilogue=ops.EPI_F32, out=acc, accumulate=True)
+    torch.cuda.synchronize()
+    _close(acc, base + ref, 1e-4)
+
+
+def test_gemm_strided_views(cuda_device):
+    """Leading dimensions larger than the logical width (e.g. Q/K/V slices of a fused QKV)."""
+    ops = _ops()
+    M, K = 256, 384
+    X = torch.randn(M, 3 * K, device="cuda").bfloat16()
+    W = torch.randn(512, K, device="cuda").bfloat16()
+    view = X[:, K:2 * K]
+    out = ops.gemm(view, W)
+    _close(out, view.float() @ W.float().t(), 1e-2)
