@@ -141,6 +141,40 @@ typedef struct bfpp_gemm_args {
 /* D[M,N] = sum_k A[m,k] B[n,k] on tcgen05 (TMA + TMEM), bf16 in, f32 accumulate */
 int bfpp_gemm_bf16(const bfpp_gemm_args* args, void* stream);
 
+/* causal multi-head attention, head_dim 128 (flash-style; never materialises T x T).
+ * qkv [B*S][3*H*128] bf16 (Q | K | V column blocks), o [B*S][H*128] bf16,
+ * lse [B*H][S] f32 (log2-sum-exp of scaled scores). Backward scratch: delta [B*H][S],
+ * dq_acc [B*S][H*128] f32; dqkv has qkv's layout. */
+int bfpp_attention_fwd(const void* qkv, void* o, float* lse, int32_t batch, int32_t seq, int32_t heads,
+                       int32_t head_dim, void* stream);
+int bfpp_attention_bwd(const void* qkv, const void* o, const void* dout, const float* lse, float* delta,
+                       float* dq_acc, void* dqkv, int32_t batch, int32_t seq, int32_t heads, int32_t head_dim,
+                       void* stream);
+
+/* LayerNorm over rows of `width` (bf16 x/y, f32 gamma/beta/mean/rstd). The backward
+ * adds dres (may be NULL) to dx and ACCUMULATES dgamma/dbeta. */
+int bfpp_layernorm_fwd(const void* x, const float* gamma, const float* beta, void* y, float* mean, float* rstd,
+                       int32_t rows, int32_t width, float eps, void* stream);
+int bfpp_layernorm_bwd(const void* dy, const void* x, const float* gamma, const float* mean, const float* rstd,
+                       const void* dres, void* dx, float* dgamma, float* dbeta, int32_t rows, int32_t width,
+                       void* stream);
+
+/* x[t] = wte[tok[t]] + wpe[t mod S] (bf16); backward scatter-adds into f32 dwte/dwpe */
+int bfpp_embed_fwd(const int32_t* tok, const void* wte, const void* wpe, void* x, int32_t T, int32_t S, int32_t h,
+                   void* stream);
+int bfpp_embed_bwd(const int32_t* tok, const void* dx, float* dwte, float* dwpe, int32_t T, int32_t S, int32_t h,
+                   void* stream);
+
+/* row_loss[t] = logsumexp(logits[t]) - logits[t][label[t]];
+ * logits[t] <- (softmax(logits[t]) - onehot(label[t])) * grad_scale   (in place, bf16) */
+int bfpp_softmax_xent(void* logits, int64_t ld, const int32_t* labels, float* row_loss, int32_t T, int32_t V,
+                      float grad_scale, void* stream);
+
+/* Adam (bias-corrected, decoupled weight decay) on f32 p/m/v with gradient g;
+ * writes the bf16 copy w16; zeroes g if zero_grad. */
+int bfpp_adam_update(float* p, float* m, float* v, float* g, void* w16, int64_t n, float lr, float beta1,
+                     float beta2, float eps, float weight_decay, int32_t step, int32_t zero_grad, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

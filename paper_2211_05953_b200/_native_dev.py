@@ -28,3 +28,16 @@ def bind(L):
         fn = getattr(L, name)
         fn.restype = res
         fn.argtypes = args
+
+_F = C.c_float
+_FP = C.c_void_p  # float* passed as raw pointers
+PROTOS.update({
+    "bfpp_attention_fwd": (C.c_int, [_P, _P, _P, _I32, _I32, _I32, _I32, _P]),
+    "bfpp_attention_bwd": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _I32, _I32, _I32, _I32, _P]),
+    "bfpp_layernorm_fwd": (C.c_int, [_P, _P, _P, _P, _P, _P, _I32, _I32, _F, _P]),
+    "bfpp_layernorm_bwd": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _I32, _P]),
+    "bfpp_embed_fwd": (C.c_int, [_P, _P, _P, _P, _I32, _I32, _I32, _P]),
+    "bfpp_embed_bwd": (C.c_int, [_P, _P, _P, _P, _I32, _I32, _I32, _P]),
+    "bfpp_softmax_xent": (C.c_int, [_P, _I64, _P, _P, _I32, _I32, _F, _P]),
+    "bfpp_adam_update": (C.c_int, [_P, _P, _P, _P, _P, _I64, _F, _F, _F, _F, _F, _I32, _I32, _P]),
+})

@@ -46,3 +46,76 @@ int bfpp_gemm_bf16(const bfpp_gemm_args* a, void* stream) {
 }
 
 }  // extern "C"
+
+extern "C" {
+
+int bfpp_attention_fwd(const void* qkv, void* o, float* lse, int32_t batch, int32_t seq, int32_t heads,
+                       int32_t head_dim, void* stream) {
+    return guarded([&] {
+        attention_fwd(qkv, o, lse, batch, seq, heads, head_dim, static_cast<cudaStream_t>(stream));
+        check_launch();
+    });
+}
+
+int bfpp_attention_bwd(const void* qkv, const void* o, const void* dout, const float* lse, float* delta,
+                       float* dq_acc, void* dqkv, int32_t batch, int32_t seq, int32_t heads, int32_t head_dim,
+                       void* stream) {
+    return guarded([&] {
+        attention_bwd(qkv, o, dout, lse, delta, dq_acc, dqkv, batch, seq, heads, head_dim,
+                      static_cast<cudaStream_t>(stream));
+        check_launch();
+    });
+}
+
+int bfpp_layernorm_fwd(const void* x, const float* gamma, const float* beta, void* y, float* mean, float* rstd,
+                       int32_t rows, int32_t width, float eps, void* stream) {
+    return guarded([&] {
+        layernorm_fwd(x, gamma, beta, y, mean, rstd, rows, width, eps, static_cast<cudaStream_t>(stream));
+        check_launch();
+    });
+}
+
+int bfpp_layernorm_bwd(const void* dy, const void* x, const float* gamma, const float* mean, const float* rstd,
+                       const void* dres, void* dx, float* dgamma, float* dbeta, int32_t rows, int32_t width,
+                       void* stream) {
+    return guarded([&] {
+        layernorm_bwd(dy, x, gamma, mean, rstd, dres, dx, dgamma, dbeta, rows, width,
+                      static_cast<cudaStream_t>(stream));
+        check_launch();
+    });
+}
+
+int bfpp_embed_fwd(const int32_t* tok, const void* wte, const void* wpe, void* x, int32_t T, int32_t S, int32_t h,
+                   void* stream) {
+    return guarded([&] {
+        embed_fwd(tok, wte, wpe, x, T, S, h, static_cast<cudaStream_t>(stream));
+        check_launch();
+    });
+}
+
+int bfpp_embed_bwd(const int32_t* tok, const void* dx, float* dwte, float* dwpe, int32_t T, int32_t S, int32_t h,
+                   void* stream) {
+    return guarded([&] {
+        embed_bwd(tok, dx, dwte, dwpe, T, S, h, static_cast<cudaStream_t>(stream));
+        check_launch();
+    });
+}
+
+int bfpp_softmax_xent(void* logits, int64_t ld, const int32_t* labels, float* row_loss, int32_t T, int32_t V,
+                      float grad_scale, void* stream) {
+    return guarded([&] {
+        softmax_xent(logits, ld, labels, row_loss, T, V, grad_scale, static_cast<cudaStream_t>(stream));
+        check_launch();
+    });
+}
+
+int bfpp_adam_update(float* p, float* m, float* v, float* g, void* w16, int64_t n, float lr, float beta1,
+                     float beta2, float eps, float weight_decay, int32_t step, int32_t zero_grad, void* stream) {
+    return guarded([&] {
+        adam_update(p, m, v, g, w16, n, lr, beta1, beta2, eps, weight_decay, step, zero_grad,
+                    static_cast<cudaStream_t>(stream));
+        check_launch();
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,256 @@
+// HBM-bound kernels of the stage executor: token/position embedding (fwd +
+// scatter-add bwd), fused softmax cross-entropy (loss + dlogits in place),
+// sharded Adam with bf16 emission, Philox normal init, reductions.
+// All use 128-bit vector accesses and grid sizes in multiples of the SM count.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <curand_kernel.h>
+
+#include <stdexcept>
+
+#include "kernels.hpp"
+
+namespace bfpp {
+namespace {
+
+int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int d = 0;
+        cudaGetDevice(&d);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+    }
+    return n;
+}
+
+__device__ __forceinline__ void bf8_to_f(const uint4& raw, float (&v)[8]) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        float2 f = __bfloat1622float2(h[u]);
+        v[2 * u] = f.x;
+        v[2 * u + 1] = f.y;
+    }
+}
+__device__ __forceinline__ uint4 f_to_bf8(const float (&v)[8]) {
+    uint4 o;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) h[u] = __floats2bfloat162_rn(v[2 * u], v[2 * u + 1]);
+    return o;
+}
+
+// x[t] = wte[tok[t]] + wpe[t % S]; one warp per row.
+__global__ void embed_fwd_kernel(const int32_t* __restrict__ tok, const __nv_bfloat16* __restrict__ wte,
+                                 const __nv_bfloat16* __restrict__ wpe, __nv_bfloat16* __restrict__ x, int T, int S,
+                                 int h) {
+    const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x & 31;
+    if (row >= T) return;
+    const int id = tok[row], pos = row % S;
+    for (int c = lane * 8; c < h; c += 256) {
+        float a[8], b[8];
+        bf8_to_f(*reinterpret_cast<const uint4*>(wte + static_cast<int64_t>(id) * h + c), a);
+        bf8_to_f(*reinterpret_cast<const uint4*>(wpe + static_cast<int64_t>(pos) * h + c), b);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a[u] += b[u];
+        *reinterpret_cast<uint4*>(x + static_cast<int64_t>(row) * h + c) = f_to_bf8(a);
+    }
+}
+
+__global__ void embed_bwd_kernel(const int32_t* __restrict__ tok, const __nv_bfloat16* __restrict__ dx,
+                                 float* __restrict__ dwte, float* __restrict__ dwpe, int T, int S, int h) {
+    const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x & 31;
+    if (row >= T) return;
+    const int id = tok[row], pos = row % S;
+    for (int c = lane * 8; c < h; c += 256) {
+        float a[8];
+        bf8_to_f(*reinterpret_cast<const uint4*>(dx + static_cast<int64_t>(row) * h + c), a);
+        float* pt = dwte + static_cast<int64_t>(id) * h + c;
+        float* pp = dwpe + static_cast<int64_t>(pos) * h + c;
+#pragma unroll
+        for (int u = 0; u < 8; u += 4) {
+            asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(pt + u), "f"(a[u]), "f"(a[u + 1]),
+                         "f"(a[u + 2]), "f"(a[u + 3])
+                         : "memory");
+            asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(pp + u), "f"(a[u]), "f"(a[u + 1]),
+                         "f"(a[u + 2]), "f"(a[u + 3])
+                         : "memory");
+        }
+    }
+}
+
+// One 256-thread block per row: online max/sum-exp, then dlogits = (softmax - onehot) * gscale in place.
+__global__ void __launch_bounds__(256) xent_kernel(__nv_bfloat16* __restrict__ logits, int64_t ld,
+                                                   const int32_t* __restrict__ labels, float* __restrict__ row_loss,
+                                                   int V, float gscale) {
+    const int row = blockIdx.x;
+    __nv_bfloat16* lr = logits + static_cast<int64_t>(row) * ld;
+    float m = -INFINITY, s = 0.f;
+    for (int c = threadIdx.x * 8; c < V; c += 256 * 8) {
+        float v[8];
+        bf8_to_f(*reinterpret_cast<const uint4*>(lr + c), v);
+        float mx = v[0];
+#pragma unroll
+        for (int u = 1; u < 8; ++u) mx = fmaxf(mx, v[u]);
+        const float nm = fmaxf(m, mx);
+        float acc = s * __expf(m - nm);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc += __expf(v[u] - nm);
+        m = nm;
+        s = acc;
+    }
+#pragma unroll
+    for (int k = 16; k; k >>= 1) {
+        const float om = __shfl_xor_sync(0xffffffff, m, k), os = __shfl_xor_sync(0xffffffff, s, k);
+        const float nm = fmaxf(m, om);
+        s = (m == -INFINITY ? 0.f : s * __expf(m - nm)) + (om == -INFINITY ? 0.f : os * __expf(om - nm));
+        m = nm;
+    }
+    __shared__ float sm_m[8], sm_s[8];
+    if ((threadIdx.x & 31) == 0) sm_m[threadIdx.x >> 5] = m, sm_s[threadIdx.x >> 5] = s;
+    __syncthreads();
+    float M = sm_m[0];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) M = fmaxf(M, sm_m[i]);
+    float Ssum = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) Ssum += sm_s[i] * __expf(sm_m[i] - M);
+    const float lse = M + __logf(Ssum);
+    const int label = labels[row];
+    if (threadIdx.x == 0) row_loss[row] = lse - __bfloat162float(lr[label]);
+    __syncthreads();  // the label logit is read before it is overwritten
+    const float inv = 1.f / Ssum;
+    for (int c = threadIdx.x * 8; c < V; c += 256 * 8) {
+        float v[8];
+        bf8_to_f(*reinterpret_cast<const uint4*>(lr + c), v);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = (__expf(v[u] - M) * inv - (c + u == label ? 1.f : 0.f)) * gscale;
+        *reinterpret_cast<uint4*>(lr + c) = f_to_bf8(v);
+    }
+}
+
+// p, m, v f32 shards; g f32 gradient (zeroed after use if zero_grad); w16 bf16 copy of p.
+__global__ void adam_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
+                            float* __restrict__ g, __nv_bfloat16* __restrict__ w16, int64_t n, float lr, float b1,
+                            float b2, float eps, float wd, float bc1, float bc2, int zero_grad) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x * 4;
+    for (int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4; i < n; i += stride) {
+        if (i + 4 <= n) {
+            float4 P = *reinterpret_cast<float4*>(p + i), Mv = *reinterpret_cast<float4*>(m + i);
+            float4 Vv = *reinterpret_cast<float4*>(v + i), G = *reinterpret_cast<const float4*>(g + i);
+            float* pp = &P.x;
+            float* mm = &Mv.x;
+            float* vv = &Vv.x;
+            const float* gg = &G.x;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                mm[u] = b1 * mm[u] + (1.f - b1) * gg[u];
+                vv[u] = b2 * vv[u] + (1.f - b2) * gg[u] * gg[u];
+                const float mh = mm[u] / bc1, vh = vv[u] / bc2;
+                pp[u] -= lr * (mh / (sqrtf(vh) + eps) + wd * pp[u]);
+            }
+            *reinterpret_cast<float4*>(p + i) = P;
+            *reinterpret_cast<float4*>(m + i) = Mv;
+            *reinterpret_cast<float4*>(v + i) = Vv;
+            if (zero_grad) *reinterpret_cast<float4*>(g + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+            __nv_bfloat162 lo = __floats2bfloat162_rn(P.x, P.y), hi = __floats2bfloat162_rn(P.z, P.w);
+            uint2 o;
+            o.x = *reinterpret_cast<uint32_t*>(&lo);
+            o.y = *reinterpret_cast<uint32_t*>(&hi);
+            *reinterpret_cast<uint2*>(w16 + i) = o;
+        } else {
+            for (int64_t j = i; j < n; ++j) {
+                m[j] = b1 * m[j] + (1.f - b1) * g[j];
+                v[j] = b2 * v[j] + (1.f - b2) * g[j] * g[j];
+                p[j] -= lr * ((m[j] / bc1) / (sqrtf(v[j] / bc2) + eps) + wd * p[j]);
+                if (zero_grad) g[j] = 0.f;
+                w16[j] = __float2bfloat16_rn(p[j]);
+            }
+        }
+    }
+}
+
+__global__ void init_normal_kernel(float* __restrict__ p, __nv_bfloat16* __restrict__ w16, int64_t n, float mean,
+                                   float std, uint64_t seed, uint64_t offset) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x * 4;
+    for (int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4; i < n; i += stride) {
+        curandStatePhilox4_32_10_t st;
+        curand_init(seed, (offset + i) / 4, 0, &st);
+        const float4 r = curand_normal4(&st);
+        const float vals[4] = {mean + std * r.x, mean + std * r.y, mean + std * r.z, mean + std * r.w};
+        for (int u = 0; u < 4 && i + u < n; ++u) {
+            if (p) p[i + u] = vals[u];
+            if (w16) w16[i + u] = __float2bfloat16_rn(vals[u]);
+        }
+    }
+}
+
+__global__ void f32_to_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst, int64_t n) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        dst[i] = __float2bfloat16_rn(src[i]);
+}
+
+__global__ void sum_kernel(const float* __restrict__ x, int64_t n, float scale, float* __restrict__ out,
+                           int accumulate) {
+    float s = 0.f;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += x[i];
+#pragma unroll
+    for (int k = 16; k; k >>= 1) s += __shfl_xor_sync(0xffffffff, s, k);
+    __shared__ float part[32];
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float t = 0.f;
+        for (int i = 0; i < static_cast<int>(blockDim.x / 32); ++i) t += part[i];
+        *out = (accumulate ? *out : 0.f) + t * scale;
+    }
+}
+
+}  // namespace
+
+void embed_fwd(const int32_t* tok, const void* wte, const void* wpe, void* x, int T, int S, int h, cudaStream_t st) {
+    if (h % 8) throw std::runtime_error("embedding: hidden size must be a multiple of 8");
+    embed_fwd_kernel<<<(T + 7) / 8, 256, 0, st>>>(tok, static_cast<const __nv_bfloat16*>(wte),
+                                                  static_cast<const __nv_bfloat16*>(wpe),
+                                                  static_cast<__nv_bfloat16*>(x), T, S, h);
+}
+
+void embed_bwd(const int32_t* tok, const void* dx, float* dwte, float* dwpe, int T, int S, int h, cudaStream_t st) {
+    embed_bwd_kernel<<<(T + 7) / 8, 256, 0, st>>>(tok, static_cast<const __nv_bfloat16*>(dx), dwte, dwpe, T, S, h);
+}
+
+void softmax_xent(void* logits, int64_t ld, const int32_t* labels, float* row_loss, int T, int V, float grad_scale,
+                  cudaStream_t st) {
+    if (V % 8 || ld % 8) throw std::runtime_error("xent: vocab and ld must be multiples of 8");
+    xent_kernel<<<T, 256, 0, st>>>(static_cast<__nv_bfloat16*>(logits), ld, labels, row_loss, V, grad_scale);
+}
+
+void adam_update(float* p, float* m, float* v, float* g, void* w16, int64_t n, float lr, float b1, float b2,
+                 float eps, float wd, int step, int zero_grad, cudaStream_t st) {
+    const float bc1 = 1.f - powf(b1, static_cast<float>(step));
+    const float bc2 = 1.f - powf(b2, static_cast<float>(step));
+    const int64_t want = (n / 4 + 255) / 256;
+    const int blocks = static_cast<int>(want < 8 * sm_count() ? (want > 0 ? want : 1) : 8 * sm_count());
+    adam_kernel<<<blocks, 256, 0, st>>>(p, m, v, g, static_cast<__nv_bfloat16*>(w16), n, lr, b1, b2, eps, wd, bc1,
+                                        bc2, zero_grad);
+}
+
+void init_normal(float* p, void* w16, int64_t n, float mean, float std, uint64_t seed, uint64_t offset,
+                 cudaStream_t st) {
+    const int64_t want = (n / 4 + 255) / 256;
+    const int blocks = static_cast<int>(want < 8 * sm_count() ? (want > 0 ? want : 1) : 8 * sm_count());
+    init_normal_kernel<<<blocks, 256, 0, st>>>(p, static_cast<__nv_bfloat16*>(w16), n, mean, std, seed, offset);
+}
+
+void f32_to_bf16(const float* src, void* dst, int64_t n, cudaStream_t st) {
+    const int64_t want = (n + 255) / 256;
+    const int blocks = static_cast<int>(want < 8 * sm_count() ? (want > 0 ? want : 1) : 8 * sm_count());
+    f32_to_bf16_kernel<<<blocks, 256, 0, st>>>(src, static_cast<__nv_bfloat16*>(dst), n);
+}
+
+void sum_f32(const float* x, int64_t n, float scale, float* out, int accumulate, cudaStream_t st) {
+    sum_kernel<<<1, 1024, 0, st>>>(x, n, scale, out, accumulate);
+}
+
+}  // namespace bfpp

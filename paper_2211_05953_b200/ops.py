@@ -50,3 +50,69 @@ def gemm(a: torch.Tensor, b: torch.Tensor, *, a_mn_major=False, b_mn_major=False
                      _ptr(aux_out), aux_out.stride(0) if aux_out is not None else 0, epilogue, int(accumulate))
     _check(_nat.lib().bfpp_gemm_bf16(C.byref(args), _stream()))
     return out
+
+
+def attention_fwd(qkv, batch, seq, heads, head_dim=128):
+    T = batch * seq
+    o = torch.empty(T, heads * head_dim, device=qkv.device, dtype=torch.bfloat16)
+    lse = torch.empty(batch * heads, seq, device=qkv.device, dtype=torch.float32)
+    _check(_nat.lib().bfpp_attention_fwd(qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), batch, seq, heads,
+                                         head_dim, _stream()))
+    return o, lse
+
+
+def attention_bwd(qkv, o, dout, lse, batch, seq, heads, head_dim=128):
+    T = batch * seq
+    delta = torch.empty(batch * heads, seq, device=qkv.device, dtype=torch.float32)
+    dq_acc = torch.empty(T, heads * head_dim, device=qkv.device, dtype=torch.float32)
+    dqkv = torch.empty_like(qkv)
+    _check(_nat.lib().bfpp_attention_bwd(qkv.data_ptr(), o.data_ptr(), dout.data_ptr(), lse.data_ptr(),
+                                         delta.data_ptr(), dq_acc.data_ptr(), dqkv.data_ptr(), batch, seq, heads,
+                                         head_dim, _stream()))
+    return dqkv
+
+
+def layernorm_fwd(x, gamma, beta, eps=1e-5):
+    rows, width = x.shape
+    y = torch.empty_like(x)
+    mean = torch.empty(rows, device=x.device, dtype=torch.float32)
+    rstd = torch.empty(rows, device=x.device, dtype=torch.float32)
+    _check(_nat.lib().bfpp_layernorm_fwd(x.data_ptr(), gamma.data_ptr(), beta.data_ptr(), y.data_ptr(),
+                                         mean.data_ptr(), rstd.data_ptr(), rows, width, eps, _stream()))
+    return y, mean, rstd
+
+
+def layernorm_bwd(dy, x, gamma, mean, rstd, dgamma, dbeta, dres=None):
+    rows, width = x.shape
+    dx = torch.empty_like(x)
+    _check(_nat.lib().bfpp_layernorm_bwd(dy.data_ptr(), x.data_ptr(), gamma.data_ptr(), mean.data_ptr(),
+                                         rstd.data_ptr(), _ptr(dres), dx.data_ptr(), dgamma.data_ptr(),
+                                         dbeta.data_ptr(), rows, width, _stream()))
+    return dx
+
+
+def embed_fwd(tok, wte, wpe, seq):
+    T, h = tok.numel(), wte.shape[1]
+    x = torch.empty(T, h, device=wte.device, dtype=torch.bfloat16)
+    _check(_nat.lib().bfpp_embed_fwd(tok.data_ptr(), wte.data_ptr(), wpe.data_ptr(), x.data_ptr(), T, seq, h,
+                                     _stream()))
+    return x
+
+
+def embed_bwd(tok, dx, dwte, dwpe, seq):
+    T, h = dx.shape
+    _check(_nat.lib().bfpp_embed_bwd(tok.data_ptr(), dx.data_ptr(), dwte.data_ptr(), dwpe.data_ptr(), T, seq, h,
+                                     _stream()))
+
+
+def softmax_xent_(logits, labels, grad_scale):
+    T, V = logits.shape
+    loss = torch.empty(T, device=logits.device, dtype=torch.float32)
+    _check(_nat.lib().bfpp_softmax_xent(logits.data_ptr(), logits.stride(0), labels.data_ptr(), loss.data_ptr(),
+                                        T, V, grad_scale, _stream()))
+    return loss
+
+
+def adam_update_(p, m, v, g, w16, lr, beta1, beta2, eps, wd, step, zero_grad=False):
+    _check(_nat.lib().bfpp_adam_update(p.data_ptr(), m.data_ptr(), v.data_ptr(), g.data_ptr(), w16.data_ptr(),
+                                       p.numel(), lr, beta1, beta2, eps, wd, step, int(zero_grad), _stream()))
