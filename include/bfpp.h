@@ -151,11 +151,11 @@ int bfpp_attention_bwd(const void* qkv, const void* o, const void* dout, const f
                        float* dq_acc, void* dqkv, int32_t batch, int32_t seq, int32_t heads, int32_t head_dim,
                        void* stream);
 
-/* LayerNorm over rows of `width` (bf16 x/y, f32 gamma/beta/mean/rstd). The backward
+/* LayerNorm over rows of `width` (bf16 x/y/gamma/beta, f32 mean/rstd). The backward
  * adds dres (may be NULL) to dx and ACCUMULATES dgamma/dbeta. */
-int bfpp_layernorm_fwd(const void* x, const float* gamma, const float* beta, void* y, float* mean, float* rstd,
+int bfpp_layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, float* mean, float* rstd,
                        int32_t rows, int32_t width, float eps, void* stream);
-int bfpp_layernorm_bwd(const void* dy, const void* x, const float* gamma, const float* mean, const float* rstd,
+int bfpp_layernorm_bwd(const void* dy, const void* x, const void* gamma, const float* mean, const float* rstd,
                        const void* dres, void* dx, float* dgamma, float* dbeta, int32_t rows, int32_t width,
                        void* stream);
 
@@ -174,6 +174,62 @@ int bfpp_softmax_xent(void* logits, int64_t ld, const int32_t* labels, float* ro
  * writes the bf16 copy w16; zeroes g if zero_grad. */
 int bfpp_adam_update(float* p, float* m, float* v, float* g, void* w16, int64_t n, float lr, float beta1,
                      float beta2, float eps, float weight_decay, int32_t step, int32_t zero_grad, void* stream);
+
+/* ---- executor: the reference's simulate() replaced by real execution --------------------
+ * One process per GPU, rank = dp * n_pp + pp (reference placement convention,
+ * types.hpp:110-113 with n_tp = 1). The executor builds the same TaskGraph as
+ * bfpp_build_tasks and runs this rank's slice: Compute lane -> compute stream in
+ * program order; DpNet lane -> DP stream in priority order (NCCL all-gather for
+ * Reconstruct, reduce-scatter / all-reduce + sharded Adam for Reduce); PpNet ->
+ * ncclSend/ncclRecv on one 2-rank communicator + stream per directed pipeline edge.
+ * The model is a pre-LN GPT (bias-free linears, GeLU MLP, untied embeddings; the
+ * embedding is folded into stage 0 and final LN + LM head + loss into the last
+ * stage). */
+
+#define BFPP_NCCL_UID_BYTES 128
+#define BFPP_EXEC_SKIP_OPTIMIZER 1 /* flags: keep gradients, do not run Adam */
+
+typedef struct bfpp_exec_opts {
+    int32_t device;          /* CUDA ordinal of this rank */
+    int32_t record_timeline; /* 1: per-task CUDA events -> bfpp_exec_timeline */
+    uint64_t seed;           /* Philox seed of the default N(0, init_std) initialisation */
+    float lr, beta1, beta2, eps, weight_decay, init_std;
+    int32_t flags;
+} bfpp_exec_opts;
+
+/* Fills 128 bytes with a fresh ncclUniqueId (generated on one rank, broadcast by the caller). */
+int bfpp_nccl_unique_id(void* out);
+/* Number of unique ids bfpp_exec_create expects: 1 + n_pp (DP groups) + 2 * n_pp * n_dp
+ * (directed pipeline edges); id[1 + d] = DP group of pipeline rank d, id[1 + n_pp + (dp*n_pp + d)*2 + dir]
+ * = edge d -> d+1 (dir 0, forward) or d -> d-1 (dir 1, backward) of replica dp. */
+int64_t bfpp_exec_n_comm_ids(const bfpp_parallel_config* c);
+int bfpp_exec_create(const bfpp_model_spec* m, const bfpp_parallel_config* c, const bfpp_exec_opts* o,
+                     int32_t rank, int32_t world, const void* uids, bfpp_exec** out);
+/* One training step (forward, backward, gradient reduction, Adam) over this replica's
+ * tokens [n_mb][s_mb][s_seq+1] int32 (inputs = [..., :-1], labels = [..., 1:]).
+ * bfpp_exec_step takes HOST tokens and returns the replica's mean token loss on the
+ * last-stage rank (NaN elsewhere); bfpp_exec_step_device takes DEVICE tokens, writes
+ * the loss to a device float (may be NULL) and does not synchronise. */
+int bfpp_exec_step(bfpp_exec* e, const int32_t* tokens_host, float* loss);
+int bfpp_exec_step_device(bfpp_exec* e, const int32_t* tokens_dev, float* loss_dev);
+int bfpp_exec_sync(bfpp_exec* e);
+void bfpp_exec_destroy(bfpp_exec* e);
+/* a copy of the executor's task graph (identical to bfpp_build_tasks) */
+int bfpp_exec_graph(const bfpp_exec* e, bfpp_graph** out);
+int64_t bfpp_exec_n_local_stages(const bfpp_exec* e);
+int64_t bfpp_exec_local_stage(const bfpp_exec* e, int64_t c);
+int64_t bfpp_exec_stage_numel(const bfpp_exec* e, int64_t stage);
+int64_t bfpp_exec_device_bytes(const bfpp_exec* e);
+/* Parameter I/O in the stage's flat layout. set_params takes the full stage
+ * vector on every DP rank; get_params / get_grads write this rank's [lo, hi) range of the
+ * f32 master weights / reduced gradients into a full-size buffer. */
+int bfpp_exec_set_params(bfpp_exec* e, int64_t stage, const float* host, int64_t n);
+int bfpp_exec_get_params(bfpp_exec* e, int64_t stage, float* host, int64_t n, int64_t* lo, int64_t* hi);
+int bfpp_exec_get_grads(bfpp_exec* e, int64_t stage, float* host, int64_t n, int64_t* lo, int64_t* hi);
+int bfpp_exec_zero_grads(bfpp_exec* e);
+/* measured [start, end] (seconds from the step origin) of this rank's tasks in the last
+ * step; tasks of other devices are NaN. Arrays have bfpp_graph_n_tasks entries. */
+int bfpp_exec_timeline(const bfpp_exec* e, double* start, double* end);
 
 #ifdef __cplusplus
 }

@@ -41,3 +41,26 @@ PROTOS.update({
     "bfpp_softmax_xent": (C.c_int, [_P, _I64, _P, _P, _I32, _I32, _F, _P]),
     "bfpp_adam_update": (C.c_int, [_P, _P, _P, _P, _P, _I64, _F, _F, _F, _F, _F, _I32, _I32, _P]),
 })
+
+from ._native import ModelSpecC, ParallelConfigC, ExecOptsC  # noqa: E402
+
+PROTOS.update({
+    "bfpp_nccl_unique_id": (C.c_int, [_P]),
+    "bfpp_exec_n_comm_ids": (_I64, [C.POINTER(ParallelConfigC)]),
+    "bfpp_exec_create": (C.c_int, [C.POINTER(ModelSpecC), C.POINTER(ParallelConfigC), C.POINTER(ExecOptsC), _I32,
+                                   _I32, _P, C.POINTER(_P)]),
+    "bfpp_exec_step": (C.c_int, [_P, _P, C.POINTER(C.c_float)]),
+    "bfpp_exec_step_device": (C.c_int, [_P, _P, _P]),
+    "bfpp_exec_sync": (C.c_int, [_P]),
+    "bfpp_exec_destroy": (None, [_P]),
+    "bfpp_exec_graph": (C.c_int, [_P, C.POINTER(_P)]),
+    "bfpp_exec_n_local_stages": (_I64, [_P]),
+    "bfpp_exec_local_stage": (_I64, [_P, _I64]),
+    "bfpp_exec_stage_numel": (_I64, [_P, _I64]),
+    "bfpp_exec_device_bytes": (_I64, [_P]),
+    "bfpp_exec_set_params": (C.c_int, [_P, _I64, _P, _I64]),
+    "bfpp_exec_get_params": (C.c_int, [_P, _I64, _P, _I64, C.POINTER(_I64), C.POINTER(_I64)]),
+    "bfpp_exec_get_grads": (C.c_int, [_P, _I64, _P, _I64, C.POINTER(_I64), C.POINTER(_I64)]),
+    "bfpp_exec_zero_grads": (C.c_int, [_P]),
+    "bfpp_exec_timeline": (C.c_int, [_P, _P, _P]),
+})

@@ -1,0 +1,95 @@
+// extern "C" boundary of the executor (include/bfpp.h, executor section).
+#include <nccl.h>
+
+#include <cstring>
+#include <vector>
+
+#include "../../../include/bfpp.h"
+#include "../sched/capi_util.hpp"
+#include "executor.hpp"
+
+struct bfpp_exec {
+    std::unique_ptr<bfpp::Executor> x;
+};
+
+using namespace bfpp;
+
+extern "C" {
+
+int bfpp_nccl_unique_id(void* out) {
+    return guarded([&] {
+        static_assert(sizeof(ncclUniqueId) == BFPP_NCCL_UID_BYTES, "ncclUniqueId size");
+        ncclUniqueId id;
+        if (ncclGetUniqueId(&id) != ncclSuccess) throw std::runtime_error("ncclGetUniqueId failed");
+        std::memcpy(out, &id, sizeof(id));
+    });
+}
+
+int64_t bfpp_exec_n_comm_ids(const bfpp_parallel_config* c) { return 1 + c->n_pp + 2 * c->n_pp * c->n_dp; }
+
+int bfpp_exec_create(const bfpp_model_spec* m, const bfpp_parallel_config* c, const bfpp_exec_opts* o, int32_t rank,
+                     int32_t world, const void* uids, bfpp_exec** out) {
+    *out = nullptr;
+    return guarded([&] {
+        ExecOptions eo;
+        eo.device = o->device;
+        eo.record_timeline = o->record_timeline != 0;
+        eo.seed = o->seed;
+        eo.lr = o->lr;
+        eo.beta1 = o->beta1;
+        eo.beta2 = o->beta2;
+        eo.eps = o->eps;
+        eo.weight_decay = o->weight_decay;
+        eo.init_std = o->init_std;
+        eo.skip_optimizer = (o->flags & BFPP_EXEC_SKIP_OPTIMIZER) != 0;
+        std::vector<ncclUniqueId> ids;
+        if (uids) {
+            const int64_t n = bfpp_exec_n_comm_ids(c);
+            ids.resize(static_cast<size_t>(n));
+            std::memcpy(ids.data(), uids, static_cast<size_t>(n) * sizeof(ncclUniqueId));
+        }
+        *out = new bfpp_exec{std::make_unique<Executor>(to_model(m), to_config(c), eo, rank, world, ids)};
+    });
+}
+
+int bfpp_exec_step(bfpp_exec* e, const int32_t* tokens_host, float* loss) {
+    return guarded([&] { e->x->step(tokens_host, true, loss, nullptr); });
+}
+
+int bfpp_exec_step_device(bfpp_exec* e, const int32_t* tokens_dev, float* loss_dev) {
+    return guarded([&] { e->x->step(tokens_dev, false, nullptr, loss_dev); });
+}
+
+int bfpp_exec_sync(bfpp_exec* e) {
+    return guarded([&] { e->x->sync(); });
+}
+
+void bfpp_exec_destroy(bfpp_exec* e) { delete e; }
+
+int bfpp_exec_graph(const bfpp_exec* e, bfpp_graph** out) {
+    *out = nullptr;
+    return guarded([&] { *out = new bfpp_graph{e->x->graph()}; });
+}
+
+int64_t bfpp_exec_n_local_stages(const bfpp_exec* e) { return e->x->n_local_stages(); }
+int64_t bfpp_exec_local_stage(const bfpp_exec* e, int64_t c) { return e->x->local_stage(c); }
+int64_t bfpp_exec_stage_numel(const bfpp_exec* e, int64_t stage) { return e->x->layout(stage).numel; }
+int64_t bfpp_exec_device_bytes(const bfpp_exec* e) { return static_cast<int64_t>(e->x->device_bytes()); }
+
+int bfpp_exec_set_params(bfpp_exec* e, int64_t stage, const float* host, int64_t n) {
+    return guarded([&] { e->x->set_params(stage, host, n); });
+}
+int bfpp_exec_get_params(bfpp_exec* e, int64_t stage, float* host, int64_t n, int64_t* lo, int64_t* hi) {
+    return guarded([&] { e->x->get_params(stage, host, n, lo, hi); });
+}
+int bfpp_exec_get_grads(bfpp_exec* e, int64_t stage, float* host, int64_t n, int64_t* lo, int64_t* hi) {
+    return guarded([&] { e->x->get_grads(stage, host, n, lo, hi); });
+}
+int bfpp_exec_zero_grads(bfpp_exec* e) {
+    return guarded([&] { e->x->zero_grads(); });
+}
+int bfpp_exec_timeline(const bfpp_exec* e, double* start, double* end) {
+    return guarded([&] { e->x->timeline(start, end); });
+}
+
+}  // extern "C"

@@ -1,0 +1,777 @@
+// Per-rank executor: runs one pipeline rank's slice of a bfpp TaskGraph on a
+// B200 with the sm_100a stage kernels, NCCL point-to-point hand-offs and
+// fully-sharded data-parallel traffic. See executor.hpp and DESIGN.md.
+#include "executor.hpp"
+
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <stdexcept>
+#include <string>
+
+#include "../kernels/gemm.hpp"
+#include "../kernels/kernels.hpp"
+
+namespace bfpp {
+
+#define CK(x)                                                                                                     \
+    do {                                                                                                          \
+        cudaError_t e_ = (x);                                                                                     \
+        if (e_ != cudaSuccess)                                                                                    \
+            throw std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(e_) + " at " #x);         \
+    } while (0)
+#define NK(x)                                                                                                     \
+    do {                                                                                                          \
+        ncclResult_t r_ = (x);                                                                                    \
+        if (r_ != ncclSuccess)                                                                                    \
+            throw std::runtime_error(std::string("NCCL error ") + ncclGetErrorString(r_) + " at " #x);         \
+    } while (0)
+
+using bf16 = __nv_bfloat16;
+
+StageLayout make_stage_layout(const ModelSpec& m, i64 stage, i64 n_stage, i64 lps, i64 n_dp) {
+    StageLayout L;
+    const int64_t h = m.s_hidden, mlp = m.s_mlp, V = m.s_voc, S = m.s_seq;
+    int64_t off = 0;
+    auto take = [&](int64_t n) {
+        const int64_t o = off;
+        off += (n + 63) / 64 * 64;  // 128-byte aligned sub-tensors (TMA needs 16 B)
+        return o;
+    };
+    L.first = stage == 0;
+    L.last = stage == n_stage - 1;
+    if (L.first) {
+        L.wte = take(V * h);
+        L.wpe = take(S * h);
+    }
+    for (i64 l = 0; l < lps; ++l) {
+        LayerParams p;
+        p.ln1_g = take(h);
+        p.ln1_b = take(h);
+        p.qkv = take(3 * h * h);
+        p.o = take(h * h);
+        p.ln2_g = take(h);
+        p.ln2_b = take(h);
+        p.fc1 = take(mlp * h);
+        p.fc2 = take(h * mlp);
+        L.layers.push_back(p);
+    }
+    if (L.last) {
+        L.lnf_g = take(h);
+        L.lnf_b = take(h);
+        L.head = take(V * h);
+    }
+    L.numel = off;
+    const int64_t q = 64 * n_dp;
+    L.padded = (off + q - 1) / q * q;
+    return L;
+}
+
+namespace {
+
+// Kinds of parameter sub-tensors for initialisation.
+struct Segment {
+    int64_t off, n;
+    float mean, std;
+};
+
+std::vector<Segment> init_segments(const StageLayout& L, const ModelSpec& m, float std) {
+    const int64_t h = m.s_hidden, mlp = m.s_mlp, V = m.s_voc, S = m.s_seq;
+    const float out_std = std / std::sqrt(2.f * static_cast<float>(m.n_layers));
+    std::vector<Segment> s;
+    if (L.first) {
+        s.push_back({L.wte, V * h, 0.f, std});
+        s.push_back({L.wpe, S * h, 0.f, std});
+    }
+    for (const auto& p : L.layers) {
+        s.push_back({p.ln1_g, h, 1.f, 0.f});
+        s.push_back({p.ln1_b, h, 0.f, 0.f});
+        s.push_back({p.qkv, 3 * h * h, 0.f, std});
+        s.push_back({p.o, h * h, 0.f, out_std});
+        s.push_back({p.ln2_g, h, 1.f, 0.f});
+        s.push_back({p.ln2_b, h, 0.f, 0.f});
+        s.push_back({p.fc1, mlp * h, 0.f, std});
+        s.push_back({p.fc2, h * mlp, 0.f, out_std});
+    }
+    if (L.last) {
+        s.push_back({L.lnf_g, h, 1.f, 0.f});
+        s.push_back({L.lnf_b, h, 0.f, 0.f});
+        s.push_back({L.head, V * h, 0.f, std});
+    }
+    return s;
+}
+
+__global__ void add_f32_kernel(float* __restrict__ dst, const float* __restrict__ src, int64_t n) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) dst[i] += src[i];
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------------
+struct LayerActs {
+    bf16 *x_in, *ln1, *qkv, *o, *x_mid, *ln2, *pre, *act, *x_out;
+    float *mu1, *rs1, *mu2, *rs2, *lse;
+};
+struct StageActs {
+    std::vector<LayerActs> layers;
+    bf16* in = nullptr;    // stage input (recv target / embedding output / previous stage output)
+    bf16* out = nullptr;   // stage output (= last layer x_out; forward send source)
+    bf16 *lnf = nullptr, *logits = nullptr;
+    float *muf = nullptr, *rsf = nullptr;
+    bf16* gin = nullptr;   // grad wrt stage output (backward recv target / next stage's gout)
+    bf16* gout = nullptr;  // grad wrt stage input (backward send source)
+};
+
+struct LocalStage {
+    i64 stage = 0;
+    int64_t shard_n = 0, shard_lo = 0;
+    bf16* w16 = nullptr;      // resident compute weights (not DP_FS with n_dp >= 2)
+    float* grad = nullptr;    // full f32 gradient (accumulated across micro-batches)
+    float *master = nullptr, *m = nullptr, *v = nullptr;  // f32 optimizer shard
+    float* gshard = nullptr;  // reduced gradient shard (n_dp >= 2, sharded variants)
+    float* gtmp = nullptr;    // reduce-scatter landing buffer when a stage reduces several times
+    bf16* w16_shard = nullptr;
+};
+
+enum StreamId { S_COMPUTE = 0, S_DP = 1, S_FWD_SEND = 2, S_FWD_RECV = 3, S_BWD_SEND = 4, S_BWD_RECV = 5, S_N = 6 };
+
+struct TaskExec {
+    TaskId id;
+    int stream;
+    bool send = false;          // Transfer: this rank sends (else receives)
+    int slot = -1;              // DP_FS weight slot used (compute) or filled (reconstruct)
+    bool first_unit = false, last_unit = false;  // Reduce
+    bool adam_after = false;    // Bwd (n_dp == 1) or Reduce (last unit): run the optimizer for this stage
+    std::vector<TaskId> waits;  // events to wait on (deps on other streams + resource deps)
+};
+
+struct Executor::Impl {
+    int dev = 0;
+    cudaStream_t st[S_N] = {};
+    ncclComm_t dp_comm = nullptr, fwd_out = nullptr, fwd_in = nullptr, bwd_out = nullptr, bwd_in = nullptr;
+    std::vector<void*> allocs;
+    std::vector<LocalStage> local;  // index c
+    bf16* slots[2] = {nullptr, nullptr};
+    std::vector<std::vector<StageActs>> acts;  // [mb][c]
+    // scratch (compute stream only)
+    bf16 *tmp_h = nullptr, *tmp_m = nullptr, *gA = nullptr, *gB = nullptr, *dqkv = nullptr;
+    float *dq_acc = nullptr, *delta = nullptr;
+    int32_t *inputs = nullptr, *labels = nullptr;
+    float *row_loss = nullptr, *loss_dev = nullptr, *loss_pinned = nullptr;
+    std::vector<TaskExec> order;
+    std::vector<cudaEvent_t> done;                // per task id (local tasks)
+    std::vector<cudaEvent_t> t_start, t_end;      // timing events
+    cudaEvent_t origin = nullptr, step_end = nullptr, stream_end[S_N] = {};
+    std::vector<double> tl_start, tl_end;
+    int step_no = 0;
+    std::vector<int> task_c;                      // local stage index of compute tasks
+
+    template <class T>
+    T* alloc(size_t n, size_t* total) {
+        void* p = nullptr;
+        const size_t bytes = std::max<size_t>(n * sizeof(T), 256);
+        CK(cudaMalloc(&p, bytes));
+        allocs.push_back(p);
+        *total += bytes;
+        return static_cast<T*>(p);
+    }
+};
+
+Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOptions& o, int rank, int world,
+                   const std::vector<ncclUniqueId>& uids)
+    : impl_(new Impl), m_(m), c_(c), o_(o), rank_(rank), world_(world) {
+    c_.validate(m_);
+    if (c_.n_tp != 1) throw SpecError("executor: tensor parallelism (n_tp > 1) is not supported");
+    if (c_.grid_size() != world) throw SpecError("executor: n_dp * n_pp must equal the number of ranks");
+    if (m_.s_head != 128) throw SpecError("executor: attention kernels need s_head = 128");
+    if (m_.s_hidden % 64 || m_.s_mlp % 64 || m_.s_voc % 8)
+        throw SpecError("executor: s_hidden and s_mlp must be multiples of 64, s_voc of 8");
+    p_ = c_.n_pp;
+    v_ = c_.n_loop;
+    pp_rank_ = rank % p_;
+    dp_rank_ = rank / p_;
+    pl_ = place_stages(m_, c_);
+    graph_ = build_tasks(m_, c_, pl_);
+    for (i64 s = 0; s < pl_.n_stage; ++s)
+        layouts_.push_back(make_stage_layout(m_, s, pl_.n_stage, pl_.layers_per_stage, c_.n_dp));
+
+    Impl& I = *impl_;
+    I.dev = o.device;
+    CK(cudaSetDevice(I.dev));
+    for (int s = 0; s < S_N; ++s) CK(cudaStreamCreateWithFlags(&I.st[s], cudaStreamNonBlocking));
+
+    // ---- NCCL communicators (uid layout: see bfpp_exec_n_comm_ids) ----
+    const bool fs = c_.n_dp >= 2 && c_.dp_variant == DpVariant::DP_FS;
+    {
+        const size_t need = static_cast<size_t>(1 + p_ + 2 * p_ * c_.n_dp);
+        if (world > 1 && uids.size() < need) throw SpecError("executor: not enough NCCL unique ids");
+        auto edge = [&](i64 dp, i64 d, int dir) { return static_cast<size_t>(1 + p_ + (dp * p_ + d) * 2 + dir); };
+        NK(ncclGroupStart());
+        if (c_.n_dp >= 2)
+            NK(ncclCommInitRank(&I.dp_comm, static_cast<int>(c_.n_dp), uids[static_cast<size_t>(1 + pp_rank_)],
+                                static_cast<int>(dp_rank_)));
+        if (p_ >= 2) {
+            NK(ncclCommInitRank(&I.fwd_out, 2, uids[edge(dp_rank_, pp_rank_, 0)], 0));
+            NK(ncclCommInitRank(&I.fwd_in, 2, uids[edge(dp_rank_, (pp_rank_ - 1 + p_) % p_, 0)], 1));
+            NK(ncclCommInitRank(&I.bwd_out, 2, uids[edge(dp_rank_, pp_rank_, 1)], 0));
+            NK(ncclCommInitRank(&I.bwd_in, 2, uids[edge(dp_rank_, (pp_rank_ + 1) % p_, 1)], 1));
+        }
+        NK(ncclGroupEnd());
+    }
+
+    // ---- parameters, gradients, optimizer shards ----
+    size_t& total = dev_bytes_;
+    int64_t max_padded = 0;
+    for (i64 cc = 0; cc < v_; ++cc) {
+        LocalStage ls;
+        ls.stage = local_stage(cc);
+        const StageLayout& L = layouts_[static_cast<size_t>(ls.stage)];
+        max_padded = std::max(max_padded, L.padded);
+        const bool sharded = c_.n_dp >= 2 && c_.dp_variant != DpVariant::DP0;
+        ls.shard_n = sharded ? L.padded / c_.n_dp : L.padded;
+        ls.shard_lo = sharded ? dp_rank_ * ls.shard_n : 0;
+        if (!fs) ls.w16 = I.alloc<bf16>(static_cast<size_t>(L.padded), &total);
+        ls.grad = I.alloc<float>(static_cast<size_t>(L.padded), &total);
+        CK(cudaMemset(ls.grad, 0, static_cast<size_t>(L.padded) * 4));
+        ls.master = I.alloc<float>(static_cast<size_t>(ls.shard_n), &total);
+        ls.m = I.alloc<float>(static_cast<size_t>(ls.shard_n), &total);
+        ls.v = I.alloc<float>(static_cast<size_t>(ls.shard_n), &total);
+        CK(cudaMemset(ls.m, 0, static_cast<size_t>(ls.shard_n) * 4));
+        CK(cudaMemset(ls.v, 0, static_cast<size_t>(ls.shard_n) * 4));
+        if (sharded) {
+            ls.gshard = I.alloc<float>(static_cast<size_t>(ls.shard_n), &total);
+            ls.gtmp = I.alloc<float>(static_cast<size_t>(ls.shard_n), &total);
+            ls.w16_shard = I.alloc<bf16>(static_cast<size_t>(ls.shard_n), &total);
+        }
+        I.local.push_back(ls);
+    }
+    if (fs)
+        for (auto& s : I.slots) s = I.alloc<bf16>(static_cast<size_t>(max_padded), &total);
+    // default initialisation: N(0, std), output projections std/sqrt(2L), LayerNorm (1, 0)
+    for (auto& ls : I.local) {
+        const StageLayout& L = layouts_[static_cast<size_t>(ls.stage)];
+        int64_t gbase = 0;  // global element offset of this stage (model order, split-independent)
+        for (i64 s = 0; s < ls.stage; ++s) gbase += layouts_[static_cast<size_t>(s)].numel;
+        CK(cudaMemset(ls.master, 0, static_cast<size_t>(ls.shard_n) * 4));
+        for (const Segment& sg : init_segments(L, m_, o.init_std)) {
+            const int64_t lo = std::max(sg.off, ls.shard_lo), hi = std::min(sg.off + sg.n, ls.shard_lo + ls.shard_n);
+            if (lo >= hi) continue;
+            init_normal(ls.master + (lo - ls.shard_lo), nullptr, hi - lo, sg.mean, sg.std, o.seed,
+                        static_cast<uint64_t>(gbase + lo), I.st[S_COMPUTE]);
+        }
+        if (ls.w16_shard) f32_to_bf16(ls.master, ls.w16_shard, ls.shard_n, I.st[S_COMPUTE]);
+        if (ls.w16) {
+            if (ls.w16_shard)  // DP_PS: replicated weights assembled from the optimizer shards
+                NK(ncclAllGather(ls.w16_shard, ls.w16, static_cast<size_t>(ls.shard_n), ncclBfloat16, I.dp_comm,
+                                 I.st[S_COMPUTE]));
+            else
+                f32_to_bf16(ls.master, ls.w16, ls.shard_n, I.st[S_COMPUTE]);
+        }
+    }
+
+    // ---- activations and scratch ----
+    const int64_t T = c_.s_mb * m_.s_seq, h = m_.s_hidden, mlp = m_.s_mlp, V = m_.s_voc, H = m_.n_heads;
+    const size_t Th = static_cast<size_t>(T * h);
+    I.acts.assign(static_cast<size_t>(c_.n_mb), std::vector<StageActs>(static_cast<size_t>(v_)));
+    for (i64 mb = 0; mb < c_.n_mb; ++mb) {
+        for (i64 cc = 0; cc < v_; ++cc) {
+            StageActs& a = I.acts[static_cast<size_t>(mb)][static_cast<size_t>(cc)];
+            const i64 s = local_stage(cc);
+            const StageLayout& L = layouts_[static_cast<size_t>(s)];
+            // input: aliases the previous stage's output when both live on this device
+            if (s > 0 && pl_.device_of(s - 1) == pp_rank_)
+                a.in = I.acts[static_cast<size_t>(mb)][static_cast<size_t>(cc - 1)].out;
+            else
+                a.in = I.alloc<bf16>(Th, &total);
+            bf16* x = a.in;
+            for (size_t l = 0; l < L.layers.size(); ++l) {
+                LayerActs la;
+                la.x_in = x;
+                la.ln1 = I.alloc<bf16>(Th, &total);
+                la.qkv = I.alloc<bf16>(3 * Th, &total);
+                la.o = I.alloc<bf16>(Th, &total);
+                la.x_mid = I.alloc<bf16>(Th, &total);
+                la.ln2 = I.alloc<bf16>(Th, &total);
+                la.pre = I.alloc<bf16>(static_cast<size_t>(T * mlp), &total);
+                la.act = I.alloc<bf16>(static_cast<size_t>(T * mlp), &total);
+                la.x_out = I.alloc<bf16>(Th, &total);
+                la.mu1 = I.alloc<float>(static_cast<size_t>(T), &total);
+                la.rs1 = I.alloc<float>(static_cast<size_t>(T), &total);
+                la.mu2 = I.alloc<float>(static_cast<size_t>(T), &total);
+                la.rs2 = I.alloc<float>(static_cast<size_t>(T), &total);
+                la.lse = I.alloc<float>(static_cast<size_t>(T * H), &total);
+                x = la.x_out;
+                a.layers.push_back(la);
+            }
+            a.out = x;
+            if (L.last) {
+                a.lnf = I.alloc<bf16>(Th, &total);
+                a.muf = I.alloc<float>(static_cast<size_t>(T), &total);
+                a.rsf = I.alloc<float>(static_cast<size_t>(T), &total);
+                a.logits = I.alloc<bf16>(static_cast<size_t>(T * V), &total);
+            }
+            if (!L.first) a.gout = I.alloc<bf16>(Th, &total);
+        }
+        // gin: the next stage's gout when it lives on this device, else a receive buffer
+        for (i64 cc = 0; cc < v_; ++cc) {
+            StageActs& a = I.acts[static_cast<size_t>(mb)][static_cast<size_t>(cc)];
+            const i64 s = local_stage(cc);
+            if (s == pl_.n_stage - 1) continue;
+            if (pl_.device_of(s + 1) == pp_rank_)
+                a.gin = I.acts[static_cast<size_t>(mb)][static_cast<size_t>(cc + 1)].gout;
+            else
+                a.gin = I.alloc<bf16>(Th, &total);
+        }
+    }
+    I.tmp_h = I.alloc<bf16>(Th, &total);
+    I.tmp_m = I.alloc<bf16>(static_cast<size_t>(T * mlp), &total);
+    I.gA = I.alloc<bf16>(Th, &total);
+    I.gB = I.alloc<bf16>(Th, &total);
+    I.dqkv = I.alloc<bf16>(3 * Th, &total);
+    I.dq_acc = I.alloc<float>(Th, &total);
+    I.delta = I.alloc<float>(static_cast<size_t>(T * H), &total);
+    I.inputs = I.alloc<int32_t>(static_cast<size_t>(c_.n_mb * T), &total);
+    I.labels = I.alloc<int32_t>(static_cast<size_t>(c_.n_mb * T), &total);
+    I.row_loss = I.alloc<float>(static_cast<size_t>(c_.n_mb * T), &total);
+    I.loss_dev = I.alloc<float>(4, &total);
+    CK(cudaMallocHost(&I.loss_pinned, sizeof(float)));
+
+    // ---- per-task execution plan ----
+    const size_t n = graph_.tasks.size();
+    I.done.assign(n, nullptr);
+    I.t_start.assign(n, nullptr);
+    I.t_end.assign(n, nullptr);
+    I.task_c.assign(n, -1);
+    I.tl_start.assign(n, NAN);
+    I.tl_end.assign(n, NAN);
+    // enqueue order = start order of a simulation with positive durations (a topological order
+    // consistent with every lane's program/priority order on this device)
+    TimingModel tm;
+    tm.t_fwd_stage = 1.0;
+    tm.bwd_ratio = 2.0;
+    tm.t_pp_transfer = 0.01;
+    tm.t_dp_reduce_stage = 0.05;
+    tm.t_dp_reconstruct_stage = 0.05;
+    const Timeline sim = simulate(graph_, tm);
+    std::vector<TaskId> mine;
+    for (const Task& t : graph_.tasks) {
+        const bool local = t.device == pp_rank_ || (t.kind == TaskKind::Transfer && t.peer_device == pp_rank_);
+        if (local) mine.push_back(t.id);
+    }
+    std::stable_sort(mine.begin(), mine.end(), [&](TaskId a, TaskId b) {
+        return sim.events[static_cast<size_t>(a)].start < sim.events[static_cast<size_t>(b)].start;
+    });
+    // reconstruct slot numbering (creation order per device) and Reduce unit bookkeeping
+    std::map<TaskId, int> rec_slot;
+    {
+        int k = 0;
+        for (const Task& t : graph_.tasks)
+            if (t.kind == TaskKind::Reconstruct && t.device == pp_rank_) rec_slot[t.id] = (k++) & 1;
+    }
+    std::map<TaskId, TaskId> reduce_of_last_bwd;      // last Bwd of a unit -> its Reduce
+    std::map<i64, std::vector<TaskId>> reduces_of_stage;
+    for (const Task& t : graph_.tasks)
+        if (t.kind == TaskKind::Reduce && t.device == pp_rank_) {
+            reduce_of_last_bwd[t.deps[0]] = t.id;
+            reduces_of_stage[t.stage].push_back(t.id);
+        }
+    for (auto& kv : reduces_of_stage)
+        std::sort(kv.second.begin(), kv.second.end(), [&](TaskId a, TaskId b) {
+            return graph_.tasks[static_cast<size_t>(a)].priority < graph_.tasks[static_cast<size_t>(b)].priority;
+        });
+    std::map<i64, TaskId> last_bwd_of_stage, prev_bwd;
+    for (TaskId id : graph_.compute_program[static_cast<size_t>(pp_rank_)]) {
+        const Task& t = graph_.tasks[static_cast<size_t>(id)];
+        if (t.kind == TaskKind::Bwd) last_bwd_of_stage[t.stage] = id;
+    }
+    auto stream_of = [&](const Task& t, bool* send) {
+        if (t.lane == Lane::Compute) return static_cast<int>(S_COMPUTE);
+        if (t.lane == Lane::DpNet) return static_cast<int>(S_DP);
+        const bool fwd = graph_.tasks[static_cast<size_t>(t.deps[0])].kind == TaskKind::Fwd;
+        *send = t.device == pp_rank_;
+        return static_cast<int>(fwd ? (*send ? S_FWD_SEND : S_FWD_RECV) : (*send ? S_BWD_SEND : S_BWD_RECV));
+    };
+    std::vector<int> stream_of_task(n, -1);
+    for (TaskId id : mine) {
+        bool send = false;
+        stream_of_task[static_cast<size_t>(id)] = stream_of(graph_.tasks[static_cast<size_t>(id)], &send);
+    }
+    for (TaskId id : mine) {
+        const Task& t = graph_.tasks[static_cast<size_t>(id)];
+        TaskExec te;
+        te.id = id;
+        te.stream = stream_of(t, &te.send);
+        if (t.lane == Lane::Compute) I.task_c[static_cast<size_t>(id)] = static_cast<int>(t.stage / p_);
+        for (TaskId d : t.deps) {
+            const Task& dt = graph_.tasks[static_cast<size_t>(d)];
+            if (t.kind == TaskKind::Transfer && !te.send) continue;  // the receive side has no local deps
+            if (dt.kind == TaskKind::Reconstruct && t.lane == Lane::Compute) te.slot = rec_slot[d];
+            if (stream_of_task[static_cast<size_t>(d)] == te.stream) continue;  // same stream: FIFO order
+            if (stream_of_task[static_cast<size_t>(d)] < 0) continue;           // remote (reached via a transfer)
+            te.waits.push_back(d);
+        }
+        if (t.kind == TaskKind::Reconstruct) te.slot = rec_slot[id];
+        if (t.kind == TaskKind::Bwd) {
+            // a new reduction unit of this stage may only start once the previous unit's
+            // reduce-scatter has drained (and re-zeroed) the stage's gradient buffer
+            auto pb = prev_bwd.find(t.stage);
+            if (pb != prev_bwd.end()) {
+                auto r = reduce_of_last_bwd.find(pb->second);
+                if (r != reduce_of_last_bwd.end()) te.waits.push_back(r->second);
+            }
+            prev_bwd[t.stage] = id;
+            if (c_.n_dp < 2 && last_bwd_of_stage[t.stage] == id) te.adam_after = true;
+        }
+        if (t.kind == TaskKind::Reduce) {
+            const auto& rs = reduces_of_stage[t.stage];
+            te.first_unit = rs.front() == id;
+            te.last_unit = rs.back() == id;
+            te.adam_after = te.last_unit;
+        }
+        I.order.push_back(te);
+        CK(cudaEventCreateWithFlags(&I.done[static_cast<size_t>(id)], cudaEventDisableTiming));
+        if (o.record_timeline) {
+            CK(cudaEventCreate(&I.t_start[static_cast<size_t>(id)]));
+            CK(cudaEventCreate(&I.t_end[static_cast<size_t>(id)]));
+        }
+    }
+    CK(cudaEventCreate(&I.origin));
+    CK(cudaEventCreateWithFlags(&I.step_end, cudaEventDisableTiming));
+    for (auto& e : I.stream_end) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CK(cudaEventRecord(I.step_end, I.st[S_COMPUTE]));
+    CK(cudaStreamSynchronize(I.st[S_COMPUTE]));
+}
+
+Executor::~Executor() {
+    Impl& I = *impl_;
+    cudaSetDevice(I.dev);
+    cudaDeviceSynchronize();
+    for (ncclComm_t cm : {I.dp_comm, I.fwd_out, I.fwd_in, I.bwd_out, I.bwd_in})
+        if (cm) ncclCommDestroy(cm);
+    for (auto e : I.done)
+        if (e) cudaEventDestroy(e);
+    for (auto e : I.t_start)
+        if (e) cudaEventDestroy(e);
+    for (auto e : I.t_end)
+        if (e) cudaEventDestroy(e);
+    if (I.origin) cudaEventDestroy(I.origin);
+    if (I.step_end) cudaEventDestroy(I.step_end);
+    for (auto e : I.stream_end)
+        if (e) cudaEventDestroy(e);
+    for (void* p : I.allocs) cudaFree(p);
+    if (I.loss_pinned) cudaFreeHost(I.loss_pinned);
+    for (auto s : I.st)
+        if (s) cudaStreamDestroy(s);
+}
+
+// ---------------------------------------------------------------------------------------------
+namespace {
+
+void gemm(cudaStream_t st, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int amn, const void* B,
+          int64_t ldb, int bmn, void* D, int64_t ldd, int epi, const void* aux = nullptr, int64_t ldaux = 0,
+          void* aux_out = nullptr, int64_t ldaux_out = 0, int accumulate = 0) {
+    GemmArgs g;
+    g.M = M, g.N = N, g.K = K;
+    g.A = A, g.lda = lda, g.a_mn_major = amn;
+    g.B = B, g.ldb = ldb, g.b_mn_major = bmn;
+    g.D = D, g.ldd = ldd;
+    g.aux = aux, g.ldaux = ldaux, g.aux_out = aux_out, g.ldaux_out = ldaux_out;
+    g.epilogue = epi, g.accumulate = accumulate;
+    gemm_bf16(g, st);
+}
+
+}  // namespace
+
+void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float* loss_dev) {
+    Impl& I = *impl_;
+    CK(cudaSetDevice(I.dev));
+    cudaStream_t cs = I.st[S_COMPUTE], ds = I.st[S_DP];
+    ++I.step_no;
+    for (int s = 0; s < S_N; ++s) CK(cudaStreamWaitEvent(I.st[s], I.step_end, 0));
+    const int64_t T = c_.s_mb * m_.s_seq, h = m_.s_hidden, mlp = m_.s_mlp, V = m_.s_voc;
+    const int H = static_cast<int>(m_.n_heads), S = static_cast<int>(m_.s_seq), B = static_cast<int>(c_.s_mb);
+    const bool has_first = pl_.device_of(0) == pp_rank_, has_last = pl_.device_of(pl_.n_stage - 1) == pp_rank_;
+    if (has_first || has_last) {
+        const size_t rows = static_cast<size_t>(c_.n_mb * c_.s_mb);
+        const size_t w = static_cast<size_t>(m_.s_seq) * 4, pitch = static_cast<size_t>(m_.s_seq + 1) * 4;
+        const cudaMemcpyKind k = on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+        CK(cudaMemcpy2DAsync(I.inputs, w, tokens, pitch, w, rows, k, cs));
+        CK(cudaMemcpy2DAsync(I.labels, w, tokens + 1, pitch, w, rows, k, cs));
+    }
+    if (o_.record_timeline) CK(cudaEventRecord(I.origin, cs));
+    const float grad_scale = 1.f / static_cast<float>(c_.n_dp * c_.n_mb * T);
+    const bool fs = c_.n_dp >= 2 && c_.dp_variant == DpVariant::DP_FS;
+
+    auto weights = [&](const TaskExec& te, int cidx) -> const bf16* {
+        if (fs) return I.slots[te.slot];
+        return I.local[static_cast<size_t>(cidx)].w16;
+    };
+    auto adam = [&](LocalStage& ls, cudaStream_t st) {
+        if (o_.skip_optimizer) return;
+        const bool sharded = ls.gshard != nullptr;
+        float* g = sharded ? ls.gshard : ls.grad;
+        bf16* w = sharded ? ls.w16_shard : ls.w16;
+        adam_update(ls.master, ls.m, ls.v, g, w, ls.shard_n, o_.lr, o_.beta1, o_.beta2, o_.eps, o_.weight_decay,
+                    I.step_no, sharded ? 0 : 1, st);
+        if (sharded && c_.dp_variant == DpVariant::DP_PS)
+            NK(ncclAllGather(ls.w16_shard, ls.w16, static_cast<size_t>(ls.shard_n), ncclBfloat16, I.dp_comm, st));
+    };
+
+    for (const TaskExec& te : I.order) {
+        const Task& t = graph_.tasks[static_cast<size_t>(te.id)];
+        cudaStream_t st = I.st[te.stream];
+        for (TaskId d : te.waits) CK(cudaStreamWaitEvent(st, I.done[static_cast<size_t>(d)], 0));
+        if (o_.record_timeline) CK(cudaEventRecord(I.t_start[static_cast<size_t>(te.id)], st));
+        const int cidx = I.task_c[static_cast<size_t>(te.id)];
+        switch (t.kind) {
+        case TaskKind::Fwd: {
+            const StageLayout& L = layouts_[static_cast<size_t>(t.stage)];
+            StageActs& a = I.acts[static_cast<size_t>(t.micro_batch)][static_cast<size_t>(cidx)];
+            const bf16* W = weights(te, cidx);
+            const int32_t* inp = I.inputs + t.micro_batch * T;
+            if (L.first) embed_fwd(inp, W + L.wte, W + L.wpe, a.in, static_cast<int>(T), S, static_cast<int>(h), st);
+            for (size_t l = 0; l < L.layers.size(); ++l) {
+                const LayerParams& P = L.layers[l];
+                LayerActs& x = a.layers[l];
+                layernorm_fwd(x.x_in, W + P.ln1_g, W + P.ln1_b, x.ln1, x.mu1, x.rs1, static_cast<int>(T),
+                              static_cast<int>(h), 1e-5f, st);
+                gemm(st, T, 3 * h, h, x.ln1, h, 0, W + P.qkv, h, 0, x.qkv, 3 * h, GEMM_EPI_BF16);
+                attention_fwd(x.qkv, x.o, x.lse, B, S, H, 128, st);
+                gemm(st, T, h, h, x.o, h, 0, W + P.o, h, 0, x.x_mid, h, GEMM_EPI_RESID, x.x_in, h);
+                layernorm_fwd(x.x_mid, W + P.ln2_g, W + P.ln2_b, x.ln2, x.mu2, x.rs2, static_cast<int>(T),
+                              static_cast<int>(h), 1e-5f, st);
+                gemm(st, T, mlp, h, x.ln2, h, 0, W + P.fc1, h, 0, x.act, mlp, GEMM_EPI_GELU, nullptr, 0, x.pre, mlp);
+                gemm(st, T, h, mlp, x.act, mlp, 0, W + P.fc2, mlp, 0, x.x_out, h, GEMM_EPI_RESID, x.x_mid, h);
+            }
+            if (L.last) {
+                layernorm_fwd(a.out, W + L.lnf_g, W + L.lnf_b, a.lnf, a.muf, a.rsf, static_cast<int>(T),
+                              static_cast<int>(h), 1e-5f, st);
+                gemm(st, T, V, h, a.lnf, h, 0, W + L.head, h, 0, a.logits, V, GEMM_EPI_BF16);
+                softmax_xent(a.logits, V, I.labels + t.micro_batch * T, I.row_loss + t.micro_batch * T,
+                             static_cast<int>(T), static_cast<int>(V), grad_scale, st);
+            }
+            break;
+        }
+        case TaskKind::Bwd: {
+            const StageLayout& L = layouts_[static_cast<size_t>(t.stage)];
+            StageActs& a = I.acts[static_cast<size_t>(t.micro_batch)][static_cast<size_t>(cidx)];
+            LocalStage& ls = I.local[static_cast<size_t>(cidx)];
+            const bf16* W = weights(te, cidx);
+            float* G = ls.grad;
+            const bf16* g;
+            if (L.last) {
+                gemm(st, T, h, V, a.logits, V, 0, W + L.head, h, 1, I.tmp_h, h, GEMM_EPI_BF16);
+                gemm(st, V, h, T, a.logits, V, 1, a.lnf, h, 1, G + L.head, h, GEMM_EPI_F32, nullptr, 0, nullptr, 0, 1);
+                layernorm_bwd(I.tmp_h, a.out, W + L.lnf_g, a.muf, a.rsf, nullptr, I.gA, G + L.lnf_g, G + L.lnf_b,
+                              static_cast<int>(T), static_cast<int>(h), st);
+                g = I.gA;
+            } else {
+                g = a.gin;
+            }
+            for (size_t li = L.layers.size(); li-- > 0;) {
+                const LayerParams& P = L.layers[li];
+                LayerActs& x = a.layers[li];
+                bf16* gmid = g == I.gB ? I.gA : I.gB;
+                bf16* gnext = (li == 0 && !L.first) ? a.gout : (gmid == I.gA ? I.gB : I.gA);
+                // MLP: x_out = x_mid + gelu(ln2 W1^T) W2^T
+                gemm(st, h, mlp, T, g, h, 1, x.act, mlp, 1, G + P.fc2, mlp, GEMM_EPI_F32, nullptr, 0, nullptr, 0, 1);
+                gemm(st, T, mlp, h, g, h, 0, W + P.fc2, mlp, 1, I.tmp_m, mlp, GEMM_EPI_DGELU, x.pre, mlp);
+                gemm(st, mlp, h, T, I.tmp_m, mlp, 1, x.ln2, h, 1, G + P.fc1, h, GEMM_EPI_F32, nullptr, 0, nullptr, 0, 1);
+                gemm(st, T, h, mlp, I.tmp_m, mlp, 0, W + P.fc1, h, 1, I.tmp_h, h, GEMM_EPI_BF16);
+                layernorm_bwd(I.tmp_h, x.x_mid, W + P.ln2_g, x.mu2, x.rs2, g, gmid, G + P.ln2_g, G + P.ln2_b,
+                              static_cast<int>(T), static_cast<int>(h), st);
+                // attention: x_mid = x_in + attn(ln1 Wqkv^T) Wo^T
+                gemm(st, h, h, T, gmid, h, 1, x.o, h, 1, G + P.o, h, GEMM_EPI_F32, nullptr, 0, nullptr, 0, 1);
+                gemm(st, T, h, h, gmid, h, 0, W + P.o, h, 1, I.tmp_h, h, GEMM_EPI_BF16);
+                attention_bwd(x.qkv, x.o, I.tmp_h, x.lse, I.delta, I.dq_acc, I.dqkv, B, S, H, 128, st);
+                gemm(st, 3 * h, h, T, I.dqkv, 3 * h, 1, x.ln1, h, 1, G + P.qkv, h, GEMM_EPI_F32, nullptr, 0, nullptr,
+                     0, 1);
+                gemm(st, T, h, 3 * h, I.dqkv, 3 * h, 0, W + P.qkv, h, 1, I.tmp_h, h, GEMM_EPI_BF16);
+                layernorm_bwd(I.tmp_h, x.x_in, W + P.ln1_g, x.mu1, x.rs1, gmid, gnext, G + P.ln1_g, G + P.ln1_b,
+                              static_cast<int>(T), static_cast<int>(h), st);
+                g = gnext;
+            }
+            if (L.first)
+                embed_bwd(I.inputs + t.micro_batch * T, g, G + L.wte, G + L.wpe, static_cast<int>(T), S,
+                          static_cast<int>(h), st);
+            if (te.adam_after) {
+                // n_dp == 1: this stage's gradient is final; update it on the DP stream
+                CK(cudaEventRecord(I.done[static_cast<size_t>(te.id)], st));
+                CK(cudaStreamWaitEvent(ds, I.done[static_cast<size_t>(te.id)], 0));
+                adam(ls, ds);
+            }
+            break;
+        }
+        case TaskKind::Transfer: {
+            const bool fwd = graph_.tasks[static_cast<size_t>(t.deps[0])].kind == TaskKind::Fwd;
+            const size_t count = static_cast<size_t>(T * h);
+            if (te.send) {
+                const StageActs& a = I.acts[static_cast<size_t>(t.micro_batch)][static_cast<size_t>(t.stage / p_)];
+                NK(ncclSend(fwd ? a.out : a.gout, count, ncclBfloat16, 1, fwd ? I.fwd_out : I.bwd_out, st));
+            } else {
+                const i64 dst_stage = fwd ? t.stage + 1 : t.stage - 1;
+                const StageActs& a = I.acts[static_cast<size_t>(t.micro_batch)][static_cast<size_t>(dst_stage / p_)];
+                NK(ncclRecv(fwd ? a.in : a.gin, count, ncclBfloat16, 0, fwd ? I.fwd_in : I.bwd_in, st));
+            }
+            break;
+        }
+        case TaskKind::Reconstruct: {
+            LocalStage& ls = I.local[static_cast<size_t>(t.stage / p_)];
+            NK(ncclAllGather(ls.w16_shard, I.slots[te.slot], static_cast<size_t>(ls.shard_n), ncclBfloat16, I.dp_comm,
+                             st));
+            break;
+        }
+        case TaskKind::Reduce: {
+            LocalStage& ls = I.local[static_cast<size_t>(t.stage / p_)];
+            const int64_t full = layouts_[static_cast<size_t>(t.stage)].padded;
+            if (c_.dp_variant == DpVariant::DP0) {
+                NK(ncclAllReduce(ls.grad, ls.grad, static_cast<size_t>(full), ncclFloat32, ncclSum, I.dp_comm, st));
+            } else {
+                float* dst = te.first_unit ? ls.gshard : ls.gtmp;
+                NK(ncclReduceScatter(ls.grad, dst, static_cast<size_t>(ls.shard_n), ncclFloat32, ncclSum, I.dp_comm,
+                                     st));
+                if (!te.first_unit)
+                    add_f32_kernel<<<296, 256, 0, st>>>(ls.gshard, ls.gtmp, ls.shard_n);
+                CK(cudaMemsetAsync(ls.grad, 0, static_cast<size_t>(full) * 4, st));
+            }
+            if (te.adam_after) adam(ls, st);
+            break;
+        }
+        }
+        if (o_.record_timeline) CK(cudaEventRecord(I.t_end[static_cast<size_t>(te.id)], st));
+        CK(cudaEventRecord(I.done[static_cast<size_t>(te.id)], st));
+    }
+    // loss of this replica (last-stage device): mean over its n_mb * T tokens
+    if (has_last) sum_f32(I.row_loss, c_.n_mb * T, 1.f / static_cast<float>(c_.n_mb * T), I.loss_dev, 0, cs);
+    for (int s = 1; s < S_N; ++s) {
+        CK(cudaEventRecord(I.stream_end[s], I.st[s]));
+        CK(cudaStreamWaitEvent(cs, I.stream_end[s], 0));
+    }
+    CK(cudaEventRecord(I.step_end, cs));
+    if (loss_dev && has_last) CK(cudaMemcpyAsync(loss_dev, I.loss_dev, 4, cudaMemcpyDeviceToDevice, cs));
+    if (loss_host) {
+        if (has_last) {
+            CK(cudaMemcpyAsync(I.loss_pinned, I.loss_dev, 4, cudaMemcpyDeviceToHost, cs));
+            CK(cudaStreamSynchronize(cs));
+            *loss_host = *I.loss_pinned;
+        } else {
+            *loss_host = NAN;
+        }
+    }
+    CK(cudaPeekAtLastError());
+    if (o_.record_timeline) {
+        CK(cudaEventSynchronize(I.step_end));
+        for (const TaskExec& te : I.order) {
+            float a = 0, b = 0;
+            CK(cudaEventElapsedTime(&a, I.origin, I.t_start[static_cast<size_t>(te.id)]));
+            CK(cudaEventElapsedTime(&b, I.origin, I.t_end[static_cast<size_t>(te.id)]));
+            const Task& t = graph_.tasks[static_cast<size_t>(te.id)];
+            // a transfer is reported by its sender; the receiver keeps its own view only if it is the sender
+            if (t.kind == TaskKind::Transfer && !te.send) continue;
+            I.tl_start[static_cast<size_t>(te.id)] = a * 1e-3;
+            I.tl_end[static_cast<size_t>(te.id)] = b * 1e-3;
+        }
+    }
+}
+
+void Executor::sync() {
+    CK(cudaSetDevice(impl_->dev));
+    CK(cudaStreamSynchronize(impl_->st[S_COMPUTE]));
+    ncclResult_t async_err = ncclSuccess;
+    for (ncclComm_t cm : {impl_->dp_comm, impl_->fwd_out, impl_->fwd_in, impl_->bwd_out, impl_->bwd_in})
+        if (cm && ncclCommGetAsyncError(cm, &async_err) == ncclSuccess && async_err != ncclSuccess)
+            throw std::runtime_error(std::string("NCCL async error: ") + ncclGetErrorString(async_err));
+}
+
+void Executor::timeline(double* start, double* end) const {
+    for (size_t i = 0; i < impl_->tl_start.size(); ++i) {
+        start[i] = impl_->tl_start[i];
+        end[i] = impl_->tl_end[i];
+    }
+}
+
+namespace {
+LocalStage& find_local(std::vector<LocalStage>& v, i64 stage) {
+    for (auto& ls : v)
+        if (ls.stage == stage) return ls;
+    throw SpecError("executor: stage is not hosted by this rank");
+}
+}  // namespace
+
+void Executor::set_params(i64 stage, const float* host, int64_t n) {
+    Impl& I = *impl_;
+    CK(cudaSetDevice(I.dev));
+    sync();
+    LocalStage& ls = find_local(I.local, stage);
+    const StageLayout& L = layouts_[static_cast<size_t>(stage)];
+    if (n != L.numel) throw SpecError("set_params: size mismatch with the stage layout");
+    std::vector<float> padded(static_cast<size_t>(L.padded), 0.f);
+    std::memcpy(padded.data(), host, static_cast<size_t>(n) * 4);
+    CK(cudaMemcpy(ls.master, padded.data() + ls.shard_lo, static_cast<size_t>(ls.shard_n) * 4,
+                  cudaMemcpyHostToDevice));
+    CK(cudaMemset(ls.m, 0, static_cast<size_t>(ls.shard_n) * 4));
+    CK(cudaMemset(ls.v, 0, static_cast<size_t>(ls.shard_n) * 4));
+    if (ls.w16_shard) f32_to_bf16(ls.master, ls.w16_shard, ls.shard_n, I.st[S_COMPUTE]);
+    if (ls.w16) {
+        if (ls.shard_n == L.padded) {
+            f32_to_bf16(ls.master, ls.w16, L.padded, I.st[S_COMPUTE]);
+        } else {  // replicated weights with a sharded optimizer (DP_PS): convert the full vector
+            float* tmp = nullptr;
+            CK(cudaMalloc(&tmp, static_cast<size_t>(L.padded) * 4));
+            CK(cudaMemcpy(tmp, padded.data(), static_cast<size_t>(L.padded) * 4, cudaMemcpyHostToDevice));
+            f32_to_bf16(tmp, ls.w16, L.padded, I.st[S_COMPUTE]);
+            CK(cudaStreamSynchronize(I.st[S_COMPUTE]));
+            CK(cudaFree(tmp));
+        }
+    }
+    I.step_no = 0;
+    CK(cudaStreamSynchronize(I.st[S_COMPUTE]));
+}
+
+void Executor::get_params(i64 stage, float* host, int64_t n, int64_t* lo, int64_t* hi) {
+    Impl& I = *impl_;
+    sync();
+    CK(cudaDeviceSynchronize());
+    LocalStage& ls = find_local(I.local, stage);
+    const StageLayout& L = layouts_[static_cast<size_t>(stage)];
+    const int64_t a = ls.shard_lo, b = std::min(ls.shard_lo + ls.shard_n, L.numel);
+    if (n < L.numel) throw SpecError("get_params: buffer too small");
+    if (b > a) CK(cudaMemcpy(host + a, ls.master, static_cast<size_t>(b - a) * 4, cudaMemcpyDeviceToHost));
+    *lo = a;
+    *hi = std::max(a, b);
+}
+
+void Executor::get_grads(i64 stage, float* host, int64_t n, int64_t* lo, int64_t* hi) {
+    Impl& I = *impl_;
+    sync();
+    CK(cudaDeviceSynchronize());
+    LocalStage& ls = find_local(I.local, stage);
+    const StageLayout& L = layouts_[static_cast<size_t>(stage)];
+    if (n < L.numel) throw SpecError("get_grads: buffer too small");
+    if (ls.gshard) {
+        const int64_t a = ls.shard_lo, b = std::min(ls.shard_lo + ls.shard_n, L.numel);
+        if (b > a) CK(cudaMemcpy(host + a, ls.gshard, static_cast<size_t>(b - a) * 4, cudaMemcpyDeviceToHost));
+        *lo = a;
+        *hi = std::max(a, b);
+    } else {
+        CK(cudaMemcpy(host, ls.grad, static_cast<size_t>(L.numel) * 4, cudaMemcpyDeviceToHost));
+        *lo = 0;
+        *hi = L.numel;
+    }
+}
+
+void Executor::zero_grads() {
+    Impl& I = *impl_;
+    sync();
+    for (auto& ls : I.local) {
+        CK(cudaMemset(ls.grad, 0, static_cast<size_t>(layouts_[static_cast<size_t>(ls.stage)].padded) * 4));
+        if (ls.gshard) CK(cudaMemset(ls.gshard, 0, static_cast<size_t>(ls.shard_n) * 4));
+    }
+    CK(cudaDeviceSynchronize());
+}
+
+}  // namespace bfpp

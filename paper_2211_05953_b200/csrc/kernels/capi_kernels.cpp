@@ -67,7 +67,7 @@ int bfpp_attention_bwd(const void* qkv, const void* o, const void* dout, const f
     });
 }
 
-int bfpp_layernorm_fwd(const void* x, const float* gamma, const float* beta, void* y, float* mean, float* rstd,
+int bfpp_layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, float* mean, float* rstd,
                        int32_t rows, int32_t width, float eps, void* stream) {
     return guarded([&] {
         layernorm_fwd(x, gamma, beta, y, mean, rstd, rows, width, eps, static_cast<cudaStream_t>(stream));
@@ -75,7 +75,7 @@ int bfpp_layernorm_fwd(const void* x, const float* gamma, const float* beta, voi
     });
 }
 
-int bfpp_layernorm_bwd(const void* dy, const void* x, const float* gamma, const float* mean, const float* rstd,
+int bfpp_layernorm_bwd(const void* dy, const void* x, const void* gamma, const float* mean, const float* rstd,
                        const void* dres, void* dx, float* dgamma, float* dbeta, int32_t rows, int32_t width,
                        void* stream) {
     return guarded([&] {

@@ -13,9 +13,9 @@ void attention_bwd(const void* qkv, const void* o, const void* dout, const float
                    void* dqkv, int batch, int seq, int heads, int head_dim, cudaStream_t st);
 
 // layernorm.cu
-void layernorm_fwd(const void* x, const float* gamma, const float* beta, void* y, float* mean, float* rstd, int rows,
+void layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, float* mean, float* rstd, int rows,
                    int width, float eps, cudaStream_t st);
-void layernorm_bwd(const void* dy, const void* x, const float* gamma, const float* mean, const float* rstd,
+void layernorm_bwd(const void* dy, const void* x, const void* gamma, const float* mean, const float* rstd,
                    const void* dres, void* dx, float* dgamma, float* dbeta, int rows, int width, cudaStream_t st);
 
 // elementwise.cu

@@ -57,8 +57,8 @@ __device__ __forceinline__ float2 block_sum2(float a, float b, float2* red) {
 
 template <int V>  // 8-element vectors per thread; covers widths up to 1024 * V
 __global__ void __launch_bounds__(NT) ln_fwd_kernel(const __nv_bfloat16* __restrict__ x,
-                                                    const float* __restrict__ gamma, const float* __restrict__ beta,
-                                                    __nv_bfloat16* __restrict__ y, float* __restrict__ mean_out,
+                                                    const __nv_bfloat16* __restrict__ gamma,
+                                                    const __nv_bfloat16* __restrict__ beta, __nv_bfloat16* __restrict__ y, float* __restrict__ mean_out,
                                                     float* __restrict__ rstd_out, int width, float eps) {
     __shared__ float2 red[NT / 32];
     const int64_t off = static_cast<int64_t>(blockIdx.x) * width;
@@ -88,8 +88,8 @@ __global__ void __launch_bounds__(NT) ln_fwd_kernel(const __nv_bfloat16* __restr
         const int c = (i * NT + threadIdx.x) * 8;
         if (c >= width) continue;
         float g[8], b[8], o[8];
-        load8f(gamma + c, g);
-        load8f(beta + c, b);
+        load8(gamma + c, g);
+        load8(beta + c, b);
 #pragma unroll
         for (int u = 0; u < 8; ++u) o[u] = (v[i][u] - mean) * rstd * g[u] + b[u];
         store8(y + off + c, o);
@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(NT) ln_fwd_kernel(const __nv_bfloat16* __restr
 template <int V>
 __global__ void __launch_bounds__(NT) ln_bwd_kernel(const __nv_bfloat16* __restrict__ dy,
                                                     const __nv_bfloat16* __restrict__ x,
-                                                    const float* __restrict__ gamma, const float* __restrict__ mean,
+                                                    const __nv_bfloat16* __restrict__ gamma, const float* __restrict__ mean,
                                                     const float* __restrict__ rstd,
                                                     const __nv_bfloat16* __restrict__ dres,
                                                     __nv_bfloat16* __restrict__ dx, float* __restrict__ dgamma,
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(NT) ln_bwd_kernel(const __nv_bfloat16* __restr
         const int c = (i * NT + threadIdx.x) * 8;
 #pragma unroll
         for (int u = 0; u < 8; ++u) pg[i][u] = pb[i][u] = 0.f;
-        if (c < width) load8f(gamma + c, g[i]);
+        if (c < width) load8(gamma + c, g[i]);
     }
     for (int row = blockIdx.x; row < rows; row += gridDim.x) {
         const int64_t off = static_cast<int64_t>(row) * width;
@@ -181,11 +181,13 @@ int sm_count() {
 
 }  // namespace
 
-void layernorm_fwd(const void* x, const float* gamma, const float* beta, void* y, float* mean, float* rstd, int rows,
+void layernorm_fwd(const void* x, const void* gamma_, const void* beta_, void* y, float* mean, float* rstd, int rows,
                    int width, float eps, cudaStream_t st) {
     if (width % 8) throw std::runtime_error("layernorm: width must be a multiple of 8");
     auto X = static_cast<const __nv_bfloat16*>(x);
     auto Y = static_cast<__nv_bfloat16*>(y);
+    auto gamma = static_cast<const __nv_bfloat16*>(gamma_);
+    auto beta = static_cast<const __nv_bfloat16*>(beta_);
     const int v = (width + 1023) / 1024;
 #define LNF(V_) \
     if (v <= V_) return ln_fwd_kernel<V_><<<rows, NT, 0, st>>>(X, gamma, beta, Y, mean, rstd, width, eps);
@@ -194,13 +196,14 @@ void layernorm_fwd(const void* x, const float* gamma, const float* beta, void* y
     throw std::runtime_error("layernorm: width too large");
 }
 
-void layernorm_bwd(const void* dy, const void* x, const float* gamma, const float* mean, const float* rstd,
+void layernorm_bwd(const void* dy, const void* x, const void* gamma_, const float* mean, const float* rstd,
                    const void* dres, void* dx, float* dgamma, float* dbeta, int rows, int width, cudaStream_t st) {
     if (width % 8) throw std::runtime_error("layernorm: width must be a multiple of 8");
     auto DY = static_cast<const __nv_bfloat16*>(dy);
     auto X = static_cast<const __nv_bfloat16*>(x);
     auto R = static_cast<const __nv_bfloat16*>(dres);
     auto DX = static_cast<__nv_bfloat16*>(dx);
+    auto gamma = static_cast<const __nv_bfloat16*>(gamma_);
     const int v = (width + 1023) / 1024;
     // enough blocks to fill the chip a few times over, few enough that the per-block
     // dgamma/dbeta partials amortise their global atomics over many rows

@@ -6,13 +6,6 @@
 #include "capi_util.hpp"
 #include "schedule.hpp"
 
-struct bfpp_graph {
-    bfpp::TaskGraph g;
-};
-struct bfpp_timeline {
-    bfpp::Timeline tl;
-};
-
 namespace bfpp {
 
 thread_local std::string g_last_error;

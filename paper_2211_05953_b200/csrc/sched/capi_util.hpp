@@ -4,9 +4,20 @@
 #include <exception>
 #include <string>
 
+#include "../../../include/bfpp.h"
 #include "schedule.hpp"
 
+struct bfpp_graph {
+    bfpp::TaskGraph g;
+};
+struct bfpp_timeline {
+    bfpp::Timeline tl;
+};
+
 namespace bfpp {
+
+ModelSpec to_model(const bfpp_model_spec* m);
+ParallelConfig to_config(const bfpp_parallel_config* c);
 
 void set_error(const std::string& msg);
 

@@ -1,0 +1,104 @@
+"""TEST INFRASTRUCTURE: runs the executor on a config and compares with the CPU oracle.
+
+Used in-process by tests/test_executor_gpu.py (1 GPU) and, per rank, by
+tests/dist_worker.py under torchrun (N GPUs)."""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+sys.path.insert(0, ROOT)
+
+import gpt_oracle as O  # noqa: E402
+
+from paper_2211_05953_b200 import pipesim as ps  # noqa: E402
+from paper_2211_05953_b200.model import GPTConfig, flatten_stage, unflatten_stage  # noqa: E402
+
+LR = 1e-3
+TINY = GPTConfig.preset("tiny")
+
+
+def make_case(cfg: GPTConfig, config: ps.ParallelConfig, seed=7):
+    params = O.init_params(cfg, seed=seed, std=0.05)
+    rng = np.random.default_rng(seed + 1)
+    tokens = rng.integers(0, cfg.s_voc, (config.n_dp, config.n_mb, config.s_mb, cfg.s_seq + 1)).astype(np.int32)
+    return params, tokens
+
+
+def run_rank(executor_factory, cfg, config, params, tokens, rank):
+    """Runs 1 step without optimizer (grads) then 1 step with (weights) on this rank.
+    Returns dict with loss, per-stage (grads, lo, hi), per-stage (params, lo, hi)."""
+    n_stage = config.n_pp * config.n_loop
+    dp = rank // config.n_pp
+    ex = executor_factory(skip_optimizer=True)
+    for s in ex.local_stages:
+        ex.set_stage_params(s, flatten_stage(params, cfg, s, n_stage))
+    loss = ex.step(tokens[dp])
+    grads = {s: ex.get_stage_grads(s) for s in ex.local_stages}
+    ex.close()
+    ex = executor_factory(skip_optimizer=False, lr=LR)
+    for s in ex.local_stages:
+        ex.set_stage_params(s, flatten_stage(params, cfg, s, n_stage))
+    loss2 = ex.step(tokens[dp])
+    newp = {s: ex.get_stage_params(s) for s in ex.local_stages}
+    ex.close()
+    return {"loss": loss, "loss2": loss2, "grads": grads, "params": newp}
+
+
+def oracle(cfg, config, params, tokens):
+    flat_tokens = tokens.reshape(-1, cfg.s_seq + 1)
+    loss, grads = O.loss_and_grads(params, flat_tokens, cfg)
+    m = {k: np.zeros_like(v) for k, v in params.items()}
+    v = {k: np.zeros_like(v) for k, v in params.items()}
+    newp = O.adam_step({k: np.asarray(a, np.float64) for k, a in params.items()}, grads, m, v, 1, LR, 0.9, 0.95,
+                       1e-8, 0.0)
+    replica_loss = [O.loss_and_grads(params, tokens[d].reshape(-1, cfg.s_seq + 1), cfg)[0]
+                    for d in range(config.n_dp)]
+    return loss, grads, newp, replica_loss
+
+
+def compare(cfg, config, results, params, tokens):
+    """results: list over ranks of run_rank dicts. Returns a report dict; raises AssertionError on mismatch.
+
+    Tolerances (bf16 weights/activations, f32 accumulation):
+      replica loss: |dl| <= 2e-3 * loss
+      gradients: per tensor ||g - g_ref|| <= 3e-2 * ||g_ref|| (+1e-6 absolute floor)
+      weights after one Adam step (first step: update = lr * sign-like): |p - p_ref| <= 2*lr for
+      every element and <= 0.05*lr for >= 95% of elements.
+    """
+    n_stage = config.n_pp * config.n_loop
+    loss, grads, newp, rloss = oracle(cfg, config, params, tokens)
+    report = {"oracle_loss": loss, "grad_rel": {}, "weights_frac_close": {}}
+    for r, res in enumerate(results):
+        dp, pp = r // config.n_pp, r % config.n_pp
+        if pp == (n_stage - 1) % config.n_pp:
+            assert abs(res["loss"] - rloss[dp]) <= 2e-3 * rloss[dp], (res["loss"], rloss[dp])
+            report.setdefault("losses", []).append((res["loss"], rloss[dp]))
+    for s in range(n_stage):
+        full_g = np.full(flatten_stage(params, cfg, s, n_stage).size, np.nan, np.float32)
+        full_p = full_g.copy()
+        for r, res in enumerate(results):
+            if s in res["grads"]:
+                g, lo, hi = res["grads"][s]
+                full_g[lo:hi] = g[lo:hi]
+                p, lo, hi = res["params"][s]
+                full_p[lo:hi] = p[lo:hi]
+        assert not np.isnan(full_g).any(), f"stage {s}: gradient shards do not cover the stage"
+        got_g = unflatten_stage(full_g, cfg, s, n_stage)
+        got_p = unflatten_stage(full_p, cfg, s, n_stage)
+        for k in got_g:
+            ref = grads[k]
+            err = np.linalg.norm(got_g[k] - ref)
+            rel = err / (np.linalg.norm(ref) + 1e-6)
+            report["grad_rel"][k] = float(rel)
+            assert err <= 3e-2 * np.linalg.norm(ref) + 1e-6, (k, rel)
+            dpar = np.abs(got_p[k] - newp[k])
+            assert dpar.max() <= 2 * LR + 1e-6, (k, dpar.max())
+            frac = float((dpar <= 0.05 * LR).mean())
+            report["weights_frac_close"][k] = frac
+            assert frac >= 0.95, (k, frac)
+    return report

@@ -1,0 +1,71 @@
+"""Executor numerics vs the CPU oracle on one B200 (tiny GPT), every schedule
+that fits one device, plus timeline/metric checks. Tolerances: tests/exec_harness.compare."""
+import numpy as np
+import pytest
+
+import exec_harness as H
+from paper_2211_05953_b200 import pipesim as ps
+
+pytestmark = pytest.mark.gpu
+S = ps.Schedule
+
+CONFIGS = {
+    "nopipe_mb4": ps.ParallelConfig(n_mb=4, schedule=S.NoPipeline),
+    "bf_loop4_mb3": ps.ParallelConfig(n_mb=3, n_loop=4, schedule=S.BreadthFirst),
+    "df_loop2_mb2": ps.ParallelConfig(n_mb=2, n_loop=2, schedule=S.DepthFirst),
+    "gpipe_mb2_smb2": ps.ParallelConfig(n_mb=2, s_mb=2, schedule=S.GPipe),
+    "1f1b_mb2": ps.ParallelConfig(n_mb=2, schedule=S.OneFOneB),
+}
+
+
+@pytest.mark.parametrize("name", list(CONFIGS))
+def test_executor_matches_oracle(cuda_device, name):
+    from paper_2211_05953_b200.executor import Executor
+    config = CONFIGS[name]
+    cfg = H.TINY
+    params, tokens = H.make_case(cfg, config)
+    res = H.run_rank(lambda **kw: Executor(cfg, config, **kw), cfg, config, params, tokens, 0)
+    rep = H.compare(cfg, config, [res], params, tokens)
+    print(name, rep["losses"], max(rep["grad_rel"].values()))
+
+
+def test_schedules_agree_with_each_other(cuda_device):
+    """Same model/batch: every schedule's gradients agree (f32 accumulation, ascending micro-batches)."""
+    from paper_2211_05953_b200.executor import Executor
+    cfg = H.TINY
+    base = ps.ParallelConfig(n_mb=4, schedule=S.NoPipeline)
+    params, tokens = H.make_case(cfg, base)
+    out = {}
+    for name, c in [("np", base), ("bf", ps.ParallelConfig(n_mb=4, n_loop=4, schedule=S.BreadthFirst)),
+                    ("df", ps.ParallelConfig(n_mb=4, n_loop=2, schedule=S.DepthFirst))]:
+        r = H.run_rank(lambda **kw: Executor(cfg, c, **kw), cfg, c, params, tokens, 0)
+        n_stage = c.n_loop
+        flat = {}
+        for s in range(n_stage):
+            flat.update(H.unflatten_stage(r["grads"][s][0], cfg, s, n_stage))
+        out[name] = (r["loss"], flat)
+    for name in ("bf", "df"):
+        assert abs(out[name][0] - out["np"][0]) <= 1e-6 * abs(out["np"][0])
+        for k, v in out["np"][1].items():
+            np.testing.assert_allclose(out[name][1][k], v, rtol=2e-3, atol=1e-6, err_msg=(name, k))
+
+
+def test_measured_timeline_contract(cuda_device):
+    from paper_2211_05953_b200.executor import Executor, measured_timeline
+    cfg = H.TINY
+    c = ps.ParallelConfig(n_mb=4, n_loop=4, schedule=S.BreadthFirst)
+    params, tokens = H.make_case(cfg, c)
+    ex = Executor(cfg, c, record_timeline=True)
+    ex.step(tokens[0])
+    ex.step(tokens[0])
+    s, e = ex.task_times()
+    tl = measured_timeline(ex.graph, [s], [e])
+    for t in ex.graph.tasks:
+        ev = tl.events[t.id]
+        assert ev.end >= ev.start >= 0
+        for d in t.deps:
+            assert tl.events[d].end <= ev.start + 1e-6
+    prog = ex.graph.compute_program[0]
+    for a, b in zip(prog, prog[1:]):
+        assert tl.events[a].end <= tl.events[b].start + 1e-6
+    assert 0 <= ps.bubble_fraction(tl) < 1.0

@@ -54,11 +54,11 @@ def test_layernorm(cuda_device, rows, width):
     ops = _ops()
     torch.manual_seed(rows + width)
     x = torch.randn(rows, width, device="cuda").bfloat16()
-    g = 1 + 0.1 * torch.randn(width, device="cuda")
-    b = 0.1 * torch.randn(width, device="cuda")
+    g = (1 + 0.1 * torch.randn(width, device="cuda")).bfloat16()
+    b = (0.1 * torch.randn(width, device="cuda")).bfloat16()
     y, mean, rstd = ops.layernorm_fwd(x, g, b)
     xf = x.float().requires_grad_()
-    gf, bf = g.clone().requires_grad_(), b.clone().requires_grad_()
+    gf, bf = g.float().requires_grad_(), b.float().requires_grad_()
     ref = torch.nn.functional.layer_norm(xf, (width,), gf, bf, 1e-5)
     torch.cuda.synchronize()
     _close(y, ref, 2e-2)
