@@ -187,7 +187,8 @@ int bfpp_adam_update(float* p, float* m, float* v, float* g, void* w16, int64_t 
  * stage). */
 
 #define BFPP_NCCL_UID_BYTES 128
-#define BFPP_EXEC_SKIP_OPTIMIZER 1 /* flags: keep gradients, do not run Adam */
+#define BFPP_EXEC_SKIP_OPTIMIZER 1  /* flags: keep gradients, do not run Adam */
+#define BFPP_EXEC_PROFILE_KERNELS 2 /* flags: CUDA events around every kernel -> bfpp_exec_kernel_stats */
 
 typedef struct bfpp_exec_opts {
     int32_t device;          /* CUDA ordinal of this rank */
@@ -230,6 +231,15 @@ int bfpp_exec_zero_grads(bfpp_exec* e);
 /* measured [start, end] (seconds from the step origin) of this rank's tasks in the last
  * step; tasks of other devices are NaN. Arrays have bfpp_graph_n_tasks entries. */
 int bfpp_exec_timeline(const bfpp_exec* e, double* start, double* end);
+/* toggles per-task timeline events and per-kernel profiling for subsequent steps */
+int bfpp_exec_set_flags(bfpp_exec* e, int32_t record_timeline, int32_t profile_kernels);
+/* the executor's compute stream (cudaStream_t); every step starts and ends on it */
+void* bfpp_exec_stream(const bfpp_exec* e);
+/* kernel statistics of the last step for category cat (0 GEMM, 1 attention fwd,
+ * 2 attention bwd, 3 LayerNorm, 4 misc (embedding, cross-entropy, reductions), 5 Adam):
+ * launches (always), summed device ms and algorithmic work (flops for 0-2, bytes for 3-5;
+ * both only with BFPP_EXEC_PROFILE_KERNELS). */
+int bfpp_exec_kernel_stats(const bfpp_exec* e, int32_t cat, int64_t* launches, double* ms, double* work);
 
 #ifdef __cplusplus
 }

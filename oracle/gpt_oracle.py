@@ -92,13 +92,84 @@ def _attention_bwd(do, q, k, v, p):
     return dq, dk, dv
 
 
+def layer_forward(P, pre, x, cfg):
+    """One pre-LN block on one sequence x [S, h]; returns (x_out, cache)."""
+    h, H = cfg.s_hidden, cfg.n_heads
+    d = h // H
+    S = x.shape[0]
+    ln1, c1 = layernorm(x, P[pre + "ln1_g"], P[pre + "ln1_b"])
+    qkv = ln1 @ P[pre + "w_qkv"].T
+    o = np.zeros((S, h), dtype=x.dtype)
+    probs = []
+    for j in range(H):
+        q = qkv[:, j * d:(j + 1) * d]
+        k = qkv[:, h + j * d:h + (j + 1) * d]
+        v = qkv[:, 2 * h + j * d:2 * h + (j + 1) * d]
+        oj, pj = _attention(q, k, v)
+        o[:, j * d:(j + 1) * d] = oj
+        probs.append(pj)
+    x_mid = x + o @ P[pre + "w_o"].T
+    ln2, c2 = layernorm(x_mid, P[pre + "ln2_g"], P[pre + "ln2_b"])
+    a_pre = ln2 @ P[pre + "w_fc1"].T
+    act = gelu(a_pre)
+    x_out = x_mid + act @ P[pre + "w_fc2"].T
+    return x_out, (ln1, c1, qkv, o, probs, ln2, c2, a_pre, act)
+
+
+def layer_backward(P, G, pre, dx, cache, cfg):
+    """Backward of layer_forward: accumulates parameter grads into G, returns d x_in."""
+    h, H = cfg.s_hidden, cfg.n_heads
+    d = h // H
+    ln1, c1, qkv, o, probs, ln2, c2, a_pre, act = cache
+    G[pre + "w_fc2"] += dx.T @ act
+    dpre = (dx @ P[pre + "w_fc2"]) * dgelu(a_pre)
+    G[pre + "w_fc1"] += dpre.T @ ln2
+    dln2 = dpre @ P[pre + "w_fc1"]
+    dmid, dg, db = layernorm_bwd(dln2, c2, P[pre + "ln2_g"])
+    dmid += dx
+    G[pre + "ln2_g"] += dg
+    G[pre + "ln2_b"] += db
+    G[pre + "w_o"] += dmid.T @ o
+    do = dmid @ P[pre + "w_o"]
+    dqkv = np.zeros_like(qkv)
+    for j in range(H):
+        sl = slice(j * d, (j + 1) * d)
+        ks = slice(h + j * d, h + (j + 1) * d)
+        vs = slice(2 * h + j * d, 2 * h + (j + 1) * d)
+        dq, dk, dv = _attention_bwd(do[:, sl], qkv[:, sl], qkv[:, ks], qkv[:, vs], probs[j])
+        dqkv[:, sl], dqkv[:, ks], dqkv[:, vs] = dq, dk, dv
+    G[pre + "w_qkv"] += dqkv.T @ ln1
+    dln1 = dqkv @ P[pre + "w_qkv"]
+    dxi, dg, db = layernorm_bwd(dln1, c1, P[pre + "ln1_g"])
+    G[pre + "ln1_g"] += dg
+    G[pre + "ln1_b"] += db
+    return dxi + dmid
+
+
+def head_forward_backward(P, G, x, lab, n_tok):
+    """Final LayerNorm + LM head + cross-entropy (summed over rows) and its backward
+    (gradient of the mean over n_tok tokens); returns (loss_sum, d x)."""
+    S = x.shape[0]
+    lnf, cf = layernorm(x, P["lnf_g"], P["lnf_b"])
+    logits = lnf @ P["w_head"].T
+    mx = logits.max(-1, keepdims=True)
+    lse = mx[:, 0] + np.log(np.exp(logits - mx).sum(-1))
+    loss = float((lse - logits[np.arange(S), lab]).sum())
+    dlog = np.exp(logits - lse[:, None])
+    dlog[np.arange(S), lab] -= 1.0
+    dlog /= n_tok
+    G["w_head"] += dlog.T @ lnf
+    dx, dg, db = layernorm_bwd(dlog @ P["w_head"], cf, P["lnf_g"])
+    G["lnf_g"] += dg
+    G["lnf_b"] += db
+    return loss, dx
+
+
 def loss_and_grads(params, tokens, cfg):
     """Mean next-token cross-entropy over all sequences of `tokens` [N, S+1] and its
     gradient w.r.t. every parameter (float64)."""
     P = {k: np.asarray(v, dtype=np.float64) for k, v in params.items()}
     G = {k: np.zeros_like(v) for k, v in P.items()}
-    h, H, L = cfg.s_hidden, cfg.n_heads, cfg.n_layers
-    d = h // H
     tokens = np.asarray(tokens)
     N, S = tokens.shape[0], tokens.shape[1] - 1
     n_tok = N * S
@@ -107,65 +178,13 @@ def loss_and_grads(params, tokens, cfg):
         inp, lab = tokens[b, :-1], tokens[b, 1:]
         x = P["wte"][inp] + P["wpe"][:S]
         caches = []
-        for l in range(L):
-            pre = f"h{l}."
-            ln1, c1 = layernorm(x, P[pre + "ln1_g"], P[pre + "ln1_b"])
-            qkv = ln1 @ P[pre + "w_qkv"].T
-            o = np.zeros((S, h))
-            probs = []
-            for j in range(H):
-                q = qkv[:, j * d:(j + 1) * d]
-                k = qkv[:, h + j * d:h + (j + 1) * d]
-                v = qkv[:, 2 * h + j * d:2 * h + (j + 1) * d]
-                oj, pj = _attention(q, k, v)
-                o[:, j * d:(j + 1) * d] = oj
-                probs.append(pj)
-            x_mid = x + o @ P[pre + "w_o"].T
-            ln2, c2 = layernorm(x_mid, P[pre + "ln2_g"], P[pre + "ln2_b"])
-            a_pre = ln2 @ P[pre + "w_fc1"].T
-            act = gelu(a_pre)
-            x_out = x_mid + act @ P[pre + "w_fc2"].T
-            caches.append((x, ln1, c1, qkv, o, probs, x_mid, ln2, c2, a_pre, act))
-            x = x_out
-        lnf, cf = layernorm(x, P["lnf_g"], P["lnf_b"])
-        logits = lnf @ P["w_head"].T
-        mx = logits.max(-1, keepdims=True)
-        lse = mx[:, 0] + np.log(np.exp(logits - mx).sum(-1))
-        total += float((lse - logits[np.arange(S), lab]).sum())
-        dlog = np.exp(logits - lse[:, None])
-        dlog[np.arange(S), lab] -= 1.0
-        dlog /= n_tok
-        G["w_head"] += dlog.T @ lnf
-        dx, dg, db = layernorm_bwd(dlog @ P["w_head"], cf, P["lnf_g"])
-        G["lnf_g"] += dg
-        G["lnf_b"] += db
-        for l in reversed(range(L)):
-            pre = f"h{l}."
-            x_in, ln1, c1, qkv, o, probs, x_mid, ln2, c2, a_pre, act = caches[l]
-            G[pre + "w_fc2"] += dx.T @ act
-            dpre = (dx @ P[pre + "w_fc2"]) * dgelu(a_pre)
-            G[pre + "w_fc1"] += dpre.T @ ln2
-            dln2 = dpre @ P[pre + "w_fc1"]
-            dmid, dg, db = layernorm_bwd(dln2, c2, P[pre + "ln2_g"])
-            dmid += dx
-            G[pre + "ln2_g"] += dg
-            G[pre + "ln2_b"] += db
-            G[pre + "w_o"] += dmid.T @ o
-            do = dmid @ P[pre + "w_o"]
-            dqkv = np.zeros_like(qkv)
-            for j in range(H):
-                sl = slice(j * d, (j + 1) * d)
-                q, k, v = qkv[:, sl], qkv[:, h + j * d:h + (j + 1) * d], qkv[:, 2 * h + j * d:2 * h + (j + 1) * d]
-                dq, dk, dv = _attention_bwd(do[:, sl], q, k, v, probs[j])
-                dqkv[:, sl] = dq
-                dqkv[:, h + j * d:h + (j + 1) * d] = dk
-                dqkv[:, 2 * h + j * d:2 * h + (j + 1) * d] = dv
-            G[pre + "w_qkv"] += dqkv.T @ ln1
-            dln1 = dqkv @ P[pre + "w_qkv"]
-            dxi, dg, db = layernorm_bwd(dln1, c1, P[pre + "ln1_g"])
-            G[pre + "ln1_g"] += dg
-            G[pre + "ln1_b"] += db
-            dx = dxi + dmid
+        for l in range(cfg.n_layers):
+            x, c = layer_forward(P, f"h{l}.", x, cfg)
+            caches.append(c)
+        loss, dx = head_forward_backward(P, G, x, lab, n_tok)
+        total += loss
+        for l in reversed(range(cfg.n_layers)):
+            dx = layer_backward(P, G, f"h{l}.", dx, caches[l], cfg)
         np.add.at(G["wte"], inp, dx)
         G["wpe"][:S] += dx
     return total / n_tok, G

@@ -63,4 +63,8 @@ PROTOS.update({
     "bfpp_exec_get_grads": (C.c_int, [_P, _I64, _P, _I64, C.POINTER(_I64), C.POINTER(_I64)]),
     "bfpp_exec_zero_grads": (C.c_int, [_P]),
     "bfpp_exec_timeline": (C.c_int, [_P, _P, _P]),
+    "bfpp_exec_stream": (_P, [_P]),
+    "bfpp_exec_set_flags": (C.c_int, [_P, _I32, _I32]),
+    "bfpp_exec_kernel_stats": (C.c_int, [_P, _I32, C.POINTER(_I64), C.POINTER(C.c_double),
+                                         C.POINTER(C.c_double)]),
 })

@@ -42,6 +42,7 @@ int bfpp_exec_create(const bfpp_model_spec* m, const bfpp_parallel_config* c, co
         eo.weight_decay = o->weight_decay;
         eo.init_std = o->init_std;
         eo.skip_optimizer = (o->flags & BFPP_EXEC_SKIP_OPTIMIZER) != 0;
+        eo.profile_kernels = (o->flags & BFPP_EXEC_PROFILE_KERNELS) != 0;
         std::vector<ncclUniqueId> ids;
         if (uids) {
             const int64_t n = bfpp_exec_n_comm_ids(c);
@@ -90,6 +91,22 @@ int bfpp_exec_zero_grads(bfpp_exec* e) {
 }
 int bfpp_exec_timeline(const bfpp_exec* e, double* start, double* end) {
     return guarded([&] { e->x->timeline(start, end); });
+}
+
+int bfpp_exec_set_flags(bfpp_exec* e, int32_t record_timeline, int32_t profile_kernels) {
+    return guarded([&] { e->x->set_flags(record_timeline != 0, profile_kernels != 0); });
+}
+
+void* bfpp_exec_stream(const bfpp_exec* e) { return e->x->compute_stream(); }
+
+int bfpp_exec_kernel_stats(const bfpp_exec* e, int32_t cat, int64_t* launches, double* ms, double* work) {
+    return guarded([&] {
+        if (cat < 0 || cat >= K_NCAT) throw SpecError("kernel_stats: unknown category");
+        const KernelStats& k = e->x->kernel_stats();
+        if (launches) *launches = k.launches[cat];
+        if (ms) *ms = k.ms[cat];
+        if (work) *work = k.work[cat];
+    });
 }
 
 }  // extern "C"

@@ -169,6 +169,14 @@ struct Executor::Impl {
     std::vector<double> tl_start, tl_end;
     int step_no = 0;
     std::vector<int> task_c;                      // local stage index of compute tasks
+    KernelStats stats;
+    struct Mark {
+        int cat;
+        double work;
+        size_t ev;
+    };
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<Mark> marks;
 
     template <class T>
     T* alloc(size_t n, size_t* total) {
@@ -434,11 +442,8 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
         }
         I.order.push_back(te);
         CK(cudaEventCreateWithFlags(&I.done[static_cast<size_t>(id)], cudaEventDisableTiming));
-        if (o.record_timeline) {
-            CK(cudaEventCreate(&I.t_start[static_cast<size_t>(id)]));
-            CK(cudaEventCreate(&I.t_end[static_cast<size_t>(id)]));
-        }
     }
+    set_flags(o.record_timeline, o.profile_kernels);
     CK(cudaEventCreate(&I.origin));
     CK(cudaEventCreateWithFlags(&I.step_end, cudaEventDisableTiming));
     for (auto& e : I.stream_end) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -458,6 +463,7 @@ Executor::~Executor() {
         if (e) cudaEventDestroy(e);
     for (auto e : I.t_end)
         if (e) cudaEventDestroy(e);
+    for (auto e : I.ev_pool) cudaEventDestroy(e);
     if (I.origin) cudaEventDestroy(I.origin);
     if (I.step_end) cudaEventDestroy(I.step_end);
     for (auto e : I.stream_end)
@@ -506,6 +512,46 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
     const float grad_scale = 1.f / static_cast<float>(c_.n_dp * c_.n_mb * T);
     const bool fs = c_.n_dp >= 2 && c_.dp_variant == DpVariant::DP_FS;
 
+    I.stats = KernelStats{};
+    I.marks.clear();
+    size_t ev_next = 0;
+    // every kernel of the step goes through K(): counts launches, optionally brackets with events
+    auto K = [&](int cat, double work, int n_launch, cudaStream_t st, auto&& fn) {
+        I.stats.launches[cat] += n_launch;
+        if (!o_.profile_kernels) {
+            fn();
+            return;
+        }
+        while (I.ev_pool.size() < ev_next + 2) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            I.ev_pool.push_back(e);
+        }
+        CK(cudaEventRecord(I.ev_pool[ev_next], st));
+        fn();
+        CK(cudaEventRecord(I.ev_pool[ev_next + 1], st));
+        I.marks.push_back({cat, work, ev_next});
+        ev_next += 2;
+    };
+    auto G = [&](cudaStream_t st, int64_t M, int64_t N, int64_t Kd, const void* A, int64_t lda, int amn,
+                 const void* Bp, int64_t ldb, int bmn, void* D, int64_t ldd, int epi, const void* aux = nullptr,
+                 int64_t ldaux = 0, void* aux_out = nullptr, int64_t ldaux_out = 0, int acc = 0) {
+        K(K_GEMM, 2.0 * M * N * Kd, 1, st,
+          [&] { gemm(st, M, N, Kd, A, lda, amn, Bp, ldb, bmn, D, ldd, epi, aux, ldaux, aux_out, ldaux_out, acc); });
+    };
+    const double Th2 = 2.0 * static_cast<double>(T * h);  // bytes of one [T,h] bf16 activation
+    const double attn_flops = 2.0 * B * static_cast<double>(S) * (S + 1) * static_cast<double>(h);  // causal, fwd
+    auto LNF = [&](cudaStream_t st, const bf16* x, const bf16* g, const bf16* b, bf16* y, float* mu, float* rs) {
+        K(K_LAYERNORM, 2 * Th2, 1, st,
+          [&] { layernorm_fwd(x, g, b, y, mu, rs, static_cast<int>(T), static_cast<int>(h), 1e-5f, st); });
+    };
+    auto LNB = [&](cudaStream_t st, const bf16* dy, const bf16* x, const bf16* g, const float* mu, const float* rs,
+                   const bf16* dres, bf16* dx, float* dg, float* db) {
+        K(K_LAYERNORM, (dres ? 4 : 3) * Th2, 1, st, [&] {
+            layernorm_bwd(dy, x, g, mu, rs, dres, dx, dg, db, static_cast<int>(T), static_cast<int>(h), st);
+        });
+    };
+
     auto weights = [&](const TaskExec& te, int cidx) -> const bf16* {
         if (fs) return I.slots[te.slot];
         return I.local[static_cast<size_t>(cidx)].w16;
@@ -515,8 +561,10 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
         const bool sharded = ls.gshard != nullptr;
         float* g = sharded ? ls.gshard : ls.grad;
         bf16* w = sharded ? ls.w16_shard : ls.w16;
-        adam_update(ls.master, ls.m, ls.v, g, w, ls.shard_n, o_.lr, o_.beta1, o_.beta2, o_.eps, o_.weight_decay,
-                    I.step_no, sharded ? 0 : 1, st);
+        K(K_ADAM, (sharded ? 26.0 : 30.0) * static_cast<double>(ls.shard_n), 1, st, [&] {
+            adam_update(ls.master, ls.m, ls.v, g, w, ls.shard_n, o_.lr, o_.beta1, o_.beta2, o_.eps, o_.weight_decay,
+                        I.step_no, sharded ? 0 : 1, st);
+        });
         if (sharded && c_.dp_variant == DpVariant::DP_PS)
             NK(ncclAllGather(ls.w16_shard, ls.w16, static_cast<size_t>(ls.shard_n), ncclBfloat16, I.dp_comm, st));
     };
@@ -533,26 +581,28 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
             StageActs& a = I.acts[static_cast<size_t>(t.micro_batch)][static_cast<size_t>(cidx)];
             const bf16* W = weights(te, cidx);
             const int32_t* inp = I.inputs + t.micro_batch * T;
-            if (L.first) embed_fwd(inp, W + L.wte, W + L.wpe, a.in, static_cast<int>(T), S, static_cast<int>(h), st);
+            if (L.first)
+                K(K_MISC, 3 * Th2, 1, st, [&] {
+                    embed_fwd(inp, W + L.wte, W + L.wpe, a.in, static_cast<int>(T), S, static_cast<int>(h), st);
+                });
             for (size_t l = 0; l < L.layers.size(); ++l) {
                 const LayerParams& P = L.layers[l];
                 LayerActs& x = a.layers[l];
-                layernorm_fwd(x.x_in, W + P.ln1_g, W + P.ln1_b, x.ln1, x.mu1, x.rs1, static_cast<int>(T),
-                              static_cast<int>(h), 1e-5f, st);
-                gemm(st, T, 3 * h, h, x.ln1, h, 0, W + P.qkv, h, 0, x.qkv, 3 * h, GEMM_EPI_BF16);
-                attention_fwd(x.qkv, x.o, x.lse, B, S, H, 128, st);
-                gemm(st, T, h, h, x.o, h, 0, W + P.o, h, 0, x.x_mid, h, GEMM_EPI_RESID, x.x_in, h);
-                layernorm_fwd(x.x_mid, W + P.ln2_g, W + P.ln2_b, x.ln2, x.mu2, x.rs2, static_cast<int>(T),
-                              static_cast<int>(h), 1e-5f, st);
-                gemm(st, T, mlp, h, x.ln2, h, 0, W + P.fc1, h, 0, x.act, mlp, GEMM_EPI_GELU, nullptr, 0, x.pre, mlp);
-                gemm(st, T, h, mlp, x.act, mlp, 0, W + P.fc2, mlp, 0, x.x_out, h, GEMM_EPI_RESID, x.x_mid, h);
+                LNF(st, x.x_in, W + P.ln1_g, W + P.ln1_b, x.ln1, x.mu1, x.rs1);
+                G(st, T, 3 * h, h, x.ln1, h, 0, W + P.qkv, h, 0, x.qkv, 3 * h, GEMM_EPI_BF16);
+                K(K_ATTN_FWD, attn_flops, 1, st, [&] { attention_fwd(x.qkv, x.o, x.lse, B, S, H, 128, st); });
+                G(st, T, h, h, x.o, h, 0, W + P.o, h, 0, x.x_mid, h, GEMM_EPI_RESID, x.x_in, h);
+                LNF(st, x.x_mid, W + P.ln2_g, W + P.ln2_b, x.ln2, x.mu2, x.rs2);
+                G(st, T, mlp, h, x.ln2, h, 0, W + P.fc1, h, 0, x.act, mlp, GEMM_EPI_GELU, nullptr, 0, x.pre, mlp);
+                G(st, T, h, mlp, x.act, mlp, 0, W + P.fc2, mlp, 0, x.x_out, h, GEMM_EPI_RESID, x.x_mid, h);
             }
             if (L.last) {
-                layernorm_fwd(a.out, W + L.lnf_g, W + L.lnf_b, a.lnf, a.muf, a.rsf, static_cast<int>(T),
-                              static_cast<int>(h), 1e-5f, st);
-                gemm(st, T, V, h, a.lnf, h, 0, W + L.head, h, 0, a.logits, V, GEMM_EPI_BF16);
-                softmax_xent(a.logits, V, I.labels + t.micro_batch * T, I.row_loss + t.micro_batch * T,
-                             static_cast<int>(T), static_cast<int>(V), grad_scale, st);
+                LNF(st, a.out, W + L.lnf_g, W + L.lnf_b, a.lnf, a.muf, a.rsf);
+                G(st, T, V, h, a.lnf, h, 0, W + L.head, h, 0, a.logits, V, GEMM_EPI_BF16);
+                K(K_MISC, 4.0 * static_cast<double>(T * V), 1, st, [&] {
+                    softmax_xent(a.logits, V, I.labels + t.micro_batch * T, I.row_loss + t.micro_batch * T,
+                                 static_cast<int>(T), static_cast<int>(V), grad_scale, st);
+                });
             }
             break;
         }
@@ -561,13 +611,12 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
             StageActs& a = I.acts[static_cast<size_t>(t.micro_batch)][static_cast<size_t>(cidx)];
             LocalStage& ls = I.local[static_cast<size_t>(cidx)];
             const bf16* W = weights(te, cidx);
-            float* G = ls.grad;
+            float* G_ = ls.grad;
             const bf16* g;
             if (L.last) {
-                gemm(st, T, h, V, a.logits, V, 0, W + L.head, h, 1, I.tmp_h, h, GEMM_EPI_BF16);
-                gemm(st, V, h, T, a.logits, V, 1, a.lnf, h, 1, G + L.head, h, GEMM_EPI_F32, nullptr, 0, nullptr, 0, 1);
-                layernorm_bwd(I.tmp_h, a.out, W + L.lnf_g, a.muf, a.rsf, nullptr, I.gA, G + L.lnf_g, G + L.lnf_b,
-                              static_cast<int>(T), static_cast<int>(h), st);
+                G(st, T, h, V, a.logits, V, 0, W + L.head, h, 1, I.tmp_h, h, GEMM_EPI_BF16);
+                G(st, V, h, T, a.logits, V, 1, a.lnf, h, 1, G_ + L.head, h, GEMM_EPI_F32, nullptr, 0, nullptr, 0, 1);
+                LNB(st, I.tmp_h, a.out, W + L.lnf_g, a.muf, a.rsf, nullptr, I.gA, G_ + L.lnf_g, G_ + L.lnf_b);
                 g = I.gA;
             } else {
                 g = a.gin;
@@ -578,26 +627,28 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
                 bf16* gmid = g == I.gB ? I.gA : I.gB;
                 bf16* gnext = (li == 0 && !L.first) ? a.gout : (gmid == I.gA ? I.gB : I.gA);
                 // MLP: x_out = x_mid + gelu(ln2 W1^T) W2^T
-                gemm(st, h, mlp, T, g, h, 1, x.act, mlp, 1, G + P.fc2, mlp, GEMM_EPI_F32, nullptr, 0, nullptr, 0, 1);
-                gemm(st, T, mlp, h, g, h, 0, W + P.fc2, mlp, 1, I.tmp_m, mlp, GEMM_EPI_DGELU, x.pre, mlp);
-                gemm(st, mlp, h, T, I.tmp_m, mlp, 1, x.ln2, h, 1, G + P.fc1, h, GEMM_EPI_F32, nullptr, 0, nullptr, 0, 1);
-                gemm(st, T, h, mlp, I.tmp_m, mlp, 0, W + P.fc1, h, 1, I.tmp_h, h, GEMM_EPI_BF16);
-                layernorm_bwd(I.tmp_h, x.x_mid, W + P.ln2_g, x.mu2, x.rs2, g, gmid, G + P.ln2_g, G + P.ln2_b,
-                              static_cast<int>(T), static_cast<int>(h), st);
+                G(st, h, mlp, T, g, h, 1, x.act, mlp, 1, G_ + P.fc2, mlp, GEMM_EPI_F32, nullptr, 0, nullptr, 0, 1);
+                G(st, T, mlp, h, g, h, 0, W + P.fc2, mlp, 1, I.tmp_m, mlp, GEMM_EPI_DGELU, x.pre, mlp);
+                G(st, mlp, h, T, I.tmp_m, mlp, 1, x.ln2, h, 1, G_ + P.fc1, h, GEMM_EPI_F32, nullptr, 0, nullptr, 0, 1);
+                G(st, T, h, mlp, I.tmp_m, mlp, 0, W + P.fc1, h, 1, I.tmp_h, h, GEMM_EPI_BF16);
+                LNB(st, I.tmp_h, x.x_mid, W + P.ln2_g, x.mu2, x.rs2, g, gmid, G_ + P.ln2_g, G_ + P.ln2_b);
                 // attention: x_mid = x_in + attn(ln1 Wqkv^T) Wo^T
-                gemm(st, h, h, T, gmid, h, 1, x.o, h, 1, G + P.o, h, GEMM_EPI_F32, nullptr, 0, nullptr, 0, 1);
-                gemm(st, T, h, h, gmid, h, 0, W + P.o, h, 1, I.tmp_h, h, GEMM_EPI_BF16);
-                attention_bwd(x.qkv, x.o, I.tmp_h, x.lse, I.delta, I.dq_acc, I.dqkv, B, S, H, 128, st);
-                gemm(st, 3 * h, h, T, I.dqkv, 3 * h, 1, x.ln1, h, 1, G + P.qkv, h, GEMM_EPI_F32, nullptr, 0, nullptr,
-                     0, 1);
-                gemm(st, T, h, 3 * h, I.dqkv, 3 * h, 0, W + P.qkv, h, 1, I.tmp_h, h, GEMM_EPI_BF16);
-                layernorm_bwd(I.tmp_h, x.x_in, W + P.ln1_g, x.mu1, x.rs1, gmid, gnext, G + P.ln1_g, G + P.ln1_b,
-                              static_cast<int>(T), static_cast<int>(h), st);
+                G(st, h, h, T, gmid, h, 1, x.o, h, 1, G_ + P.o, h, GEMM_EPI_F32, nullptr, 0, nullptr, 0, 1);
+                G(st, T, h, h, gmid, h, 0, W + P.o, h, 1, I.tmp_h, h, GEMM_EPI_BF16);
+                K(K_ATTN_BWD, 2.5 * attn_flops, 3, st, [&] {
+                    attention_bwd(x.qkv, x.o, I.tmp_h, x.lse, I.delta, I.dq_acc, I.dqkv, B, S, H, 128, st);
+                });
+                G(st, 3 * h, h, T, I.dqkv, 3 * h, 1, x.ln1, h, 1, G_ + P.qkv, h, GEMM_EPI_F32, nullptr, 0, nullptr, 0,
+                  1);
+                G(st, T, h, 3 * h, I.dqkv, 3 * h, 0, W + P.qkv, h, 1, I.tmp_h, h, GEMM_EPI_BF16);
+                LNB(st, I.tmp_h, x.x_in, W + P.ln1_g, x.mu1, x.rs1, gmid, gnext, G_ + P.ln1_g, G_ + P.ln1_b);
                 g = gnext;
             }
             if (L.first)
-                embed_bwd(I.inputs + t.micro_batch * T, g, G + L.wte, G + L.wpe, static_cast<int>(T), S,
-                          static_cast<int>(h), st);
+                K(K_MISC, 2 * Th2, 1, st, [&] {
+                    embed_bwd(I.inputs + t.micro_batch * T, g, G_ + L.wte, G_ + L.wpe, static_cast<int>(T), S,
+                              static_cast<int>(h), st);
+                });
             if (te.adam_after) {
                 // n_dp == 1: this stage's gradient is final; update it on the DP stream
                 CK(cudaEventRecord(I.done[static_cast<size_t>(te.id)], st));
@@ -635,7 +686,7 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
                 NK(ncclReduceScatter(ls.grad, dst, static_cast<size_t>(ls.shard_n), ncclFloat32, ncclSum, I.dp_comm,
                                      st));
                 if (!te.first_unit)
-                    add_f32_kernel<<<296, 256, 0, st>>>(ls.gshard, ls.gtmp, ls.shard_n);
+                    K(K_MISC, 12.0 * ls.shard_n, 1, st, [&] { add_f32_kernel<<<296, 256, 0, st>>>(ls.gshard, ls.gtmp, ls.shard_n); });
                 CK(cudaMemsetAsync(ls.grad, 0, static_cast<size_t>(full) * 4, st));
             }
             if (te.adam_after) adam(ls, st);
@@ -646,7 +697,9 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
         CK(cudaEventRecord(I.done[static_cast<size_t>(te.id)], st));
     }
     // loss of this replica (last-stage device): mean over its n_mb * T tokens
-    if (has_last) sum_f32(I.row_loss, c_.n_mb * T, 1.f / static_cast<float>(c_.n_mb * T), I.loss_dev, 0, cs);
+    if (has_last)
+        K(K_MISC, 4.0 * c_.n_mb * T, 1, cs,
+          [&] { sum_f32(I.row_loss, c_.n_mb * T, 1.f / static_cast<float>(c_.n_mb * T), I.loss_dev, 0, cs); });
     for (int s = 1; s < S_N; ++s) {
         CK(cudaEventRecord(I.stream_end[s], I.st[s]));
         CK(cudaStreamWaitEvent(cs, I.stream_end[s], 0));
@@ -663,6 +716,15 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
         }
     }
     CK(cudaPeekAtLastError());
+    if (o_.profile_kernels) {
+        CK(cudaEventSynchronize(I.step_end));
+        for (const auto& mk : I.marks) {
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, I.ev_pool[mk.ev], I.ev_pool[mk.ev + 1]));
+            I.stats.ms[mk.cat] += ms;
+            I.stats.work[mk.cat] += mk.work;
+        }
+    }
     if (o_.record_timeline) {
         CK(cudaEventSynchronize(I.step_end));
         for (const TaskExec& te : I.order) {
@@ -677,6 +739,22 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
         }
     }
 }
+
+const KernelStats& Executor::kernel_stats() const { return impl_->stats; }
+
+void Executor::set_flags(bool record_timeline, bool profile_kernels) {
+    Impl& I = *impl_;
+    CK(cudaSetDevice(I.dev));
+    o_.record_timeline = record_timeline;
+    o_.profile_kernels = profile_kernels;
+    if (record_timeline)
+        for (const TaskExec& te : I.order) {
+            const size_t id = static_cast<size_t>(te.id);
+            if (!I.t_start[id]) CK(cudaEventCreate(&I.t_start[id]));
+            if (!I.t_end[id]) CK(cudaEventCreate(&I.t_end[id]));
+        }
+}
+cudaStream_t Executor::compute_stream() const { return impl_->st[S_COMPUTE]; }
 
 void Executor::sync() {
     CK(cudaSetDevice(impl_->dev));

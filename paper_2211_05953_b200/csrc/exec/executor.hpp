@@ -26,6 +26,15 @@ struct ExecOptions {
     uint64_t seed = 1234;
     float lr = 1e-4f, beta1 = 0.9f, beta2 = 0.95f, eps = 1e-8f, weight_decay = 0.f, init_std = 0.02f;
     bool skip_optimizer = false;
+    bool profile_kernels = false;  // CUDA events around every kernel of the step (per-category stats)
+};
+
+// Kernel categories for per-step statistics (launch counts always; times when profiling).
+enum KernelCat : int { K_GEMM = 0, K_ATTN_FWD, K_ATTN_BWD, K_LAYERNORM, K_MISC, K_ADAM, K_NCAT };
+struct KernelStats {
+    double ms[K_NCAT] = {};
+    double work[K_NCAT] = {};  // flops (GEMM, attention) or bytes (HBM-bound kernels)
+    int64_t launches[K_NCAT] = {};
 };
 
 // Element offsets of one transformer layer inside a stage's flat parameter vector.
@@ -65,6 +74,9 @@ public:
     // per-task [start,end] seconds of the last step (tasks of other devices: NaN)
     void timeline(double* start, double* end) const;
     size_t device_bytes() const { return dev_bytes_; }
+    const KernelStats& kernel_stats() const;  // of the last step
+    cudaStream_t compute_stream() const;
+    void set_flags(bool record_timeline, bool profile_kernels);
 
 private:
     struct Impl;

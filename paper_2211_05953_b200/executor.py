@@ -22,6 +22,8 @@ from . import pipesim as ps
 from .model import GPTConfig
 
 SKIP_OPTIMIZER = 1
+PROFILE_KERNELS = 2
+KERNEL_CATEGORIES = ("gemm", "attention_fwd", "attention_bwd", "layernorm", "misc", "adam")
 
 
 def _check(st):
@@ -50,14 +52,14 @@ class Executor:
                  device: Optional[int] = None, uids: Optional[bytes] = None, record_timeline: bool = False,
                  seed: int = 1234, lr: float = 1e-4, beta1: float = 0.9, beta2: float = 0.95,
                  eps: float = 1e-8, weight_decay: float = 0.0, init_std: float = 0.02,
-                 skip_optimizer: bool = False):
+                 skip_optimizer: bool = False, profile_kernels: bool = False):
         if isinstance(model, GPTConfig):
             model = model_spec(model)
         self.model, self.config, self.rank, self.world = model, config, rank, world
         if device is None:
             device = int(os.environ.get("LOCAL_RANK", rank))
         opts = N.ExecOptsC(device, int(record_timeline), seed, lr, beta1, beta2, eps, weight_decay, init_std,
-                           SKIP_OPTIMIZER if skip_optimizer else 0)
+                           (SKIP_OPTIMIZER if skip_optimizer else 0) | (PROFILE_KERNELS if profile_kernels else 0))
         h = C.c_void_p()
         ubuf = C.create_string_buffer(uids, len(uids)) if uids else None
         _check(N.lib().bfpp_exec_create(C.byref(model._c()), C.byref(config._c()), C.byref(opts), rank, world,
@@ -118,6 +120,23 @@ class Executor:
         e = np.zeros(n)
         _check(N.lib().bfpp_exec_timeline(self._h, s.ctypes.data, e.ctypes.data))
         return s, e
+
+    @property
+    def stream_handle(self) -> int:
+        """cudaStream_t of the executor's compute stream (every step starts and ends on it)."""
+        return N.lib().bfpp_exec_stream(self._h)
+
+    def set_flags(self, record_timeline: bool = False, profile_kernels: bool = False):
+        _check(N.lib().bfpp_exec_set_flags(self._h, int(record_timeline), int(profile_kernels)))
+
+    def kernel_stats(self):
+        """{category: (launches, ms, work)} of the last step (ms/work need profile_kernels)."""
+        out = {}
+        for i, name in enumerate(KERNEL_CATEGORIES):
+            n, ms, w = C.c_int64(), C.c_double(), C.c_double()
+            _check(N.lib().bfpp_exec_kernel_stats(self._h, i, C.byref(n), C.byref(ms), C.byref(w)))
+            out[name] = (n.value, ms.value, w.value)
+        return out
 
     def close(self):
         if getattr(self, "_h", None):
