@@ -153,6 +153,7 @@ struct Executor::Impl {
     int dev = 0;
     cudaStream_t st[S_N] = {};
     ncclComm_t dp_comm = nullptr, fwd_out = nullptr, fwd_in = nullptr, bwd_out = nullptr, bwd_in = nullptr;
+    std::vector<std::pair<size_t, ncclComm_t>> comm_ids;  // (global uid index, comm) for ordered teardown
     std::vector<void*> allocs;
     std::vector<LocalStage> local;  // index c
     bf16* slots[2] = {nullptr, nullptr};
@@ -229,6 +230,13 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
             NK(ncclCommInitRank(&I.bwd_in, 2, uids[edge(dp_rank_, (pp_rank_ + 1) % p_, 1)], 1));
         }
         NK(ncclGroupEnd());
+        if (I.dp_comm) I.comm_ids.push_back({static_cast<size_t>(1 + pp_rank_), I.dp_comm});
+        if (p_ >= 2) {
+            I.comm_ids.push_back({edge(dp_rank_, pp_rank_, 0), I.fwd_out});
+            I.comm_ids.push_back({edge(dp_rank_, (pp_rank_ - 1 + p_) % p_, 0), I.fwd_in});
+            I.comm_ids.push_back({edge(dp_rank_, pp_rank_, 1), I.bwd_out});
+            I.comm_ids.push_back({edge(dp_rank_, (pp_rank_ + 1) % p_, 1), I.bwd_in});
+        }
     }
 
     // ---- parameters, gradients, optimizer shards ----
@@ -455,8 +463,12 @@ Executor::~Executor() {
     Impl& I = *impl_;
     cudaSetDevice(I.dev);
     cudaDeviceSynchronize();
-    for (ncclComm_t cm : {I.dp_comm, I.fwd_out, I.fwd_in, I.bwd_out, I.bwd_in})
-        if (cm) ncclCommDestroy(cm);
+    // Tear communicators down in ascending global id order so that the two members of
+    // every 2-rank edge communicator finalise it at the same point (the forward ring
+    // d -> d+1 and its wrap cross, so per-rank "out before in" orders would cycle).
+    std::vector<std::pair<size_t, ncclComm_t>> comms(I.comm_ids.begin(), I.comm_ids.end());
+    std::sort(comms.begin(), comms.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    for (auto& kv : comms) ncclCommDestroy(kv.second);
     for (auto e : I.done)
         if (e) cudaEventDestroy(e);
     for (auto e : I.t_start)

@@ -1,0 +1,70 @@
+"""TEST INFRASTRUCTURE: one rank of a multi-GPU executor run (launched by torchrun from
+tests/test_multi_gpu.py). Writes its run_rank() result to <out>/rank<r>.pkl."""
+import argparse
+import os
+import pickle
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+sys.path.insert(0, os.path.dirname(HERE))
+
+import exec_harness as H  # noqa: E402
+from paper_2211_05953_b200 import pipesim as ps  # noqa: E402
+
+CASES = {
+    # BASELINE configs[0]: tiny BF, 2 stages x 2 loops, 4 micro-batches, 2 DP ranks (fully sharded)
+    "tiny_bf_pp2x2_dp2_fs": dict(n_dp=2, n_pp=2, n_loop=2, n_mb=4, dp_variant="DP_FS", schedule="BreadthFirst"),
+    "bf_pp2x2_mb4": dict(n_dp=1, n_pp=2, n_loop=2, n_mb=4, dp_variant="DP0", schedule="BreadthFirst"),
+    "df_pp2x2_mb4": dict(n_dp=1, n_pp=2, n_loop=2, n_mb=4, dp_variant="DP0", schedule="DepthFirst"),
+    "gpipe_pp2_mb3": dict(n_dp=1, n_pp=2, n_loop=1, n_mb=3, dp_variant="DP0", schedule="GPipe"),
+    "1f1b_pp2_mb4": dict(n_dp=1, n_pp=2, n_loop=1, n_mb=4, dp_variant="DP0", schedule="OneFOneB"),
+    "bf_pp1x4_dp2_fs": dict(n_dp=2, n_pp=1, n_loop=4, n_mb=2, dp_variant="DP_FS", schedule="BreadthFirst"),
+    "np_dp2_dp0": dict(n_dp=2, n_pp=1, n_loop=1, n_mb=2, dp_variant="DP0", schedule="NoPipeline"),
+    "np_dp2_ps": dict(n_dp=2, n_pp=1, n_loop=1, n_mb=2, dp_variant="DP_PS", schedule="NoPipeline"),
+    "gpipe_dp2_fs_mb2": dict(n_dp=2, n_pp=1, n_loop=1, n_mb=2, dp_variant="DP_FS", schedule="GPipe"),
+    "df_pp2x2_dp2_fs": dict(n_dp=2, n_pp=2, n_loop=2, n_mb=4, dp_variant="DP_FS", schedule="DepthFirst"),
+    "bf_pp4x1_mb4": dict(n_dp=1, n_pp=4, n_loop=1, n_mb=4, dp_variant="DP0", schedule="BreadthFirst"),
+    "1f1b_pp2_dp2_fs": dict(n_dp=2, n_pp=2, n_loop=1, n_mb=2, dp_variant="DP_FS", schedule="OneFOneB"),
+}
+
+
+def config_of(name):
+    c = dict(CASES[name])
+    c["dp_variant"] = ps.DpVariant[c["dp_variant"]]
+    c["schedule"] = ps.Schedule[c["schedule"]]
+    return ps.ParallelConfig(**c)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--case", required=True)
+    ap.add_argument("--out", required=True)
+    a = ap.parse_args()
+    import faulthandler
+    faulthandler.dump_traceback_later(int(os.environ.get("BFPP_HANG_DUMP_S", "100")), exit=True)
+    import torch
+    import torch.distributed as dist
+    from paper_2211_05953_b200.executor import Executor, comm_ids
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(local)
+    config = config_of(a.case)
+    cfg = H.TINY
+    params, tokens = H.make_case(cfg, config)
+
+    def factory(**kw):
+        obj = [comm_ids(config) if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return Executor(cfg, config, rank=rank, world=world, device=local, uids=obj[0], **kw)
+
+    res = H.run_rank(factory, cfg, config, params, tokens, rank)
+    with open(os.path.join(a.out, f"rank{rank}.pkl"), "wb") as f:
+        pickle.dump(res, f)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
