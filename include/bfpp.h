@@ -228,6 +228,8 @@ int bfpp_exec_set_params(bfpp_exec* e, int64_t stage, const float* host, int64_t
 int bfpp_exec_get_params(bfpp_exec* e, int64_t stage, float* host, int64_t n, int64_t* lo, int64_t* hi);
 int bfpp_exec_get_grads(bfpp_exec* e, int64_t stage, float* host, int64_t n, int64_t* lo, int64_t* hi);
 int bfpp_exec_zero_grads(bfpp_exec* e);
+/* bf16 compute weights (resident copy, or this rank's all-gather source shard under DP_FS) */
+int bfpp_exec_get_weights16(bfpp_exec* e, int64_t stage, uint16_t* host, int64_t n, int64_t* lo, int64_t* hi);
 /* measured [start, end] (seconds from the step origin) of this rank's tasks in the last
  * step; tasks of other devices are NaN. Arrays have bfpp_graph_n_tasks entries. */
 int bfpp_exec_timeline(const bfpp_exec* e, double* start, double* end);

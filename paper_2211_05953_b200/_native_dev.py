@@ -62,6 +62,7 @@ PROTOS.update({
     "bfpp_exec_get_params": (C.c_int, [_P, _I64, _P, _I64, C.POINTER(_I64), C.POINTER(_I64)]),
     "bfpp_exec_get_grads": (C.c_int, [_P, _I64, _P, _I64, C.POINTER(_I64), C.POINTER(_I64)]),
     "bfpp_exec_zero_grads": (C.c_int, [_P]),
+    "bfpp_exec_get_weights16": (C.c_int, [_P, _I64, _P, _I64, C.POINTER(_I64), C.POINTER(_I64)]),
     "bfpp_exec_timeline": (C.c_int, [_P, _P, _P]),
     "bfpp_exec_stream": (_P, [_P]),
     "bfpp_exec_set_flags": (C.c_int, [_P, _I32, _I32]),

@@ -86,6 +86,9 @@ int bfpp_exec_get_params(bfpp_exec* e, int64_t stage, float* host, int64_t n, in
 int bfpp_exec_get_grads(bfpp_exec* e, int64_t stage, float* host, int64_t n, int64_t* lo, int64_t* hi) {
     return guarded([&] { e->x->get_grads(stage, host, n, lo, hi); });
 }
+int bfpp_exec_get_weights16(bfpp_exec* e, int64_t stage, uint16_t* host, int64_t n, int64_t* lo, int64_t* hi) {
+    return guarded([&] { e->x->get_weights16(stage, host, n, lo, hi); });
+}
 int bfpp_exec_zero_grads(bfpp_exec* e) {
     return guarded([&] { e->x->zero_grads(); });
 }

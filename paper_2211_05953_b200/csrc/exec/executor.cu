@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstring>
 #include <map>
+#include <set>
 #include <stdexcept>
 #include <string>
 
@@ -451,6 +452,43 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
         I.order.push_back(te);
         CK(cudaEventCreateWithFlags(&I.done[static_cast<size_t>(id)], cudaEventDisableTiming));
     }
+    // Host enqueue order: a topological order of this rank's tasks over the explicit waits
+    // (graph deps on other streams + the executor's gradient-buffer resource deps) and the
+    // per-stream FIFO order, ties broken by simulated start. Every event is then recorded
+    // before any stream waits on it.
+    {
+        const size_t m = I.order.size();
+        std::map<TaskId, size_t> pos;
+        for (size_t i = 0; i < m; ++i) pos[I.order[i].id] = i;
+        std::vector<std::vector<size_t>> succ(m);
+        std::vector<int> indeg(m, 0);
+        std::vector<long> last(S_N, -1);
+        for (size_t i = 0; i < m; ++i) {
+            const TaskExec& te = I.order[i];
+            if (last[te.stream] >= 0) {
+                succ[static_cast<size_t>(last[te.stream])].push_back(i);
+                ++indeg[i];
+            }
+            last[te.stream] = static_cast<long>(i);
+            for (TaskId w : te.waits) {
+                succ[pos.at(w)].push_back(i);
+                ++indeg[i];
+            }
+        }
+        std::set<size_t> ready;
+        for (size_t i = 0; i < m; ++i)
+            if (indeg[i] == 0) ready.insert(i);
+        std::vector<TaskExec> sorted;
+        while (!ready.empty()) {
+            const size_t i = *ready.begin();
+            ready.erase(ready.begin());
+            sorted.push_back(I.order[i]);
+            for (size_t j : succ[i])
+                if (--indeg[j] == 0) ready.insert(j);
+        }
+        if (sorted.size() != m) throw SimError("executor: cyclic local dependencies");
+        I.order = std::move(sorted);
+    }
     set_flags(o.record_timeline, o.profile_kernels);
     CK(cudaEventCreate(&I.origin));
     CK(cudaEventCreateWithFlags(&I.step_end, cudaEventDisableTiming));
@@ -793,33 +831,36 @@ LocalStage& find_local(std::vector<LocalStage>& v, i64 stage) {
 }  // namespace
 
 void Executor::set_params(i64 stage, const float* host, int64_t n) {
+    // All copies are stream-ordered on the compute stream: a synchronous cudaMemcpy from
+    // pageable memory may return before its DMA lands, and the executor's streams do not
+    // synchronise with the legacy default stream.
     Impl& I = *impl_;
     CK(cudaSetDevice(I.dev));
     sync();
+    cudaStream_t cs = I.st[S_COMPUTE];
     LocalStage& ls = find_local(I.local, stage);
     const StageLayout& L = layouts_[static_cast<size_t>(stage)];
     if (n != L.numel) throw SpecError("set_params: size mismatch with the stage layout");
     std::vector<float> padded(static_cast<size_t>(L.padded), 0.f);
     std::memcpy(padded.data(), host, static_cast<size_t>(n) * 4);
-    CK(cudaMemcpy(ls.master, padded.data() + ls.shard_lo, static_cast<size_t>(ls.shard_n) * 4,
-                  cudaMemcpyHostToDevice));
-    CK(cudaMemset(ls.m, 0, static_cast<size_t>(ls.shard_n) * 4));
-    CK(cudaMemset(ls.v, 0, static_cast<size_t>(ls.shard_n) * 4));
-    if (ls.w16_shard) f32_to_bf16(ls.master, ls.w16_shard, ls.shard_n, I.st[S_COMPUTE]);
+    CK(cudaMemcpyAsync(ls.master, padded.data() + ls.shard_lo, static_cast<size_t>(ls.shard_n) * 4,
+                       cudaMemcpyHostToDevice, cs));
+    CK(cudaMemsetAsync(ls.m, 0, static_cast<size_t>(ls.shard_n) * 4, cs));
+    CK(cudaMemsetAsync(ls.v, 0, static_cast<size_t>(ls.shard_n) * 4, cs));
+    if (ls.w16_shard) f32_to_bf16(ls.master, ls.w16_shard, ls.shard_n, cs);
+    float* tmp = nullptr;
     if (ls.w16) {
         if (ls.shard_n == L.padded) {
-            f32_to_bf16(ls.master, ls.w16, L.padded, I.st[S_COMPUTE]);
+            f32_to_bf16(ls.master, ls.w16, L.padded, cs);
         } else {  // replicated weights with a sharded optimizer (DP_PS): convert the full vector
-            float* tmp = nullptr;
             CK(cudaMalloc(&tmp, static_cast<size_t>(L.padded) * 4));
-            CK(cudaMemcpy(tmp, padded.data(), static_cast<size_t>(L.padded) * 4, cudaMemcpyHostToDevice));
-            f32_to_bf16(tmp, ls.w16, L.padded, I.st[S_COMPUTE]);
-            CK(cudaStreamSynchronize(I.st[S_COMPUTE]));
-            CK(cudaFree(tmp));
+            CK(cudaMemcpyAsync(tmp, padded.data(), static_cast<size_t>(L.padded) * 4, cudaMemcpyHostToDevice, cs));
+            f32_to_bf16(tmp, ls.w16, L.padded, cs);
         }
     }
+    CK(cudaStreamSynchronize(cs));
+    if (tmp) CK(cudaFree(tmp));
     I.step_no = 0;
-    CK(cudaStreamSynchronize(I.st[S_COMPUTE]));
 }
 
 void Executor::get_params(i64 stage, float* host, int64_t n, int64_t* lo, int64_t* hi) {
@@ -851,6 +892,25 @@ void Executor::get_grads(i64 stage, float* host, int64_t n, int64_t* lo, int64_t
         CK(cudaMemcpy(host, ls.grad, static_cast<size_t>(L.numel) * 4, cudaMemcpyDeviceToHost));
         *lo = 0;
         *hi = L.numel;
+    }
+}
+
+void Executor::get_weights16(i64 stage, uint16_t* host, int64_t n, int64_t* lo, int64_t* hi) {
+    Impl& I = *impl_;
+    sync();
+    CK(cudaDeviceSynchronize());
+    LocalStage& ls = find_local(I.local, stage);
+    const StageLayout& L = layouts_[static_cast<size_t>(stage)];
+    if (n < L.numel) throw SpecError("get_weights16: buffer too small");
+    if (ls.w16) {
+        CK(cudaMemcpy(host, ls.w16, static_cast<size_t>(L.numel) * 2, cudaMemcpyDeviceToHost));
+        *lo = 0;
+        *hi = L.numel;
+    } else {
+        const int64_t a = ls.shard_lo, b = std::min(ls.shard_lo + ls.shard_n, L.numel);
+        if (b > a) CK(cudaMemcpy(host + a, ls.w16_shard, static_cast<size_t>(b - a) * 2, cudaMemcpyDeviceToHost));
+        *lo = a;
+        *hi = std::max(a, b);
     }
 }
 

@@ -71,6 +71,8 @@ public:
     void get_params(i64 stage, float* host, int64_t n, int64_t* lo, int64_t* hi);
     void get_grads(i64 stage, float* host, int64_t n, int64_t* lo, int64_t* hi);
     void zero_grads();
+    // bf16 compute weights: resident copy (full) or this rank's all-gather source shard (DP_FS)
+    void get_weights16(i64 stage, uint16_t* host, int64_t n, int64_t* lo, int64_t* hi);
     // per-task [start,end] seconds of the last step (tasks of other devices: NaN)
     void timeline(double* start, double* end) const;
     size_t device_bytes() const { return dev_bytes_; }

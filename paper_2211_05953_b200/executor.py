@@ -111,6 +111,14 @@ class Executor:
     def get_stage_grads(self, stage: int):
         return self._get(N.lib().bfpp_exec_get_grads, stage)
 
+    def get_stage_weights16(self, stage: int):
+        """(bf16 compute weights as float32, lo, hi): the resident copy or this rank's DP_FS shard."""
+        n = self.stage_numel(stage)
+        raw = np.zeros(n, dtype=np.uint16)
+        lo, hi = C.c_int64(), C.c_int64()
+        _check(N.lib().bfpp_exec_get_weights16(self._h, stage, raw.ctypes.data, n, C.byref(lo), C.byref(hi)))
+        return (raw.astype(np.uint32) << 16).view(np.float32), lo.value, hi.value
+
     def zero_grads(self):
         _check(N.lib().bfpp_exec_zero_grads(self._h))
 

@@ -36,7 +36,11 @@ def run_rank(executor_factory, cfg, config, params, tokens, rank):
     dp = rank // config.n_pp
     ex = executor_factory(skip_optimizer=True)
     for s in ex.local_stages:
-        ex.set_stage_params(s, flatten_stage(params, cfg, s, n_stage))
+        flat = flatten_stage(params, cfg, s, n_stage)
+        ex.set_stage_params(s, flat)
+        w16, lo, hi = ex.get_stage_weights16(s)
+        want = torch_bf16(flat[lo:hi])
+        assert np.array_equal(w16[lo:hi], want), f"stage {s}: bf16 compute weights differ after set_params"
     loss = ex.step(tokens[dp])
     grads = {s: ex.get_stage_grads(s) for s in ex.local_stages}
     ex.close()
@@ -45,8 +49,19 @@ def run_rank(executor_factory, cfg, config, params, tokens, rank):
         ex.set_stage_params(s, flatten_stage(params, cfg, s, n_stage))
     loss2 = ex.step(tokens[dp])
     newp = {s: ex.get_stage_params(s) for s in ex.local_stages}
+    for s in ex.local_stages:  # the bf16 copy the next step computes with is the rounded master
+        w16, lo, hi = ex.get_stage_weights16(s)
+        p, plo, phi = newp[s]
+        a, b = max(lo, plo), min(hi, phi)
+        assert np.array_equal(w16[a:b], torch_bf16(p[a:b])), f"stage {s}: bf16 weights != bf16(master)"
     ex.close()
     return {"loss": loss, "loss2": loss2, "grads": grads, "params": newp}
+
+
+def torch_bf16(x):
+    """Round-to-nearest-even float32 -> bf16 -> float32 (the kernels' __float2bfloat16_rn)."""
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(x, np.float32)).bfloat16().float().numpy()
 
 
 def oracle(cfg, config, params, tokens):
