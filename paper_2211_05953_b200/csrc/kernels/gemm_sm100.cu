@@ -1,5 +1,6 @@
 // Persistent warp-specialised bf16 GEMM for sm_100a: TMA -> SMEM (SWIZZLE_128B)
-// -> tcgen05.mma (accumulator in TMEM, double-buffered) -> fused epilogue.
+// -> tcgen05.mma (accumulator in TMEM, double-buffered) -> fused epilogue ->
+// SMEM staging -> TMA store (or TMA reduce-add for f32 gradient accumulation).
 //
 //   D[M,N] = sum_k A[m,k] * B[n,k]      (f32 accumulate)
 //
@@ -8,8 +9,9 @@
 // forms are then: forward X.W^T (K,K), data-grad dY.W (K,MN) and weight-grad
 // dY^T.X (MN,MN), with no explicit transposes.
 //
-// Warp roles (192 threads): warp 0 = TMA producer, warp 1 = MMA issuer (+ TMEM
-// owner), warps 2..5 = epilogue (TMEM lane quarter = warp % 4).
+// Warp roles (320 threads): warp 0 = TMA producer, warp 1 = MMA issuer (+ TMEM
+// owner), warps 2..9 = epilogue. Epilogue warp w reads TMEM lane quarter w % 4
+// and every other 128-byte column strip of the tile ("half" = (w - 2) / 4).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -30,22 +32,21 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int kStages = 4;
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 64 + 32 * kEpiWarps;
+constexpr int kStageBytesOut = 32 * 128;  // one [32 rows x 128 B] TMA store box per epilogue warp
 
 __device__ __forceinline__ float gelu_f(float x) {
     const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-    return 0.5f * x * (1.f + tanhf(k0 * (x + k1 * x * x * x)));
+    return 0.5f * x * (1.f + ptx::tanh_fast(k0 * (x + k1 * x * x * x)));
 }
 __device__ __forceinline__ float dgelu_f(float x) {
     const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-    const float u = k0 * (x + k1 * x * x * x);
-    const float t = tanhf(u);
+    const float t = ptx::tanh_fast(k0 * (x + k1 * x * x * x));
     return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x * x);
 }
 
 struct EpiArgs {
-    void* d;
-    int64_t ldd;
     const __nv_bfloat16* aux;  // residual / gelu pre-activation input
     int64_t ldaux;
     __nv_bfloat16* aux_out;    // gelu pre-activation output
@@ -59,14 +60,34 @@ struct Smem {
     static constexpr int kABytes = BM * BK * 2;
     static constexpr int kBBytes = BN * BK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kBarOffset = kStages * kStageBytes;
+    static constexpr int kOutOffset = kStages * kStageBytes;
+    static constexpr int kBarOffset = kOutOffset + kEpiWarps * kStageBytesOut;
     static constexpr int kBytes = kBarOffset + 256 + 1024;  // barriers + alignment slack
 };
 
+__device__ __forceinline__ void load_row64_bf16(const __nv_bfloat16* p, int valid, float (&v)[64]) {
+    if (valid >= 64) {
+#pragma unroll
+        for (int j = 0; j < 64; j += 8) {
+            uint4 raw = *reinterpret_cast<const uint4*>(p + j);
+            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                float2 f = __bfloat1622float2(h[u]);
+                v[j + 2 * u] = f.x;
+                v[j + 2 * u + 1] = f.y;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 64; ++j) v[j] = j < valid ? __bfloat162float(p[j]) : 0.f;
+    }
+}
+
 template <int BN, int A_MN, int B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
-                EpiArgs ep) {
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmD, int M, int N, int K, EpiArgs ep) {
     using S = Smem<BN>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -86,13 +107,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch(&tmA);
         ptx::tma_prefetch(&tmB);
+        ptx::tma_prefetch(&tmD);
         for (int s = 0; s < kStages; ++s) {
             ptx::mbar_init(&full[s], 1);
             ptx::mbar_init(&empty[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
             ptx::mbar_init(&tfull[b], 1);
-            ptx::mbar_init(&tempty[b], 4);
+            ptx::mbar_init(&tempty[b], kEpiWarps);
         }
         ptx::fence_barrier_init();
     }
@@ -117,13 +139,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int k0 = kb * BK;
                     if (A_MN) {
 #pragma unroll
-                        for (int i = 0; i < BM / 64; ++i) ptx::tma_load_2d(sa + i * 64 * BK * 2, &tmA, &full[stage], m0 + 64 * i, k0);
+                        for (int i = 0; i < BM / 64; ++i)
+                            ptx::tma_load_2d(sa + i * 64 * BK * 2, &tmA, &full[stage], m0 + 64 * i, k0);
                     } else {
                         ptx::tma_load_2d(sa, &tmA, &full[stage], k0, m0);
                     }
                     if (B_MN) {
 #pragma unroll
-                        for (int i = 0; i < BN / 64; ++i) ptx::tma_load_2d(sb + i * 64 * BK * 2, &tmB, &full[stage], n0 + 64 * i, k0);
+                        for (int i = 0; i < BN / 64; ++i)
+                            ptx::tma_load_2d(sb + i * 64 * BK * 2, &tmB, &full[stage], n0 + 64 * i, k0);
                     } else {
                         ptx::tma_load_2d(sb, &tmB, &full[stage], k0, n0);
                     }
@@ -171,102 +195,112 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else {
-        // ===== epilogue: TMEM -> registers -> fused op -> global =====
-        const int q = warp & 3;
+        // ===== epilogue: TMEM -> registers -> fused op -> swizzled SMEM -> TMA store =====
+        const int ew = warp - 2;
+        const int q = warp & 3;        // TMEM lane quarter (hardware: warp id % 4)
+        const int half = ew >> 2;      // which alternate 128-byte column strips this warp owns
+        uint8_t* stage_out = smem + S::kOutOffset + ew * kStageBytesOut;
+        const bool f32_out = ep.epi == GEMM_EPI_F32;
+        const int cw = f32_out ? 32 : 64;  // tile columns per 128-byte strip
+        const int n_strips = BN / cw;
         int it = 0;
         for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
             const int m0 = (t % m_tiles) * BM, n0 = (t / m_tiles) * BN;
-            ptx::mbar_wait(&tfull[acc], acc_phase);
-            ptx::tc_fence_after();
             const int row = m0 + q * 32 + lane;
             const bool row_ok = row < M;
-#pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
-                uint32_t r[32];
-                ptx::tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + acc * BN + c * 32, r);
-                ptx::tmem_ld_wait();
-                const int col0 = n0 + c * 32;
-                if (!row_ok || col0 >= N) continue;
-                const bool full_chunk = col0 + 32 <= N;
-                float v[32];
+            ptx::mbar_wait(&tfull[acc], acc_phase);
+            ptx::tc_fence_after();
+            for (int sidx = half; sidx < n_strips; sidx += 2) {
+                const int col0 = n0 + sidx * cw;
+                const uint32_t tcol = tmem_base + ((q * 32) << 16) + acc * BN + sidx * cw;
+                float v[64];
+                float a[64];
+                const bool need_aux = (ep.epi == GEMM_EPI_RESID || ep.epi == GEMM_EPI_DGELU);
+                const int valid = row_ok ? min(64, N - col0) : 0;
+                // issue the aux loads before the TMEM loads so both latencies overlap
+                if (need_aux && valid > 0) load_row64_bf16(ep.aux + static_cast<int64_t>(row) * ep.ldaux + col0, valid, a);
+                {
+                    uint32_t r[32];
+                    ptx::tmem_ld_32x32b_x32(tcol, r);
+                    if (!f32_out) {
+                        uint32_t r2[32];
+                        ptx::tmem_ld_32x32b_x32(tcol + 32, r2);
+                        ptx::tmem_ld_wait();
 #pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-                if (ep.epi == GEMM_EPI_F32) {
-                    float* d = static_cast<float*>(ep.d) + static_cast<int64_t>(row) * ep.ldd + col0;
-                    if (full_chunk) {
-#pragma unroll
-                        for (int j = 0; j < 32; j += 4) {
-                            float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-                            if (ep.accumulate) {
-                                float4 p = *reinterpret_cast<const float4*>(d + j);
-                                o.x += p.x;
-                                o.y += p.y;
-                                o.z += p.z;
-                                o.w += p.w;
-                            }
-                            *reinterpret_cast<float4*>(d + j) = o;
-                        }
+                        for (int j = 0; j < 32; ++j) v[32 + j] = __uint_as_float(r2[j]);
                     } else {
-                        for (int j = 0; j < 32 && col0 + j < N; ++j) d[j] = ep.accumulate ? d[j] + v[j] : v[j];
+                        ptx::tmem_ld_wait();
                     }
-                    continue;
-                }
-                __nv_bfloat16* d = static_cast<__nv_bfloat16*>(ep.d) + static_cast<int64_t>(row) * ep.ldd + col0;
-                if (ep.epi == GEMM_EPI_RESID || ep.epi == GEMM_EPI_DGELU) {
-                    const __nv_bfloat16* a = ep.aux + static_cast<int64_t>(row) * ep.ldaux + col0;
-                    if (full_chunk) {
 #pragma unroll
-                        for (int j = 0; j < 32; j += 8) {
-                            uint4 raw = *reinterpret_cast<const uint4*>(a + j);
-                            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+                    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+                }
+                if (sidx + 2 >= n_strips) {
+                    // this warp's last TMEM read of the tile: hand the accumulator back to the MMA warp
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+                }
+                // staging buffer reuse: the previous TMA store must have finished reading it
+                if (lane == 0) ptx::bulk_wait_read<0>();
+                __syncwarp();
+                uint8_t* rowp = stage_out + lane * 128;
+                if (f32_out) {
+#pragma unroll
+                    for (int c = 0; c < 8; ++c)
+                        *reinterpret_cast<float4*>(rowp + ((c ^ (lane & 7)) << 4)) =
+                            make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+                } else {
+                    if (ep.epi == GEMM_EPI_RESID) {
+#pragma unroll
+                        for (int j = 0; j < 64; ++j) v[j] += a[j];
+                    } else if (ep.epi == GEMM_EPI_DGELU) {
+#pragma unroll
+                        for (int j = 0; j < 64; ++j) v[j] *= dgelu_f(a[j]);
+                    } else if (ep.epi == GEMM_EPI_GELU) {
+                        // pre-activation stored as bf16; gelu evaluated on the stored value
+                        __nv_bfloat16* pre = ep.aux_out + static_cast<int64_t>(row) * ep.ldaux_out + col0;
+#pragma unroll
+                        for (int j = 0; j < 64; j += 8) {
+                            uint4 o;
+                            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
 #pragma unroll
                             for (int u = 0; u < 4; ++u) {
-                                float2 f = __bfloat1622float2(h[u]);
-                                if (ep.epi == GEMM_EPI_RESID) {
-                                    v[j + 2 * u] += f.x;
-                                    v[j + 2 * u + 1] += f.y;
-                                } else {
-                                    v[j + 2 * u] *= dgelu_f(f.x);
-                                    v[j + 2 * u + 1] *= dgelu_f(f.y);
-                                }
+                                h[u] = __floats2bfloat162_rn(v[j + 2 * u], v[j + 2 * u + 1]);
+                                const float2 f = __bfloat1622float2(h[u]);
+                                v[j + 2 * u] = gelu_f(f.x);
+                                v[j + 2 * u + 1] = gelu_f(f.y);
+                            }
+                            if (valid >= j + 8) {
+                                *reinterpret_cast<uint4*>(pre + j) = o;
+                            } else {
+                                for (int u = 0; u < 8; ++u)
+                                    if (j + u < valid) pre[j + u] = reinterpret_cast<__nv_bfloat16*>(&o)[u];
                             }
                         }
-                    } else {
-                        for (int j = 0; j < 32 && col0 + j < N; ++j) {
-                            float f = __bfloat162float(a[j]);
-                            v[j] = ep.epi == GEMM_EPI_RESID ? v[j] + f : v[j] * dgelu_f(f);
-                        }
                     }
-                }
-                if (ep.epi == GEMM_EPI_GELU) {
-                    __nv_bfloat16* pre = ep.aux_out + static_cast<int64_t>(row) * ep.ldaux_out + col0;
-                    // keep the pre-activation exactly as stored (bf16) so dgelu sees the same value
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        __nv_bfloat16 b = __float2bfloat16_rn(v[j]);
-                        if (full_chunk || col0 + j < N) pre[j] = b;
-                        v[j] = gelu_f(__bfloat162float(b));
-                    }
-                }
-                if (full_chunk) {
-#pragma unroll
-                    for (int j = 0; j < 32; j += 8) {
+                    for (int c = 0; c < 8; ++c) {
                         uint4 o;
                         __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) h[u] = __floats2bfloat162_rn(v[j + 2 * u], v[j + 2 * u + 1]);
-                        *reinterpret_cast<uint4*>(d + j) = o;
+                        for (int u = 0; u < 4; ++u) h[u] = __floats2bfloat162_rn(v[8 * c + 2 * u], v[8 * c + 2 * u + 1]);
+                        *reinterpret_cast<uint4*>(rowp + ((c ^ (lane & 7)) << 4)) = o;
                     }
-                } else {
-                    for (int j = 0; j < 32 && col0 + j < N; ++j) d[j] = __float2bfloat16_rn(v[j]);
+                }
+                ptx::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0 && col0 < N && m0 + q * 32 < M) {
+                    if (f32_out && ep.accumulate)
+                        ptx::tma_reduce_add_2d(&tmD, stage_out, col0, m0 + q * 32);
+                    else
+                        ptx::tma_store_2d(&tmD, stage_out, col0, m0 + q * 32);
+                    ptx::bulk_commit();
                 }
             }
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
         }
+        if (lane == 0) ptx::bulk_wait<0>();
     }
     __syncthreads();
     if (warp == 1) ptx::tmem_dealloc<2 * BN>(tmem_base);
@@ -287,17 +321,19 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-// 2-D bf16 tensor map over a row-major [rows][ld] matrix with `inner` valid
-// columns; box = {64 (inner), box_rows}, SWIZZLE_128B, OOB -> zero.
-CUtensorMap make_map(const void* ptr, int64_t inner, int64_t rows, int64_t ld, int box_rows) {
+// 2-D tensor map over a row-major [rows][ld] matrix with `inner` valid columns;
+// box = {128 B of inner, box_rows}, SWIZZLE_128B, OOB loads -> zero, OOB stores dropped.
+CUtensorMap make_map(const void* ptr, int64_t inner, int64_t rows, int64_t ld, int box_rows, bool f32 = false) {
     CUtensorMap m;
+    const int esz = f32 ? 4 : 2;
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(rows)};
-    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
-    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * esz)};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / esz), static_cast<cuuint32_t>(box_rows)};
     cuuint32_t estr[2] = {1, 1};
-    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r = encode_fn()(&m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                             const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
     return m;
 }
@@ -316,8 +352,10 @@ template <int BN, int A_MN, int B_MN>
 void launch(const GemmArgs& g, cudaStream_t st) {
     CUtensorMap ta = A_MN ? make_map(g.A, g.M, g.K, g.lda, BK) : make_map(g.A, g.K, g.M, g.lda, BM);
     CUtensorMap tb = B_MN ? make_map(g.B, g.N, g.K, g.ldb, BK) : make_map(g.B, g.K, g.N, g.ldb, BN);
-    EpiArgs ep{g.D, g.ldd, static_cast<const __nv_bfloat16*>(g.aux), g.ldaux,
-               static_cast<__nv_bfloat16*>(g.aux_out), g.ldaux_out, g.epilogue, g.accumulate};
+    const bool f32 = g.epilogue == GEMM_EPI_F32;
+    CUtensorMap td = make_map(g.D, g.N, g.M, g.ldd, 32, f32);
+    EpiArgs ep{static_cast<const __nv_bfloat16*>(g.aux), g.ldaux, static_cast<__nv_bfloat16*>(g.aux_out),
+               g.ldaux_out, g.epilogue, g.accumulate};
     auto kern = gemm_kernel<BN, A_MN, B_MN>;
     static bool configured = false;
     if (!configured) {
@@ -326,7 +364,7 @@ void launch(const GemmArgs& g, cudaStream_t st) {
     }
     const int tiles = static_cast<int>(((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN));
     const int grid = tiles < num_sms() ? tiles : num_sms();
-    kern<<<grid, kThreads, Smem<BN>::kBytes, st>>>(ta, tb, static_cast<int>(g.M), static_cast<int>(g.N),
+    kern<<<grid, kThreads, Smem<BN>::kBytes, st>>>(ta, tb, td, static_cast<int>(g.M), static_cast<int>(g.N),
                                                    static_cast<int>(g.K), ep);
 }
 

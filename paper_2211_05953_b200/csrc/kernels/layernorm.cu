@@ -106,8 +106,8 @@ __global__ void __launch_bounds__(NT) ln_bwd_kernel(const __nv_bfloat16* __restr
                                                     const __nv_bfloat16* __restrict__ gamma, const float* __restrict__ mean,
                                                     const float* __restrict__ rstd,
                                                     const __nv_bfloat16* __restrict__ dres,
-                                                    __nv_bfloat16* __restrict__ dx, float* __restrict__ dgamma,
-                                                    float* __restrict__ dbeta, int rows, int width) {
+                                                    __nv_bfloat16* __restrict__ dx, float* __restrict__ ws,
+                                                    int rows, int width) {
     __shared__ float2 red[NT / 32];
     float pg[V][8], pb[V][8], g[V][8];
 #pragma unroll
@@ -157,16 +157,31 @@ __global__ void __launch_bounds__(NT) ln_bwd_kernel(const __nv_bfloat16* __restr
             store8(dx + off + c, r);
         }
     }
+    // per-block partial column sums -> workspace [gridDim.x][2][width] (reduced by ln_colsum_kernel)
 #pragma unroll
     for (int i = 0; i < V; ++i) {
         const int c = (i * NT + threadIdx.x) * 8;
         if (c >= width) continue;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            atomicAdd(dgamma + c + u, pg[i][u]);
-            atomicAdd(dbeta + c + u, pb[i][u]);
-        }
+        float* wg = ws + static_cast<int64_t>(blockIdx.x) * 2 * width + c;
+        *reinterpret_cast<float4*>(wg) = make_float4(pg[i][0], pg[i][1], pg[i][2], pg[i][3]);
+        *reinterpret_cast<float4*>(wg + 4) = make_float4(pg[i][4], pg[i][5], pg[i][6], pg[i][7]);
+        *reinterpret_cast<float4*>(wg + width) = make_float4(pb[i][0], pb[i][1], pb[i][2], pb[i][3]);
+        *reinterpret_cast<float4*>(wg + width + 4) = make_float4(pb[i][4], pb[i][5], pb[i][6], pb[i][7]);
     }
+}
+
+// dgamma/dbeta (+)= column sums of the per-block partials; one thread per output column,
+// coalesced across the block, deterministic order.
+__global__ void ln_colsum_kernel(const float* __restrict__ ws, int nblk, int width, float* __restrict__ dgamma,
+                                 float* __restrict__ dbeta) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= 2 * width) return;
+    float s = 0.f;
+    for (int b = 0; b < nblk; ++b) s += ws[static_cast<int64_t>(b) * 2 * width + c];
+    if (c < width)
+        dgamma[c] += s;
+    else
+        dbeta[c - width] += s;
 }
 
 int sm_count() {
@@ -205,13 +220,23 @@ void layernorm_bwd(const void* dy, const void* x, const void* gamma_, const floa
     auto DX = static_cast<__nv_bfloat16*>(dx);
     auto gamma = static_cast<const __nv_bfloat16*>(gamma_);
     const int v = (width + 1023) / 1024;
-    // enough blocks to fill the chip a few times over, few enough that the per-block
-    // dgamma/dbeta partials amortise their global atomics over many rows
-    const int blocks = rows < 4 * sm_count() ? rows : 4 * sm_count();
-#define LNB(V_)                                                                                         \
-    if (v <= V_)                                                                                        \
-        return ln_bwd_kernel<V_><<<blocks, NT, 0, st>>>(DY, X, gamma, mean, rstd, R, DX, dgamma, dbeta, rows, \
-                                                        width);
+    // one block per SM: partial dgamma/dbeta stay in registers over ~rows/148 rows, then a
+    // deterministic column reduction (no contended atomics)
+    const int blocks = rows < sm_count() ? rows : sm_count();
+    static float* ws = nullptr;
+    static size_t ws_bytes = 0;
+    const size_t need = static_cast<size_t>(blocks) * 2 * width * sizeof(float);
+    if (need > ws_bytes) {
+        if (ws) cudaFree(ws);
+        if (cudaMalloc(&ws, need) != cudaSuccess) throw std::runtime_error("layernorm: workspace allocation failed");
+        ws_bytes = need;
+    }
+#define LNB(V_)                                                                                           \
+    if (v <= V_) {                                                                                        \
+        ln_bwd_kernel<V_><<<blocks, NT, 0, st>>>(DY, X, gamma, mean, rstd, R, DX, ws, rows, width);        \
+        ln_colsum_kernel<<<(2 * width + 255) / 256, 256, 0, st>>>(ws, blocks, width, dgamma, dbeta);     \
+        return;                                                                                           \
+    }
     LNB(1) LNB(2) LNB(4) LNB(8)
 #undef LNB
     throw std::runtime_error("layernorm: width too large for backward");
