@@ -212,7 +212,15 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
     Impl& I = *impl_;
     I.dev = o.device;
     CK(cudaSetDevice(I.dev));
-    for (int s = 0; s < S_N; ++s) CK(cudaStreamCreateWithFlags(&I.st[s], cudaStreamNonBlocking));
+    // Stream priorities: compute and pipeline hand-offs high, the DP lane (all-gather,
+    // reduce-scatter, Adam) low, so bandwidth-bound optimizer blocks fill gaps instead of
+    // delaying the compute stream's CTAs.
+    {
+        int least = 0, greatest = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        for (int s = 0; s < S_N; ++s)
+            CK(cudaStreamCreateWithPriority(&I.st[s], cudaStreamNonBlocking, s == S_DP ? least : greatest));
+    }
 
     // ---- NCCL communicators (uid layout: see bfpp_exec_n_comm_ids) ----
     const bool fs = c_.n_dp >= 2 && c_.dp_variant == DpVariant::DP_FS;
@@ -597,7 +605,7 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
     };
     auto LNB = [&](cudaStream_t st, const bf16* dy, const bf16* x, const bf16* g, const float* mu, const float* rs,
                    const bf16* dres, bf16* dx, float* dg, float* db) {
-        K(K_LAYERNORM, (dres ? 4 : 3) * Th2, 1, st, [&] {
+        K(K_LAYERNORM, (dres ? 6 : 5) * Th2, 3, st, [&] {
             layernorm_bwd(dy, x, g, mu, rs, dres, dx, dg, db, static_cast<int>(T), static_cast<int>(h), st);
         });
     };
