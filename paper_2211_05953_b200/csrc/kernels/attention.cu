@@ -478,8 +478,8 @@ constexpr int kBwdSmem = (2 * B_BC + 4 * B_BR) * 256 + B_BC * 128 + 4 * B_BR * 4
 
 }  // namespace
 
-void attention_fwd(const void* qkv, void* o, float* lse, int batch, int seq, int heads, int head_dim,
-                   cudaStream_t st) {
+void attention_fwd_mma(const void* qkv, void* o, float* lse, int batch, int seq, int heads, int head_dim,
+                       cudaStream_t st) {
     if (head_dim != D) throw std::runtime_error("attention: head_dim must be 128");
     static bool cfg = false;
     if (!cfg) {
@@ -493,24 +493,21 @@ void attention_fwd(const void* qkv, void* o, float* lse, int batch, int seq, int
                                                           scale_log2);
 }
 
+// forward entry point: the tcgen05/TMEM kernel (attention_tc.cu)
+void attention_fwd(const void* qkv, void* o, float* lse, int batch, int seq, int heads, int head_dim,
+                   cudaStream_t st) {
+    attention_fwd_tc(qkv, o, lse, batch, seq, heads, head_dim, st);
+}
+
 void attention_bwd(const void* qkv, const void* o, const void* dout, const float* lse, float* delta, float* dq_acc,
                    void* dqkv, int batch, int seq, int heads, int head_dim, cudaStream_t st) {
     if (head_dim != D) throw std::runtime_error("attention: head_dim must be 128");
-    static bool cfg = false;
-    if (!cfg) {
-        cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem);
-        cfg = true;
-    }
     const int T = batch * seq;
     const int warps = T * heads;
     attn_bwd_prep_kernel<<<(warps + 7) / 8, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(o),
                                                           static_cast<const __nv_bfloat16*>(dout), delta, dq_acc, seq,
                                                           heads, T);
-    const float scale = 1.f / sqrtf(static_cast<float>(head_dim));
-    dim3 grid((seq + B_BC - 1) / B_BC, heads, batch);
-    attn_bwd_kernel<<<grid, B_WARPS * 32, kBwdSmem, st>>>(
-        static_cast<const __nv_bfloat16*>(qkv), static_cast<const __nv_bfloat16*>(dout), lse, delta, dq_acc,
-        static_cast<__nv_bfloat16*>(dqkv), seq, heads, scale, scale * kLog2e);
+    attention_bwd_tc(qkv, dout, lse, delta, dq_acc, dqkv, batch, seq, heads, head_dim, st);
     const int64_t n4 = static_cast<int64_t>(T) * heads * head_dim / 4;
     attn_dq_convert_kernel<<<static_cast<unsigned>((n4 + 255) / 256), 256, 0, st>>>(
         dq_acc, static_cast<__nv_bfloat16*>(dqkv), T, heads * head_dim);

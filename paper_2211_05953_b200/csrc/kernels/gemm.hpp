@@ -1,6 +1,7 @@
 // Host interface of the sm_100a bf16 GEMM (gemm_sm100.cu).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -33,5 +34,9 @@ struct GemmArgs {
 };
 
 void gemm_bf16(const GemmArgs& g, cudaStream_t stream);
+
+// 2-D TMA descriptor over a row-major [rows][ld] matrix (bf16, or f32 if `f32`) with `inner`
+// valid columns; box = {128 bytes of the inner dimension, box_rows}, SWIZZLE_128B, OOB -> 0.
+CUtensorMap make_tma_2d(const void* ptr, int64_t inner, int64_t rows, int64_t ld, int box_rows, bool f32);
 
 }  // namespace bfpp

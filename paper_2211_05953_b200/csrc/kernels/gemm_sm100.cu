@@ -27,6 +27,39 @@
 
 namespace bfpp {
 
+// ---- host side -----------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    if (!fn) throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+// 2-D tensor map over a row-major [rows][ld] matrix with `inner` valid columns;
+// box = {128 B of inner, box_rows}, SWIZZLE_128B, OOB loads -> zero, OOB stores dropped.
+CUtensorMap make_tma_2d(const void* ptr, int64_t inner, int64_t rows, int64_t ld, int box_rows, bool f32) {
+    CUtensorMap m;
+    const int esz = f32 ? 4 : 2;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * esz)};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / esz), static_cast<cuuint32_t>(box_rows)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode_fn()(&m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                             const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+    return m;
+}
+
+
 namespace {
 
 constexpr int BM = 128;
@@ -306,38 +339,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 1) ptx::tmem_dealloc<2 * BN>(tmem_base);
 }
 
-// ---- host side -----------------------------------------------------------------
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    });
-    if (!fn) throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
-    return fn;
-}
-
-// 2-D tensor map over a row-major [rows][ld] matrix with `inner` valid columns;
-// box = {128 B of inner, box_rows}, SWIZZLE_128B, OOB loads -> zero, OOB stores dropped.
-CUtensorMap make_map(const void* ptr, int64_t inner, int64_t rows, int64_t ld, int box_rows, bool f32 = false) {
-    CUtensorMap m;
-    const int esz = f32 ? 4 : 2;
-    cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(rows)};
-    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * esz)};
-    cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / esz), static_cast<cuuint32_t>(box_rows)};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult r = encode_fn()(&m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
-                             const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
-    return m;
-}
-
 int num_sms() {
     static int n = 0;
     if (!n) {
@@ -350,10 +351,10 @@ int num_sms() {
 
 template <int BN, int A_MN, int B_MN>
 void launch(const GemmArgs& g, cudaStream_t st) {
-    CUtensorMap ta = A_MN ? make_map(g.A, g.M, g.K, g.lda, BK) : make_map(g.A, g.K, g.M, g.lda, BM);
-    CUtensorMap tb = B_MN ? make_map(g.B, g.N, g.K, g.ldb, BK) : make_map(g.B, g.K, g.N, g.ldb, BN);
+    CUtensorMap ta = A_MN ? make_tma_2d(g.A, g.M, g.K, g.lda, BK, false) : make_tma_2d(g.A, g.K, g.M, g.lda, BM, false);
+    CUtensorMap tb = B_MN ? make_tma_2d(g.B, g.N, g.K, g.ldb, BK, false) : make_tma_2d(g.B, g.K, g.N, g.ldb, BN, false);
     const bool f32 = g.epilogue == GEMM_EPI_F32;
-    CUtensorMap td = make_map(g.D, g.N, g.M, g.ldd, 32, f32);
+    CUtensorMap td = make_tma_2d(g.D, g.N, g.M, g.ldd, 32, f32);
     EpiArgs ep{static_cast<const __nv_bfloat16*>(g.aux), g.ldaux, static_cast<__nv_bfloat16*>(g.aux_out),
                g.ldaux_out, g.epilogue, g.accumulate};
     auto kern = gemm_kernel<BN, A_MN, B_MN>;

@@ -8,6 +8,11 @@ namespace bfpp {
 
 // attention.cu — causal MHA, head_dim 128; qkv [B*S][3*H*128], o [B*S][H*128], lse [B*H][S] (log2 domain)
 void attention_fwd(const void* qkv, void* o, float* lse, int batch, int seq, int heads, int head_dim, cudaStream_t st);
+// tcgen05/TMEM version of attention_fwd (attention_tc.cu); same inputs/outputs
+void attention_fwd_tc(const void* qkv, void* o, float* lse, int batch, int seq, int heads, int head_dim,
+                      cudaStream_t st);
+void attention_bwd_tc(const void* qkv, const void* dout, const float* lse, const float* delta, float* dq_acc,
+                      void* dqkv, int batch, int seq, int heads, int head_dim, cudaStream_t st);
 // delta [B*H][S] and dq_acc [B*S][H*128] f32 are scratch; dqkv receives dQ, dK, dV.
 void attention_bwd(const void* qkv, const void* o, const void* dout, const float* lse, float* delta, float* dq_acc,
                    void* dqkv, int batch, int seq, int heads, int head_dim, cudaStream_t st);
