@@ -147,6 +147,7 @@ struct TaskExec {
     int slot = -1;              // DP_FS weight slot used (compute) or filled (reconstruct)
     bool first_unit = false, last_unit = false;  // Reduce
     bool adam_after = false;    // Bwd (n_dp == 1) or Reduce (last unit): run the optimizer for this stage
+    bool first_in_unit = false; // Bwd: first gradient contribution of its reduction unit (overwrite, no zeroing)
     std::vector<TaskId> waits;  // events to wait on (deps on other streams + resource deps)
 };
 
@@ -444,9 +445,13 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
             // a new reduction unit of this stage may only start once the previous unit's
             // reduce-scatter has drained (and re-zeroed) the stage's gradient buffer
             auto pb = prev_bwd.find(t.stage);
+            if (pb == prev_bwd.end()) te.first_in_unit = true;
             if (pb != prev_bwd.end()) {
                 auto r = reduce_of_last_bwd.find(pb->second);
-                if (r != reduce_of_last_bwd.end()) te.waits.push_back(r->second);
+                if (r != reduce_of_last_bwd.end()) {
+                    te.waits.push_back(r->second);
+                    te.first_in_unit = true;
+                }
             }
             prev_bwd[t.stage] = id;
             if (c_.n_dp < 2 && last_bwd_of_stage[t.stage] == id) te.adam_after = true;
@@ -604,9 +609,9 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
           [&] { layernorm_fwd(x, g, b, y, mu, rs, static_cast<int>(T), static_cast<int>(h), 1e-5f, st); });
     };
     auto LNB = [&](cudaStream_t st, const bf16* dy, const bf16* x, const bf16* g, const float* mu, const float* rs,
-                   const bf16* dres, bf16* dx, float* dg, float* db) {
+                   const bf16* dres, bf16* dx, float* dg, float* db, int acc) {
         K(K_LAYERNORM, (dres ? 6 : 5) * Th2, 3, st, [&] {
-            layernorm_bwd(dy, x, g, mu, rs, dres, dx, dg, db, static_cast<int>(T), static_cast<int>(h), st);
+            layernorm_bwd(dy, x, g, mu, rs, dres, dx, dg, db, static_cast<int>(T), static_cast<int>(h), st, acc);
         });
     };
 
@@ -621,7 +626,7 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
         bf16* w = sharded ? ls.w16_shard : ls.w16;
         K(K_ADAM, (sharded ? 26.0 : 30.0) * static_cast<double>(ls.shard_n), 1, st, [&] {
             adam_update(ls.master, ls.m, ls.v, g, w, ls.shard_n, o_.lr, o_.beta1, o_.beta2, o_.eps, o_.weight_decay,
-                        I.step_no, sharded ? 0 : 1, st);
+                        I.step_no, 0, st);
         });
         if (sharded && c_.dp_variant == DpVariant::DP_PS)
             NK(ncclAllGather(ls.w16_shard, ls.w16, static_cast<size_t>(ls.shard_n), ncclBfloat16, I.dp_comm, st));
@@ -670,11 +675,12 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
             LocalStage& ls = I.local[static_cast<size_t>(cidx)];
             const bf16* W = weights(te, cidx);
             float* G_ = ls.grad;
+            const int acc = te.first_in_unit ? 0 : 1;  // the unit's first contribution overwrites
             const bf16* g;
             if (L.last) {
                 G(st, T, h, V, a.logits, V, 0, W + L.head, h, 1, I.tmp_h, h, GEMM_EPI_BF16);
-                G(st, V, h, T, a.logits, V, 1, a.lnf, h, 1, G_ + L.head, h, GEMM_EPI_F32, nullptr, 0, nullptr, 0, 1);
-                LNB(st, I.tmp_h, a.out, W + L.lnf_g, a.muf, a.rsf, nullptr, I.gA, G_ + L.lnf_g, G_ + L.lnf_b);
+                G(st, V, h, T, a.logits, V, 1, a.lnf, h, 1, G_ + L.head, h, GEMM_EPI_F32, nullptr, 0, nullptr, 0, acc);
+                LNB(st, I.tmp_h, a.out, W + L.lnf_g, a.muf, a.rsf, nullptr, I.gA, G_ + L.lnf_g, G_ + L.lnf_b, acc);
                 g = I.gA;
             } else {
                 g = a.gin;
@@ -685,22 +691,26 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
                 bf16* gmid = g == I.gB ? I.gA : I.gB;
                 bf16* gnext = (li == 0 && !L.first) ? a.gout : (gmid == I.gA ? I.gB : I.gA);
                 // MLP: x_out = x_mid + gelu(ln2 W1^T) W2^T
-                G(st, h, mlp, T, g, h, 1, x.act, mlp, 1, G_ + P.fc2, mlp, GEMM_EPI_F32, nullptr, 0, nullptr, 0, 1);
+                G(st, h, mlp, T, g, h, 1, x.act, mlp, 1, G_ + P.fc2, mlp, GEMM_EPI_F32, nullptr, 0, nullptr, 0, acc);
                 G(st, T, mlp, h, g, h, 0, W + P.fc2, mlp, 1, I.tmp_m, mlp, GEMM_EPI_DGELU, x.pre, mlp);
-                G(st, mlp, h, T, I.tmp_m, mlp, 1, x.ln2, h, 1, G_ + P.fc1, h, GEMM_EPI_F32, nullptr, 0, nullptr, 0, 1);
+                G(st, mlp, h, T, I.tmp_m, mlp, 1, x.ln2, h, 1, G_ + P.fc1, h, GEMM_EPI_F32, nullptr, 0, nullptr, 0, acc);
                 G(st, T, h, mlp, I.tmp_m, mlp, 0, W + P.fc1, h, 1, I.tmp_h, h, GEMM_EPI_BF16);
-                LNB(st, I.tmp_h, x.x_mid, W + P.ln2_g, x.mu2, x.rs2, g, gmid, G_ + P.ln2_g, G_ + P.ln2_b);
+                LNB(st, I.tmp_h, x.x_mid, W + P.ln2_g, x.mu2, x.rs2, g, gmid, G_ + P.ln2_g, G_ + P.ln2_b, acc);
                 // attention: x_mid = x_in + attn(ln1 Wqkv^T) Wo^T
-                G(st, h, h, T, gmid, h, 1, x.o, h, 1, G_ + P.o, h, GEMM_EPI_F32, nullptr, 0, nullptr, 0, 1);
+                G(st, h, h, T, gmid, h, 1, x.o, h, 1, G_ + P.o, h, GEMM_EPI_F32, nullptr, 0, nullptr, 0, acc);
                 G(st, T, h, h, gmid, h, 0, W + P.o, h, 1, I.tmp_h, h, GEMM_EPI_BF16);
                 K(K_ATTN_BWD, 2.5 * attn_flops, 3, st, [&] {
                     attention_bwd(x.qkv, x.o, I.tmp_h, x.lse, I.delta, I.dq_acc, I.dqkv, B, S, H, 128, st);
                 });
                 G(st, 3 * h, h, T, I.dqkv, 3 * h, 1, x.ln1, h, 1, G_ + P.qkv, h, GEMM_EPI_F32, nullptr, 0, nullptr, 0,
-                  1);
+                  acc);
                 G(st, T, h, 3 * h, I.dqkv, 3 * h, 0, W + P.qkv, h, 1, I.tmp_h, h, GEMM_EPI_BF16);
-                LNB(st, I.tmp_h, x.x_in, W + P.ln1_g, x.mu1, x.rs1, gmid, gnext, G_ + P.ln1_g, G_ + P.ln1_b);
+                LNB(st, I.tmp_h, x.x_in, W + P.ln1_g, x.mu1, x.rs1, gmid, gnext, G_ + P.ln1_g, G_ + P.ln1_b, acc);
                 g = gnext;
+            }
+            if (L.first && acc == 0) {  // scatter-added gradients need a zeroed start
+                CK(cudaMemsetAsync(G_ + L.wte, 0, static_cast<size_t>(V * h) * 4, st));
+                CK(cudaMemsetAsync(G_ + L.wpe, 0, static_cast<size_t>(m_.s_seq * h) * 4, st));
             }
             if (L.first)
                 K(K_MISC, 2 * Th2, 1, st, [&] {
@@ -745,7 +755,7 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
                                      st));
                 if (!te.first_unit)
                     K(K_MISC, 12.0 * ls.shard_n, 1, st, [&] { add_f32_kernel<<<296, 256, 0, st>>>(ls.gshard, ls.gtmp, ls.shard_n); });
-                CK(cudaMemsetAsync(ls.grad, 0, static_cast<size_t>(full) * 4, st));
+                // no re-zeroing: the next unit's first backward overwrites the gradient buffer
             }
             if (te.adam_after) adam(ls, st);
             break;

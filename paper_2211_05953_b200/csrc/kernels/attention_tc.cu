@@ -64,9 +64,11 @@ __global__ void __launch_bounds__(192, 1)
     uint64_t* o_done = bar + 14;  // PV_j complete (P buffer free, O stable)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
 
+    // grid (H, query blocks, B): x (heads) varies fastest, so the longest query blocks (most
+    // key tiles under the causal mask) of every head are scheduled first
     const int n_qb = (S + BQ - 1) / BQ;
-    const int qb = n_qb - 1 - blockIdx.x;  // longest (most key tiles) blocks first
-    const int head = blockIdx.y, b = blockIdx.z;
+    const int qb = n_qb - 1 - blockIdx.y;
+    const int head = blockIdx.x, b = blockIdx.z;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int HD = H * D;
     const int row0 = b * S;
@@ -274,7 +276,7 @@ void attention_fwd_tc(const void* qkv, void* o, float* lse, int batch, int seq, 
     }
     const int64_t T = static_cast<int64_t>(batch) * seq, h3 = 3LL * heads * head_dim;
     const CUtensorMap tm = make_tma_2d(qkv, h3, T, h3, 128, false);
-    dim3 grid((seq + BQ - 1) / BQ, heads, batch);
+    dim3 grid(heads, (seq + BQ - 1) / BQ, batch);
     const float scale_log2 = kLog2e / sqrtf(static_cast<float>(head_dim));
     attn_fwd_tc_kernel<<<grid, 192, FwdSmem::kBytes, st>>>(tm, static_cast<__nv_bfloat16*>(o), lse, seq, heads,
                                                            scale_log2);
@@ -326,9 +328,11 @@ __global__ void __launch_bounds__(192, 1)
     float* s_lse = reinterpret_cast<float*>(sm + BwdSmem::kLse);
     float* s_del = reinterpret_cast<float*>(sm + BwdSmem::kDelta);
 
+    // grid (H, key blocks, B): the block scheduler walks x fastest, so every head's key block 0
+    // (which sees the most query blocks under the causal mask) starts in the first wave
     const int n_kb = (S + BKV - 1) / BKV;
-    const int kb = blockIdx.x;
-    const int head = blockIdx.y, b = blockIdx.z;
+    const int kb = blockIdx.y;
+    const int head = blockIdx.x, b = blockIdx.z;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int HD = H * D;
     const int row0 = b * S;
@@ -535,7 +539,7 @@ void attention_bwd_tc(const void* qkv, const void* dout, const float* lse, const
     const int64_t T = static_cast<int64_t>(batch) * seq, HD = static_cast<int64_t>(heads) * head_dim;
     const CUtensorMap tq = make_tma_2d(qkv, 3 * HD, T, 3 * HD, 128, false);
     const CUtensorMap to = make_tma_2d(dout, HD, T, HD, 128, false);
-    dim3 grid((seq + BKV - 1) / BKV, heads, batch);
+    dim3 grid(heads, (seq + BKV - 1) / BKV, batch);
     const float scale = 1.f / sqrtf(static_cast<float>(head_dim));
     attn_bwd_tc_kernel<<<grid, 192, BwdSmem::kBytes, st>>>(tq, to, lse, delta, dq_acc,
                                                            static_cast<__nv_bfloat16*>(dqkv), seq, heads, scale,

@@ -130,43 +130,62 @@ __global__ void __launch_bounds__(256) xent_kernel(__nv_bfloat16* __restrict__ l
 }
 
 // p, m, v f32 shards; g f32 gradient (zeroed after use if zero_grad); w16 bf16 copy of p.
-__global__ void adam_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
-                            float* __restrict__ g, __nv_bfloat16* __restrict__ w16, int64_t n, float lr, float b1,
-                            float b2, float eps, float wd, float bc1, float bc2, int zero_grad) {
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x * 4;
-    for (int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4; i < n; i += stride) {
-        if (i + 4 <= n) {
-            float4 P = *reinterpret_cast<float4*>(p + i), Mv = *reinterpret_cast<float4*>(m + i);
-            float4 Vv = *reinterpret_cast<float4*>(v + i), G = *reinterpret_cast<const float4*>(g + i);
-            float* pp = &P.x;
-            float* mm = &Mv.x;
-            float* vv = &Vv.x;
-            const float* gg = &G.x;
+// Launched with one 256-thread block per SM so it co-resides with the compute stream's
+// GEMM CTAs; each thread keeps ILP float4 groups of all four arrays in flight.
+template <int ILP>
+__global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, float* __restrict__ m,
+                                                   float* __restrict__ v, float* __restrict__ g,
+                                                   __nv_bfloat16* __restrict__ w16, int64_t n, float lr, float b1,
+                                                   float b2, float eps, float wd, float bc1, float bc2,
+                                                   int zero_grad) {
+    const int64_t n4 = n / 4;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; base < n4;
+         base += stride * ILP) {
+        float4 P[ILP], M[ILP], Vv[ILP], G[ILP];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                mm[u] = b1 * mm[u] + (1.f - b1) * gg[u];
-                vv[u] = b2 * vv[u] + (1.f - b2) * gg[u] * gg[u];
-                const float mh = mm[u] / bc1, vh = vv[u] / bc2;
-                pp[u] -= lr * (mh / (sqrtf(vh) + eps) + wd * pp[u]);
+        for (int u = 0; u < ILP; ++u) {
+            const int64_t i = base + u * stride;
+            if (i < n4) {
+                P[u] = reinterpret_cast<const float4*>(p)[i];
+                M[u] = reinterpret_cast<const float4*>(m)[i];
+                Vv[u] = reinterpret_cast<const float4*>(v)[i];
+                G[u] = reinterpret_cast<const float4*>(g)[i];
             }
-            *reinterpret_cast<float4*>(p + i) = P;
-            *reinterpret_cast<float4*>(m + i) = Mv;
-            *reinterpret_cast<float4*>(v + i) = Vv;
-            if (zero_grad) *reinterpret_cast<float4*>(g + i) = make_float4(0.f, 0.f, 0.f, 0.f);
-            __nv_bfloat162 lo = __floats2bfloat162_rn(P.x, P.y), hi = __floats2bfloat162_rn(P.z, P.w);
+        }
+#pragma unroll
+        for (int u = 0; u < ILP; ++u) {
+            const int64_t i = base + u * stride;
+            if (i >= n4) continue;
+            float* pp = &P[u].x;
+            float* mm = &M[u].x;
+            float* vv = &Vv[u].x;
+            const float* gg = &G[u].x;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                mm[k] = b1 * mm[k] + (1.f - b1) * gg[k];
+                vv[k] = b2 * vv[k] + (1.f - b2) * gg[k] * gg[k];
+                pp[k] -= lr * ((mm[k] / bc1) / (sqrtf(vv[k] / bc2) + eps) + wd * pp[k]);
+            }
+            reinterpret_cast<float4*>(p)[i] = P[u];
+            reinterpret_cast<float4*>(m)[i] = M[u];
+            reinterpret_cast<float4*>(v)[i] = Vv[u];
+            if (zero_grad) reinterpret_cast<float4*>(g)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            __nv_bfloat162 lo = __floats2bfloat162_rn(P[u].x, P[u].y), hi = __floats2bfloat162_rn(P[u].z, P[u].w);
             uint2 o;
             o.x = *reinterpret_cast<uint32_t*>(&lo);
             o.y = *reinterpret_cast<uint32_t*>(&hi);
-            *reinterpret_cast<uint2*>(w16 + i) = o;
-        } else {
-            for (int64_t j = i; j < n; ++j) {
-                m[j] = b1 * m[j] + (1.f - b1) * g[j];
-                v[j] = b2 * v[j] + (1.f - b2) * g[j] * g[j];
-                p[j] -= lr * ((m[j] / bc1) / (sqrtf(v[j] / bc2) + eps) + wd * p[j]);
-                if (zero_grad) g[j] = 0.f;
-                w16[j] = __float2bfloat16_rn(p[j]);
-            }
+            reinterpret_cast<uint2*>(w16)[i] = o;
         }
+    }
+    // scalar tail
+    const int64_t t = n4 * 4 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t < n) {
+        m[t] = b1 * m[t] + (1.f - b1) * g[t];
+        v[t] = b2 * v[t] + (1.f - b2) * g[t] * g[t];
+        p[t] -= lr * ((m[t] / bc1) / (sqrtf(v[t] / bc2) + eps) + wd * p[t]);
+        if (zero_grad) g[t] = 0.f;
+        w16[t] = __float2bfloat16_rn(p[t]);
     }
 }
 
@@ -231,9 +250,9 @@ void adam_update(float* p, float* m, float* v, float* g, void* w16, int64_t n, f
     const float bc1 = 1.f - powf(b1, static_cast<float>(step));
     const float bc2 = 1.f - powf(b2, static_cast<float>(step));
     const int64_t want = (n / 4 + 255) / 256;
-    const int blocks = static_cast<int>(want < 8 * sm_count() ? (want > 0 ? want : 1) : 8 * sm_count());
-    adam_kernel<<<blocks, 256, 0, st>>>(p, m, v, g, static_cast<__nv_bfloat16*>(w16), n, lr, b1, b2, eps, wd, bc1,
-                                        bc2, zero_grad);
+    const int blocks = static_cast<int>(want < sm_count() ? (want > 0 ? want : 1) : sm_count());
+    adam_kernel<4><<<blocks, 256, 0, st>>>(p, m, v, g, static_cast<__nv_bfloat16*>(w16), n, lr, b1, b2, eps, wd,
+                                           bc1, bc2, zero_grad);
 }
 
 void init_normal(float* p, void* w16, int64_t n, float mean, float std, uint64_t seed, uint64_t offset,

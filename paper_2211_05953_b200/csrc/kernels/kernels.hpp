@@ -21,7 +21,8 @@ void attention_bwd(const void* qkv, const void* o, const void* dout, const float
 void layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, float* mean, float* rstd, int rows,
                    int width, float eps, cudaStream_t st);
 void layernorm_bwd(const void* dy, const void* x, const void* gamma, const float* mean, const float* rstd,
-                   const void* dres, void* dx, float* dgamma, float* dbeta, int rows, int width, cudaStream_t st);
+                   const void* dres, void* dx, float* dgamma, float* dbeta, int rows, int width, cudaStream_t st,
+                   int accumulate = 1);
 
 // elementwise.cu
 void embed_fwd(const int32_t* tok, const void* wte, const void* wpe, void* x, int T, int S, int h, cudaStream_t st);

@@ -174,7 +174,8 @@ void layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, 
 }
 
 void layernorm_bwd(const void* dy, const void* x, const void* gamma, const float* mean, const float* rstd,
-                   const void* dres, void* dx, float* dgamma, float* dbeta, int rows, int width, cudaStream_t st) {
+                   const void* dres, void* dx, float* dgamma, float* dbeta, int rows, int width, cudaStream_t st,
+                   int accumulate) {
     if (width % 8) throw std::runtime_error("layernorm: width must be a multiple of 8");
     auto DY = static_cast<const __nv_bfloat16*>(dy);
     auto X = static_cast<const __nv_bfloat16*>(x);
@@ -194,7 +195,11 @@ void layernorm_bwd(const void* dy, const void* x, const void* gamma, const float
         ws_bytes = need;
     }
     ln_bwd_param_kernel<<<dim3(col_blocks, chunks), 256, 0, st>>>(DY, X, mean, rstd, ws, rows, width, per);
-    ln_colsum_kernel<<<dim3((2 * width + 255) / 256, 8), 256, 0, st>>>(ws, chunks, width, dgamma, dbeta);
+    if (!accumulate) {  // first contribution of this gradient unit: overwrite instead of add
+        cudaMemsetAsync(dgamma, 0, static_cast<size_t>(width) * sizeof(float), st);
+        cudaMemsetAsync(dbeta, 0, static_cast<size_t>(width) * sizeof(float), st);
+    }
+    ln_colsum_kernel<<<dim3((2 * width + 255) / 256, 32), 256, 0, st>>>(ws, chunks, width, dgamma, dbeta);
 }
 
 }  // namespace bfpp
