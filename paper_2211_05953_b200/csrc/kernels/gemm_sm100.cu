@@ -18,6 +18,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -339,6 +340,248 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 1) ptx::tmem_dealloc<2 * BN>(tmem_base);
 }
 
+
+// ===================================================================================
+// 2-CTA variant (cta_group::2): a cluster of two CTAs on neighbouring SMs computes a 256 x 256
+// tile; each CTA stages its own 128 rows of A and 128 rows (half the N extent) of B per
+// k-block (32 KB instead of 48 KB per SM for the same flops per SM), the leader CTA issues
+// tcgen05.mma.cta_group::2 (M = 256) over both CTAs' shared memory, and each CTA's TMEM holds
+// its 128 x 256 half of the accumulator, drained by its own 8 epilogue warps.
+constexpr int kStages2 = 6;
+struct Smem2 {
+    static constexpr int kABytes = 128 * BK * 2;
+    static constexpr int kBBytes = 128 * BK * 2;
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kOutOffset = kStages2 * kStageBytes;
+    static constexpr int kBarOffset = kOutOffset + kEpiWarps * kStageBytesOut;
+    static constexpr int kBytes = kBarOffset + 256 + 1024;
+};
+
+template <int A_MN, int B_MN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 const __grid_constant__ CUtensorMap tmD, int M, int N, int K, EpiArgs ep) {
+    constexpr int BN = 256;
+    using S = Smem2;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kBarOffset);
+    uint64_t* empty = full + kStages2;
+    uint64_t* tfull = empty + kStages2;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    const uint32_t rank = ptx::cluster_ctarank();
+    const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+    const int m_tiles = (M + 255) / 256;
+    const int n_tiles = (N + BN - 1) / BN;
+    const int num_tiles = m_tiles * n_tiles;
+    const int nk = (K + BK - 1) / BK;
+
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch(&tmA);
+        ptx::tma_prefetch(&tmB);
+        ptx::tma_prefetch(&tmD);
+        for (int s = 0; s < kStages2; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            ptx::mbar_init(&tfull[b], 1);
+            ptx::mbar_init(&tempty[b], 2 * kEpiWarps);
+        }
+        ptx::fence_barrier_init();
+    }
+    if (warp == 1) ptx::tmem_alloc_2sm<2 * BN>(tmem_slot);
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ===== TMA producer (both CTAs): own 128 rows of A and own 128-row half of B =====
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = pair; t < num_tiles; t += n_pairs) {
+                const int m0 = (t % m_tiles) * 256 + 128 * rank, n0 = (t / m_tiles) * BN + 128 * rank;
+                for (int kb = 0; kb < nk; ++kb) {
+                    ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t* sa = smem + stage * S::kStageBytes;
+                    uint8_t* sb = sa + S::kABytes;
+                    if (rank == 0) ptx::mbar_expect_tx(&full[stage], 2 * S::kStageBytes);
+                    const int k0 = kb * BK;
+                    if (A_MN) {
+#pragma unroll
+                        for (int i = 0; i < 2; ++i)
+                            ptx::tma_load_2d_2sm(sa + i * 64 * BK * 2, &tmA, &full[stage], m0 + 64 * i, k0);
+                    } else {
+                        ptx::tma_load_2d_2sm(sa, &tmA, &full[stage], k0, m0);
+                    }
+                    if (B_MN) {
+#pragma unroll
+                        for (int i = 0; i < 2; ++i)
+                            ptx::tma_load_2d_2sm(sb + i * 64 * BK * 2, &tmB, &full[stage], n0 + 64 * i, k0);
+                    } else {
+                        ptx::tma_load_2d_2sm(sb, &tmB, &full[stage], k0, n0);
+                    }
+                    if (++stage == kStages2) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && rank == 0) {
+            // ===== MMA issuer (leader CTA only) =====
+            constexpr uint32_t idesc = ptx::idesc_bf16_f32(256, BN, A_MN, B_MN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int it = 0;
+            for (int t = pair; t < num_tiles; t += n_pairs, ++it) {
+                const int acc = it & 1;
+                const uint32_t acc_phase = (it >> 1) & 1;
+                ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * BN;
+                for (int kb = 0; kb < nk; ++kb) {
+                    ptx::mbar_wait(&full[stage], phase);
+                    ptx::tc_fence_after();
+                    const uint32_t sa = ptx::smem_u32(smem + stage * S::kStageBytes);
+                    const uint32_t sb = sa + S::kABytes;
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k) {
+                        const uint64_t ad = A_MN ? ptx::sdesc_sw128(sa + k * 2048, 64 * BK * 2, 1024)
+                                                 : ptx::sdesc_sw128(sa + k * 32, 16, 1024);
+                        const uint64_t bd = B_MN ? ptx::sdesc_sw128(sb + k * 2048, 64 * BK * 2, 1024)
+                                                 : ptx::sdesc_sw128(sb + k * 32, 16, 1024);
+                        ptx::umma_f16_2sm(d_tmem, ad, bd, idesc, (kb | k) != 0);
+                    }
+                    ptx::umma_commit_2sm(&empty[stage], 0x3);
+                    if (++stage == kStages2) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                ptx::umma_commit_2sm(&tfull[acc], 0x3);
+            }
+        }
+    } else {
+        // ===== epilogue: TMEM -> registers -> fused op -> swizzled SMEM -> TMA store =====
+        const int ew = warp - 2;
+        const int q = warp & 3;        // TMEM lane quarter (hardware: warp id % 4)
+        const int half = ew >> 2;      // which alternate 128-byte column strips this warp owns
+        uint8_t* stage_out = smem + S::kOutOffset + ew * kStageBytesOut;
+        const bool f32_out = ep.epi == GEMM_EPI_F32;
+        const int cw = f32_out ? 32 : 64;  // tile columns per 128-byte strip
+        const int n_strips = BN / cw;
+        int it = 0;
+        for (int t = pair; t < num_tiles; t += n_pairs, ++it) {
+            const int acc = it & 1;
+            const uint32_t acc_phase = (it >> 1) & 1;
+            const int m0 = (t % m_tiles) * 256 + 128 * rank, n0 = (t / m_tiles) * BN;
+            const int row = m0 + q * 32 + lane;
+            const bool row_ok = row < M;
+            ptx::mbar_wait(&tfull[acc], acc_phase);
+            ptx::tc_fence_after();
+            for (int sidx = half; sidx < n_strips; sidx += 2) {
+                const int col0 = n0 + sidx * cw;
+                const uint32_t tcol = tmem_base + ((q * 32) << 16) + acc * BN + sidx * cw;
+                float v[64];
+                float a[64];
+                const bool need_aux = (ep.epi == GEMM_EPI_RESID || ep.epi == GEMM_EPI_DGELU);
+                const int valid = row_ok ? min(64, N - col0) : 0;
+                // issue the aux loads before the TMEM loads so both latencies overlap
+                if (need_aux && valid > 0) load_row64_bf16(ep.aux + static_cast<int64_t>(row) * ep.ldaux + col0, valid, a);
+                {
+                    uint32_t r[32];
+                    ptx::tmem_ld_32x32b_x32(tcol, r);
+                    if (!f32_out) {
+                        uint32_t r2[32];
+                        ptx::tmem_ld_32x32b_x32(tcol + 32, r2);
+                        ptx::tmem_ld_wait();
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) v[32 + j] = __uint_as_float(r2[j]);
+                    } else {
+                        ptx::tmem_ld_wait();
+                    }
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+                }
+                if (sidx + 2 >= n_strips) {
+                    // this warp's last TMEM read of the tile: hand the accumulator back to the MMA warp
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tempty[acc]), 0));
+                }
+                // staging buffer reuse: the previous TMA store must have finished reading it
+                if (lane == 0) ptx::bulk_wait_read<0>();
+                __syncwarp();
+                uint8_t* rowp = stage_out + lane * 128;
+                if (f32_out) {
+#pragma unroll
+                    for (int c = 0; c < 8; ++c)
+                        *reinterpret_cast<float4*>(rowp + ((c ^ (lane & 7)) << 4)) =
+                            make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+                } else {
+                    if (ep.epi == GEMM_EPI_RESID) {
+#pragma unroll
+                        for (int j = 0; j < 64; ++j) v[j] += a[j];
+                    } else if (ep.epi == GEMM_EPI_DGELU) {
+#pragma unroll
+                        for (int j = 0; j < 64; ++j) v[j] *= dgelu_f(a[j]);
+                    } else if (ep.epi == GEMM_EPI_GELU) {
+                        // pre-activation stored as bf16; gelu evaluated on the stored value
+                        __nv_bfloat16* pre = ep.aux_out + static_cast<int64_t>(row) * ep.ldaux_out + col0;
+#pragma unroll
+                        for (int j = 0; j < 64; j += 8) {
+                            uint4 o;
+                            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                h[u] = __floats2bfloat162_rn(v[j + 2 * u], v[j + 2 * u + 1]);
+                                const float2 f = __bfloat1622float2(h[u]);
+                                v[j + 2 * u] = gelu_f(f.x);
+                                v[j + 2 * u + 1] = gelu_f(f.y);
+                            }
+                            if (valid >= j + 8) {
+                                *reinterpret_cast<uint4*>(pre + j) = o;
+                            } else {
+                                for (int u = 0; u < 8; ++u)
+                                    if (j + u < valid) pre[j + u] = reinterpret_cast<__nv_bfloat16*>(&o)[u];
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        uint4 o;
+                        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) h[u] = __floats2bfloat162_rn(v[8 * c + 2 * u], v[8 * c + 2 * u + 1]);
+                        *reinterpret_cast<uint4*>(rowp + ((c ^ (lane & 7)) << 4)) = o;
+                    }
+                }
+                ptx::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0 && col0 < N && m0 + q * 32 < M) {
+                    if (f32_out && ep.accumulate)
+                        ptx::tma_reduce_add_2d(&tmD, stage_out, col0, m0 + q * 32);
+                    else
+                        ptx::tma_store_2d(&tmD, stage_out, col0, m0 + q * 32);
+                    ptx::bulk_commit();
+                }
+            }
+        }
+        if (lane == 0) ptx::bulk_wait<0>();
+    }
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    if (warp == 1) ptx::tmem_dealloc_2sm<2 * BN>(tmem_base);
+}
+
 int num_sms() {
     static int n = 0;
     if (!n) {
@@ -369,13 +612,59 @@ void launch(const GemmArgs& g, cudaStream_t st) {
                                                    static_cast<int>(g.K), ep);
 }
 
+template <int A_MN, int B_MN>
+void launch2(const GemmArgs& g, cudaStream_t st) {
+    CUtensorMap ta = A_MN ? make_tma_2d(g.A, g.M, g.K, g.lda, BK, false) : make_tma_2d(g.A, g.K, g.M, g.lda, 128, false);
+    CUtensorMap tb = B_MN ? make_tma_2d(g.B, g.N, g.K, g.ldb, BK, false) : make_tma_2d(g.B, g.K, g.N, g.ldb, 128, false);
+    const bool f32 = g.epilogue == GEMM_EPI_F32;
+    CUtensorMap td = make_tma_2d(g.D, g.N, g.M, g.ldd, 32, f32);
+    EpiArgs ep{static_cast<const __nv_bfloat16*>(g.aux), g.ldaux, static_cast<__nv_bfloat16*>(g.aux_out),
+               g.ldaux_out, g.epilogue, g.accumulate};
+    auto kern = gemm2_kernel<A_MN, B_MN>;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem2::kBytes);
+        configured = true;
+    }
+    const int tiles = static_cast<int>(((g.M + 255) / 256) * ((g.N + 255) / 256));
+    const int pairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = Smem2::kBytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, ta, tb, td, static_cast<int>(g.M), static_cast<int>(g.N), static_cast<int>(g.K),
+                       ep);
+}
+
 }  // namespace
 
+int gemm_mode = -1;  // -1 auto, 1 force 1-CTA, 2 force 2-CTA (benchmarks / tests)
+
 void gemm_bf16(const GemmArgs& g, cudaStream_t st) {
+    static bool env_read = false;
+    if (!env_read) {
+        if (const char* e = getenv("BFPP_GEMM_MODE")) gemm_mode = atoi(e);
+        env_read = true;
+    }
     if (g.M <= 0 || g.N <= 0 || g.K <= 0) throw std::runtime_error("gemm: empty problem");
     if (g.K % 8 || g.lda % 8 || g.ldb % 8 || g.ldd % 8) throw std::runtime_error("gemm: K and leading dims must be multiples of 8");
     const bool small_n = g.N <= 128;
     const int a = g.a_mn_major ? 1 : 0, b = g.b_mn_major ? 1 : 0;
+    const bool pair = gemm_mode == 2 || (gemm_mode < 0 && g.M >= 256 && g.N >= 256);
+    if (pair) {
+        if (a == 0 && b == 0) return launch2<0, 0>(g, st);
+        if (a == 0 && b == 1) return launch2<0, 1>(g, st);
+        if (a == 1 && b == 0) return launch2<1, 0>(g, st);
+        return launch2<1, 1>(g, st);
+    }
 #define BFPP_GEMM_CASE(BN_, A_, B_) \
     if (a == A_ && b == B_) return launch<BN_, A_, B_>(g, st);
     if (small_n) {
