@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <set>
@@ -138,7 +139,11 @@ struct LocalStage {
     bf16* w16_shard = nullptr;
 };
 
-enum StreamId { S_COMPUTE = 0, S_DP = 1, S_FWD_SEND = 2, S_FWD_RECV = 3, S_BWD_SEND = 4, S_BWD_RECV = 5, S_N = 6 };
+enum StreamId {
+    S_COMPUTE = 0, S_DP = 1, S_FWD_SEND = 2, S_FWD_RECV = 3, S_BWD_SEND = 4, S_BWD_RECV = 5,
+    S_WGRAD = 6,  // weight-gradient GEMMs of backward tasks, overlapping the data-gradient chain
+    S_N = 7
+};
 
 struct TaskExec {
     TaskId id;
@@ -160,8 +165,12 @@ struct Executor::Impl {
     std::vector<LocalStage> local;  // index c
     bf16* slots[2] = {nullptr, nullptr};
     std::vector<std::vector<StageActs>> acts;  // [mb][c]
-    // scratch (compute stream only)
-    bf16 *tmp_h = nullptr, *tmp_m = nullptr, *gA = nullptr, *gB = nullptr, *dqkv = nullptr;
+    // scratch: tmp_h is compute-stream private; the per-layer sets [2] are read by the wgrad
+    // stream and alternate by backward layer counter (event hand-offs in both directions)
+    bf16* tmp_h = nullptr;
+    bf16 *gmid_s[2] = {}, *dpre_s[2] = {}, *dqkv_s[2] = {}, *gout_s[2] = {}, *g_head = nullptr;
+    cudaEvent_t ev_a[2] = {}, ev_b[2] = {}, ev_wg[2] = {};
+    std::vector<cudaEvent_t> done_g;  // per Bwd task: its gradients are complete (compute + wgrad streams)
     float *dq_acc = nullptr, *delta = nullptr;
     int32_t *inputs = nullptr, *labels = nullptr;
     float *row_loss = nullptr, *loss_dev = nullptr, *loss_pinned = nullptr;
@@ -171,6 +180,8 @@ struct Executor::Impl {
     cudaEvent_t origin = nullptr, step_end = nullptr, stream_end[S_N] = {};
     std::vector<double> tl_start, tl_end;
     int step_no = 0;
+    int bwd_layers = 0;  // backward layers processed in the current step (scratch set parity)
+    bool wgrad_stream = false;
     std::vector<int> task_c;                      // local stage index of compute tasks
     KernelStats stats;
     struct Mark {
@@ -212,6 +223,7 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
 
     Impl& I = *impl_;
     I.dev = o.device;
+    if (const char* e = getenv("BFPP_WGRAD_STREAM")) I.wgrad_stream = atoi(e) != 0;
     CK(cudaSetDevice(I.dev));
     // Stream priorities: compute and pipeline hand-offs high, the DP lane (all-gather,
     // reduce-scatter, Adam) low, so bandwidth-bound optimizer blocks fill gaps instead of
@@ -219,8 +231,10 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
     {
         int least = 0, greatest = 0;
         CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        const int wgrad_prio = greatest + 1 <= least ? greatest + 1 : greatest;
         for (int s = 0; s < S_N; ++s)
-            CK(cudaStreamCreateWithPriority(&I.st[s], cudaStreamNonBlocking, s == S_DP ? least : greatest));
+            CK(cudaStreamCreateWithPriority(&I.st[s], cudaStreamNonBlocking,
+                                            s == S_DP ? least : s == S_WGRAD ? wgrad_prio : greatest));
     }
 
     // ---- NCCL communicators (uid layout: see bfpp_exec_n_comm_ids) ----
@@ -354,10 +368,16 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
         }
     }
     I.tmp_h = I.alloc<bf16>(Th, &total);
-    I.tmp_m = I.alloc<bf16>(static_cast<size_t>(T * mlp), &total);
-    I.gA = I.alloc<bf16>(Th, &total);
-    I.gB = I.alloc<bf16>(Th, &total);
-    I.dqkv = I.alloc<bf16>(3 * Th, &total);
+    I.g_head = I.alloc<bf16>(Th, &total);
+    for (int k = 0; k < 2; ++k) {
+        I.gmid_s[k] = I.alloc<bf16>(Th, &total);
+        I.gout_s[k] = I.alloc<bf16>(Th, &total);
+        I.dpre_s[k] = I.alloc<bf16>(static_cast<size_t>(T * mlp), &total);
+        I.dqkv_s[k] = I.alloc<bf16>(3 * Th, &total);
+        CK(cudaEventCreateWithFlags(&I.ev_a[k], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&I.ev_b[k], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&I.ev_wg[k], cudaEventDisableTiming));
+    }
     I.dq_acc = I.alloc<float>(Th, &total);
     I.delta = I.alloc<float>(static_cast<size_t>(T * H), &total);
     I.inputs = I.alloc<int32_t>(static_cast<size_t>(c_.n_mb * T), &total);
@@ -369,6 +389,7 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
     // ---- per-task execution plan ----
     const size_t n = graph_.tasks.size();
     I.done.assign(n, nullptr);
+    I.done_g.assign(n, nullptr);
     I.t_start.assign(n, nullptr);
     I.t_end.assign(n, nullptr);
     I.task_c.assign(n, -1);
@@ -464,6 +485,8 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
         }
         I.order.push_back(te);
         CK(cudaEventCreateWithFlags(&I.done[static_cast<size_t>(id)], cudaEventDisableTiming));
+        if (t.kind == TaskKind::Bwd)
+            CK(cudaEventCreateWithFlags(&I.done_g[static_cast<size_t>(id)], cudaEventDisableTiming));
     }
     // Host enqueue order: a topological order of this rank's tasks over the explicit waits
     // (graph deps on other streams + the executor's gradient-buffer resource deps) and the
@@ -527,6 +550,11 @@ Executor::~Executor() {
     for (auto e : I.t_end)
         if (e) cudaEventDestroy(e);
     for (auto e : I.ev_pool) cudaEventDestroy(e);
+    for (auto e : I.done_g)
+        if (e) cudaEventDestroy(e);
+    for (int k = 0; k < 2; ++k)
+        for (cudaEvent_t e : {I.ev_a[k], I.ev_b[k], I.ev_wg[k]})
+            if (e) cudaEventDestroy(e);
     if (I.origin) cudaEventDestroy(I.origin);
     if (I.step_end) cudaEventDestroy(I.step_end);
     for (auto e : I.stream_end)
@@ -577,6 +605,7 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
 
     I.stats = KernelStats{};
     I.marks.clear();
+    I.bwd_layers = 0;
     size_t ev_next = 0;
     // every kernel of the step goes through K(): counts launches, optionally brackets with events
     auto K = [&](int cat, double work, int n_launch, cudaStream_t st, auto&& fn) {
@@ -635,7 +664,11 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
     for (const TaskExec& te : I.order) {
         const Task& t = graph_.tasks[static_cast<size_t>(te.id)];
         cudaStream_t st = I.st[te.stream];
-        for (TaskId d : te.waits) CK(cudaStreamWaitEvent(st, I.done[static_cast<size_t>(d)], 0));
+        for (TaskId d : te.waits) {
+            // gradient consumers (Reduce) need the wgrad stream's half of a backward task too
+            const bool grads = graph_.tasks[static_cast<size_t>(d)].kind == TaskKind::Bwd && t.kind == TaskKind::Reduce;
+            CK(cudaStreamWaitEvent(st, grads ? I.done_g[static_cast<size_t>(d)] : I.done[static_cast<size_t>(d)], 0));
+        }
         if (o_.record_timeline) CK(cudaEventRecord(I.t_start[static_cast<size_t>(te.id)], st));
         const int cidx = I.task_c[static_cast<size_t>(te.id)];
         switch (t.kind) {
@@ -675,36 +708,63 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
             LocalStage& ls = I.local[static_cast<size_t>(cidx)];
             const bf16* W = weights(te, cidx);
             float* G_ = ls.grad;
+            // weight-gradient GEMMs: same stream by default (measured faster at T = 2048, where two
+            // persistent GEMM grids only interleave at CTA granularity); BFPP_WGRAD_STREAM=1 runs
+            // them on a separate stream overlapping the data-gradient chain
+            cudaStream_t ws = I.wgrad_stream ? I.st[S_WGRAD] : st;
             const int acc = te.first_in_unit ? 0 : 1;  // the unit's first contribution overwrites
+            // the wgrad stream also writes this stage's gradient buffer: honour the same
+            // resource waits (previous unit's reduce-scatter) as the compute stream
+            for (TaskId d : te.waits)
+                if (graph_.tasks[static_cast<size_t>(d)].kind == TaskKind::Reduce)
+                    CK(cudaStreamWaitEvent(ws, I.done[static_cast<size_t>(d)], 0));
+            auto wait_wgrad_latest = [&] {
+                if (I.bwd_layers > 0) CK(cudaStreamWaitEvent(st, I.ev_wg[(I.bwd_layers - 1) & 1], 0));
+            };
             const bf16* g;
             if (L.last) {
                 G(st, T, h, V, a.logits, V, 0, W + L.head, h, 1, I.tmp_h, h, GEMM_EPI_BF16);
-                G(st, V, h, T, a.logits, V, 1, a.lnf, h, 1, G_ + L.head, h, GEMM_EPI_F32, nullptr, 0, nullptr, 0, acc);
-                LNB(st, I.tmp_h, a.out, W + L.lnf_g, a.muf, a.rsf, nullptr, I.gA, G_ + L.lnf_g, G_ + L.lnf_b, acc);
-                g = I.gA;
+                CK(cudaEventRecord(I.ev_a[0], st));  // logits/lnf are persistent; only ordering matters
+                CK(cudaStreamWaitEvent(ws, I.ev_a[0], 0));
+                G(ws, V, h, T, a.logits, V, 1, a.lnf, h, 1, G_ + L.head, h, GEMM_EPI_F32, nullptr, 0, nullptr, 0, acc);
+                wait_wgrad_latest();  // g_head was last read by an earlier layer's wgrad
+                LNB(st, I.tmp_h, a.out, W + L.lnf_g, a.muf, a.rsf, nullptr, I.g_head, G_ + L.lnf_g, G_ + L.lnf_b,
+                    acc);
+                g = I.g_head;
             } else {
                 g = a.gin;
             }
             for (size_t li = L.layers.size(); li-- > 0;) {
                 const LayerParams& P = L.layers[li];
                 LayerActs& x = a.layers[li];
-                bf16* gmid = g == I.gB ? I.gA : I.gB;
-                bf16* gnext = (li == 0 && !L.first) ? a.gout : (gmid == I.gA ? I.gB : I.gA);
+                const int lc = I.bwd_layers++;
+                const int k = lc & 1;
+                // set k was last read by the wgrads of layer lc-2
+                if (lc >= 2) CK(cudaStreamWaitEvent(st, I.ev_wg[k], 0));
+                bf16 *gmid = I.gmid_s[k], *dpre = I.dpre_s[k], *dqkv = I.dqkv_s[k];
+                bf16* gnext = (li == 0 && !L.first) ? a.gout : I.gout_s[k];
                 // MLP: x_out = x_mid + gelu(ln2 W1^T) W2^T
-                G(st, h, mlp, T, g, h, 1, x.act, mlp, 1, G_ + P.fc2, mlp, GEMM_EPI_F32, nullptr, 0, nullptr, 0, acc);
-                G(st, T, mlp, h, g, h, 0, W + P.fc2, mlp, 1, I.tmp_m, mlp, GEMM_EPI_DGELU, x.pre, mlp);
-                G(st, mlp, h, T, I.tmp_m, mlp, 1, x.ln2, h, 1, G_ + P.fc1, h, GEMM_EPI_F32, nullptr, 0, nullptr, 0, acc);
-                G(st, T, h, mlp, I.tmp_m, mlp, 0, W + P.fc1, h, 1, I.tmp_h, h, GEMM_EPI_BF16);
+                G(st, T, mlp, h, g, h, 0, W + P.fc2, mlp, 1, dpre, mlp, GEMM_EPI_DGELU, x.pre, mlp);
+                CK(cudaEventRecord(I.ev_a[k], st));
+                CK(cudaStreamWaitEvent(ws, I.ev_a[k], 0));
+                G(ws, h, mlp, T, g, h, 1, x.act, mlp, 1, G_ + P.fc2, mlp, GEMM_EPI_F32, nullptr, 0, nullptr, 0, acc);
+                G(ws, mlp, h, T, dpre, mlp, 1, x.ln2, h, 1, G_ + P.fc1, h, GEMM_EPI_F32, nullptr, 0, nullptr, 0, acc);
+                G(st, T, h, mlp, dpre, mlp, 0, W + P.fc1, h, 1, I.tmp_h, h, GEMM_EPI_BF16);
                 LNB(st, I.tmp_h, x.x_mid, W + P.ln2_g, x.mu2, x.rs2, g, gmid, G_ + P.ln2_g, G_ + P.ln2_b, acc);
                 // attention: x_mid = x_in + attn(ln1 Wqkv^T) Wo^T
-                G(st, h, h, T, gmid, h, 1, x.o, h, 1, G_ + P.o, h, GEMM_EPI_F32, nullptr, 0, nullptr, 0, acc);
                 G(st, T, h, h, gmid, h, 0, W + P.o, h, 1, I.tmp_h, h, GEMM_EPI_BF16);
                 K(K_ATTN_BWD, 2.5 * attn_flops, 3, st, [&] {
-                    attention_bwd(x.qkv, x.o, I.tmp_h, x.lse, I.delta, I.dq_acc, I.dqkv, B, S, H, 128, st);
+                    attention_bwd(x.qkv, x.o, I.tmp_h, x.lse, I.delta, I.dq_acc, dqkv, B, S, H, 128, st);
                 });
-                G(st, 3 * h, h, T, I.dqkv, 3 * h, 1, x.ln1, h, 1, G_ + P.qkv, h, GEMM_EPI_F32, nullptr, 0, nullptr, 0,
+                CK(cudaEventRecord(I.ev_b[k], st));
+                CK(cudaStreamWaitEvent(ws, I.ev_b[k], 0));
+                G(ws, h, h, T, gmid, h, 1, x.o, h, 1, G_ + P.o, h, GEMM_EPI_F32, nullptr, 0, nullptr, 0, acc);
+                G(ws, 3 * h, h, T, dqkv, 3 * h, 1, x.ln1, h, 1, G_ + P.qkv, h, GEMM_EPI_F32, nullptr, 0, nullptr, 0,
                   acc);
-                G(st, T, h, 3 * h, I.dqkv, 3 * h, 0, W + P.qkv, h, 1, I.tmp_h, h, GEMM_EPI_BF16);
+                CK(cudaEventRecord(I.ev_wg[k], ws));
+                G(st, T, h, 3 * h, dqkv, 3 * h, 0, W + P.qkv, h, 1, I.tmp_h, h, GEMM_EPI_BF16);
+                // gnext (set k) was last read as g_in by the wgrad of layer lc-1
+                if (gnext == I.gout_s[k] && lc >= 1) CK(cudaStreamWaitEvent(st, I.ev_wg[(lc - 1) & 1], 0));
                 LNB(st, I.tmp_h, x.x_in, W + P.ln1_g, x.mu1, x.rs1, gmid, gnext, G_ + P.ln1_g, G_ + P.ln1_b, acc);
                 g = gnext;
             }
@@ -717,10 +777,13 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
                     embed_bwd(I.inputs + t.micro_batch * T, g, G_ + L.wte, G_ + L.wpe, static_cast<int>(T), S,
                               static_cast<int>(h), st);
                 });
+            // gradients complete = compute-stream part (LN, embedding) joined into the wgrad stream
+            CK(cudaEventRecord(I.done[static_cast<size_t>(te.id)], st));
+            CK(cudaStreamWaitEvent(ws, I.done[static_cast<size_t>(te.id)], 0));
+            CK(cudaEventRecord(I.done_g[static_cast<size_t>(te.id)], ws));
             if (te.adam_after) {
                 // n_dp == 1: this stage's gradient is final; update it on the DP stream
-                CK(cudaEventRecord(I.done[static_cast<size_t>(te.id)], st));
-                CK(cudaStreamWaitEvent(ds, I.done[static_cast<size_t>(te.id)], 0));
+                CK(cudaStreamWaitEvent(ds, I.done_g[static_cast<size_t>(te.id)], 0));
                 adam(ls, ds);
             }
             break;
