@@ -153,6 +153,7 @@ struct TaskExec {
     bool first_unit = false, last_unit = false;  // Reduce
     bool adam_after = false;    // Bwd (n_dp == 1) or Reduce (last unit): run the optimizer for this stage
     bool first_in_unit = false; // Bwd: first gradient contribution of its reduction unit (overwrite, no zeroing)
+    bool adam_tail = false;     // the step's last optimizer update (nothing left to overlap: full-chip grid)
     std::vector<TaskId> waits;  // events to wait on (deps on other streams + resource deps)
 };
 
@@ -524,6 +525,11 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
         }
         if (sorted.size() != m) throw SimError("executor: cyclic local dependencies");
         I.order = std::move(sorted);
+        for (size_t i = I.order.size(); i-- > 0;)
+            if (I.order[i].adam_after) {
+                I.order[i].adam_tail = true;
+                break;
+            }
     }
     set_flags(o.record_timeline, o.profile_kernels);
     CK(cudaEventCreate(&I.origin));
@@ -648,14 +654,15 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
         if (fs) return I.slots[te.slot];
         return I.local[static_cast<size_t>(cidx)].w16;
     };
-    auto adam = [&](LocalStage& ls, cudaStream_t st) {
+    auto adam = [&](LocalStage& ls, cudaStream_t st, bool tail) {
         if (o_.skip_optimizer) return;
         const bool sharded = ls.gshard != nullptr;
         float* g = sharded ? ls.gshard : ls.grad;
         bf16* w = sharded ? ls.w16_shard : ls.w16;
-        K(K_ADAM, (sharded ? 26.0 : 30.0) * static_cast<double>(ls.shard_n), 1, st, [&] {
+        // overlapped updates use one co-resident block per SM; the tail update owns the chip
+        K(K_ADAM, 26.0 * static_cast<double>(ls.shard_n), 1, st, [&] {
             adam_update(ls.master, ls.m, ls.v, g, w, ls.shard_n, o_.lr, o_.beta1, o_.beta2, o_.eps, o_.weight_decay,
-                        I.step_no, 0, st);
+                        I.step_no, 0, st, tail ? 8 : 1);
         });
         if (sharded && c_.dp_variant == DpVariant::DP_PS)
             NK(ncclAllGather(ls.w16_shard, ls.w16, static_cast<size_t>(ls.shard_n), ncclBfloat16, I.dp_comm, st));
@@ -784,7 +791,7 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
             if (te.adam_after) {
                 // n_dp == 1: this stage's gradient is final; update it on the DP stream
                 CK(cudaStreamWaitEvent(ds, I.done_g[static_cast<size_t>(te.id)], 0));
-                adam(ls, ds);
+                adam(ls, ds, te.adam_tail);
             }
             break;
         }
@@ -820,7 +827,7 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
                     K(K_MISC, 12.0 * ls.shard_n, 1, st, [&] { add_f32_kernel<<<296, 256, 0, st>>>(ls.gshard, ls.gtmp, ls.shard_n); });
                 // no re-zeroing: the next unit's first backward overwrites the gradient buffer
             }
-            if (te.adam_after) adam(ls, st);
+            if (te.adam_after) adam(ls, st, te.adam_tail);
             break;
         }
         }

@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(192, 1)
         const int r = q4 * 32 + lane;          // row within the tile (= TMEM lane)
         const int qrow = qb * BQ + r;          // query position within the sequence
         const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
-        uint8_t* prow = sm + FwdSmem::kP + r * 128;
+        const uint32_t prow = ptx::smem_u32(sm + FwdSmem::kP) + r * 128;
         float m_used = -INFINITY, l = 0.f;
         for (int j = 0; j < n_tiles; ++j) {
             const int st = j & 1;
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(192, 1)
                 }
                 // [2 key-blocks][128 rows][128 B], 16-byte chunk swizzled by row & 7
                 const int blk = c >> 3, ch = c & 7;
-                *reinterpret_cast<uint4*>(prow + blk * (kTile / 2) + ((ch ^ (r & 7)) << 4)) = pk;
+                ptx::st_shared_v4(prow + blk * (kTile / 2) + ((ch ^ (r & 7)) << 4), pk);
             }
             l += sum;
             ptx::fence_proxy_async_smem();
@@ -325,8 +325,8 @@ __global__ void __launch_bounds__(192, 1)
     uint64_t* dq_full = bar + 5;
     uint64_t* dq_empty = bar + 6;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 8);
-    float* s_lse = reinterpret_cast<float*>(sm + BwdSmem::kLse);
-    float* s_del = reinterpret_cast<float*>(sm + BwdSmem::kDelta);
+    const uint32_t s_lse = ptx::smem_u32(sm + BwdSmem::kLse);
+    const uint32_t s_del = ptx::smem_u32(sm + BwdSmem::kDelta);
 
     // grid (H, key blocks, B): the block scheduler walks x fastest, so every head's key block 0
     // (which sees the most query blocks under the causal mask) starts in the first wave
@@ -416,17 +416,18 @@ __global__ void __launch_bounds__(192, 1)
         const int key = kb * BKV + r;
         const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
         const int tid = threadIdx.x - 64;
+        const uint32_t sp_base = ptx::smem_u32(sm + BwdSmem::kP), sds_base = ptx::smem_u32(sm + BwdSmem::kS);
         for (int i = i0; i < n_qb; ++i) {
             const int it = i - i0;
             const int q0 = i * BQ;
             // double-buffered by iteration: a warp one iteration ahead never overwrites values a
             // slower warp is still reading (nobody gets two ahead past the barrier below)
-            float* L = s_lse + (it & 1) * 128;
-            float* Dl = s_del + (it & 1) * 128;
+            const uint32_t L = s_lse + (it & 1) * 512;
+            const uint32_t Dl = s_del + (it & 1) * 512;
             {
                 const int q = q0 + tid;
-                L[tid] = q < S ? lse[(static_cast<int64_t>(b) * H + head) * S + q] : 0.f;
-                Dl[tid] = q < S ? delta[(static_cast<int64_t>(b) * H + head) * S + q] : 0.f;
+                ptx::st_shared_f32(L + 4 * tid, q < S ? lse[(static_cast<int64_t>(b) * H + head) * S + q] : 0.f);
+                ptx::st_shared_f32(Dl + 4 * tid, q < S ? delta[(static_cast<int64_t>(b) * H + head) * S + q] : 0.f);
             }
             named_bar_sync(1, 128);
             ptx::mbar_wait(s_full, it & 1);
@@ -445,10 +446,10 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
                         const int ql = c * 32 + j + e;
-                        float pv = ptx::ex2_fast(__uint_as_float(rs[j + e]) * scale_log2 - L[ql]);
+                        float pv = ptx::ex2_fast(__uint_as_float(rs[j + e]) * scale_log2 - ptx::ld_shared_f32(L + 4 * ql));
                         if (mask && (key > q0 + ql || q0 + ql >= S || key >= S)) pv = 0.f;
                         p[e] = pv;
-                        d[e] = pv * (__uint_as_float(rd[j + e]) - Dl[ql]);
+                        d[e] = pv * (__uint_as_float(rd[j + e]) - ptx::ld_shared_f32(Dl + 4 * ql));
                     }
                     __nv_bfloat162 hp = __floats2bfloat162_rn(p[0], p[1]), hd = __floats2bfloat162_rn(d[0], d[1]);
                     pw[j / 2] = *reinterpret_cast<uint32_t*>(&hp);
@@ -458,11 +459,9 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const int blk = c >> 1, ch = (c & 1) * 4 + u;
-                    const int off = blk * (kTile / 2) + r * 128 + ((ch ^ (r & 7)) << 4);
-                    *reinterpret_cast<uint4*>(sm + BwdSmem::kP + off) =
-                        make_uint4(pw[4 * u], pw[4 * u + 1], pw[4 * u + 2], pw[4 * u + 3]);
-                    *reinterpret_cast<uint4*>(sm + BwdSmem::kS + off) =
-                        make_uint4(dw[4 * u], dw[4 * u + 1], dw[4 * u + 2], dw[4 * u + 3]);
+                    const uint32_t off = blk * (kTile / 2) + r * 128 + ((ch ^ (r & 7)) << 4);
+                    ptx::st_shared_v4(sp_base + off, pw[4 * u], pw[4 * u + 1], pw[4 * u + 2], pw[4 * u + 3]);
+                    ptx::st_shared_v4(sds_base + off, dw[4 * u], dw[4 * u + 1], dw[4 * u + 2], dw[4 * u + 3]);
                 }
             }
             ptx::fence_proxy_async_smem();

@@ -246,11 +246,12 @@ void softmax_xent(void* logits, int64_t ld, const int32_t* labels, float* row_lo
 }
 
 void adam_update(float* p, float* m, float* v, float* g, void* w16, int64_t n, float lr, float b1, float b2,
-                 float eps, float wd, int step, int zero_grad, cudaStream_t st) {
+                 float eps, float wd, int step, int zero_grad, cudaStream_t st, int blocks_per_sm) {
     const float bc1 = 1.f - powf(b1, static_cast<float>(step));
     const float bc2 = 1.f - powf(b2, static_cast<float>(step));
     const int64_t want = (n / 4 + 255) / 256;
-    const int blocks = static_cast<int>(want < sm_count() ? (want > 0 ? want : 1) : sm_count());
+    const int cap = blocks_per_sm * sm_count();
+    const int blocks = static_cast<int>(want < cap ? (want > 0 ? want : 1) : cap);
     adam_kernel<4><<<blocks, 256, 0, st>>>(p, m, v, g, static_cast<__nv_bfloat16*>(w16), n, lr, b1, b2, eps, wd,
                                            bc1, bc2, zero_grad);
 }

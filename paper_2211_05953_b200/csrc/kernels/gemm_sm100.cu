@@ -279,12 +279,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // staging buffer reuse: the previous TMA store must have finished reading it
                 if (lane == 0) ptx::bulk_wait_read<0>();
                 __syncwarp();
-                uint8_t* rowp = stage_out + lane * 128;
+                const uint32_t rowa = ptx::smem_u32(stage_out) + lane * 128;
                 if (f32_out) {
 #pragma unroll
                     for (int c = 0; c < 8; ++c)
-                        *reinterpret_cast<float4*>(rowp + ((c ^ (lane & 7)) << 4)) =
-                            make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+                        ptx::st_shared_v4(rowa + ((c ^ (lane & 7)) << 4), __float_as_uint(v[4 * c]),
+                                          __float_as_uint(v[4 * c + 1]), __float_as_uint(v[4 * c + 2]),
+                                          __float_as_uint(v[4 * c + 3]));
                 } else {
                     if (ep.epi == GEMM_EPI_RESID) {
 #pragma unroll
@@ -320,7 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
 #pragma unroll
                         for (int u = 0; u < 4; ++u) h[u] = __floats2bfloat162_rn(v[8 * c + 2 * u], v[8 * c + 2 * u + 1]);
-                        *reinterpret_cast<uint4*>(rowp + ((c ^ (lane & 7)) << 4)) = o;
+                        ptx::st_shared_v4(rowa + ((c ^ (lane & 7)) << 4), o);
                     }
                 }
                 ptx::fence_proxy_async_smem();
@@ -520,12 +521,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // staging buffer reuse: the previous TMA store must have finished reading it
                 if (lane == 0) ptx::bulk_wait_read<0>();
                 __syncwarp();
-                uint8_t* rowp = stage_out + lane * 128;
+                const uint32_t rowa = ptx::smem_u32(stage_out) + lane * 128;
                 if (f32_out) {
 #pragma unroll
                     for (int c = 0; c < 8; ++c)
-                        *reinterpret_cast<float4*>(rowp + ((c ^ (lane & 7)) << 4)) =
-                            make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+                        ptx::st_shared_v4(rowa + ((c ^ (lane & 7)) << 4), __float_as_uint(v[4 * c]),
+                                          __float_as_uint(v[4 * c + 1]), __float_as_uint(v[4 * c + 2]),
+                                          __float_as_uint(v[4 * c + 3]));
                 } else {
                     if (ep.epi == GEMM_EPI_RESID) {
 #pragma unroll
@@ -561,7 +563,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
 #pragma unroll
                         for (int u = 0; u < 4; ++u) h[u] = __floats2bfloat162_rn(v[8 * c + 2 * u], v[8 * c + 2 * u + 1]);
-                        *reinterpret_cast<uint4*>(rowp + ((c ^ (lane & 7)) << 4)) = o;
+                        ptx::st_shared_v4(rowa + ((c ^ (lane & 7)) << 4), o);
                     }
                 }
                 ptx::fence_proxy_async_smem();
