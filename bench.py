@@ -20,6 +20,9 @@ import time
 
 import numpy as np
 
+# executor streams need their own hardware work queues (paper_2211_05953_b200/__init__.py)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # one hardware queue per executor stream (see executor.py)
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -151,8 +154,16 @@ def reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+def _progress(msg):
+    if os.environ.get("BFPP_BENCH_VERBOSE"):
+        print(f"[rank {os.environ.get('RANK', '0')}] {msg}", file=sys.stderr, flush=True)
+
+
 def main():
     args = parse()
+    if os.environ.get("BFPP_HANG_DUMP_S"):
+        import faulthandler
+        faulthandler.dump_traceback_later(int(os.environ["BFPP_HANG_DUMP_S"]), exit=True)
     if args.impl == "reference":
         return reference_arm(args)
 
@@ -201,6 +212,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t.item()
 
+    _progress('warmup')
     for _ in range(args.warmup):
         ex.step_device(tokens_dev, loss_dev)
     barrier()
@@ -212,6 +224,7 @@ def main():
             ex.step_device(tokens_dev, loss_dev)
         e1.record(stream)
         barrier()
+    _progress('timed done')
     ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
     launches_step = sum(v[0] for v in ex.kernel_stats().values())
     tokens_per_step = n_mb * args.s_mb * dp * cfg.s_seq
@@ -219,6 +232,7 @@ def main():
     loss_val = float(loss_dev.item())
 
     # ---- end-to-end through the public API: pinned host tokens in, loss out, every step ----
+    _progress('e2e start')
     e2e = None
     if not args.no_e2e:
         host = tokens_dev.cpu().pin_memory()
@@ -242,6 +256,7 @@ def main():
         e2e = {"value": tokens_per_step / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms}
 
+    _progress('diagnostics')
     # ---- untimed diagnostic steps: per-kernel CUDA events, measured timeline ----
     ex.set_flags(record_timeline=False, profile_kernels=True)
     ex.step_device(tokens_dev, loss_dev)
@@ -249,6 +264,7 @@ def main():
     kst = ex.kernel_stats()
     bubble = None
     sim_bubble = None
+    _progress('timeline')
     if not args.no_timeline:
         ex.set_flags(record_timeline=True, profile_kernels=False)
         ex.step_device(tokens_dev, loss_dev)

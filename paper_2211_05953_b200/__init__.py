@@ -3,6 +3,13 @@
 ``pipesim`` mirrors the reference's schedule/stage API (drop-in surface);
 ``executor`` runs the resulting task graphs on B200s (tcgen05 kernels + NCCL).
 """
+import os
+
+# The executor runs 7 streams plus NCCL's; with fewer hardware work queues than streams, CUDA
+# maps streams onto shared queues and a NCCL receive waiting for its peer can block an unrelated
+# send queued behind it -> cross-GPU deadlock. Must be set before the CUDA context exists.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # one hardware queue per executor stream (see executor.py)
+
 from . import pipesim  # noqa: F401
 from .pipesim import *  # noqa: F401,F403
 

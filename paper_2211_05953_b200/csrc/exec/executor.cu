@@ -3,10 +3,15 @@
 // fully-sharded data-parallel traffic. See executor.hpp and DESIGN.md.
 #include "executor.hpp"
 
+#include <cuda.h>
+
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <chrono>
+#include <thread>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -73,6 +78,34 @@ StageLayout make_stage_layout(const ModelSpec& m, i64 stage, i64 n_stage, i64 lp
 }
 
 namespace {
+
+// Stream memory operations (driver API, resolved at run time): the pipeline hand-off is a
+// copy-engine peer copy followed by a 32-bit flag write into the receiver's memory; the
+// receiver's stream waits on the flag. No SMs, no communicator-ordering hazards.
+using PFN_waitv32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using PFN_writev32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+struct StreamMemOps {
+    PFN_waitv32 wait = nullptr;
+    PFN_writev32 write = nullptr;
+};
+const StreamMemOps& memops() {
+    static StreamMemOps ops;
+    static bool init = false;
+    if (!init) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            ops.wait = reinterpret_cast<PFN_waitv32>(p);
+        p = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            ops.write = reinterpret_cast<PFN_writev32>(p);
+        init = true;
+    }
+    if (!ops.wait || !ops.write) throw std::runtime_error("executor: stream memory operations unavailable");
+    return ops;
+}
 
 // Kinds of parameter sub-tensors for initialisation.
 struct Segment {
@@ -160,8 +193,16 @@ struct TaskExec {
 struct Executor::Impl {
     int dev = 0;
     cudaStream_t st[S_N] = {};
-    ncclComm_t dp_comm = nullptr, fwd_out = nullptr, fwd_in = nullptr, bwd_out = nullptr, bwd_in = nullptr;
+    ncclComm_t world_comm = nullptr, dp_comm = nullptr;
     std::vector<std::pair<size_t, ncclComm_t>> comm_ids;  // (global uid index, comm) for ordered teardown
+    // pipeline hand-off: receive arena (all activation / gradient receive slots of this rank) and
+    // its ready flags, both exported by CUDA IPC to the two ring neighbours
+    bf16* recv_arena = nullptr;
+    uint32_t* recv_flags = nullptr;
+    std::map<int, bf16*> peer_arena;       // rank -> mapped receive arena
+    std::map<int, uint32_t*> peer_flags;   // rank -> mapped flags
+    std::vector<void*> ipc_opened;
+    uint32_t xfer_seq = 0;                 // step sequence number written into the flags
     std::vector<void*> allocs;
     std::vector<LocalStage> local;  // index c
     bf16* slots[2] = {nullptr, nullptr};
@@ -179,10 +220,12 @@ struct Executor::Impl {
     std::vector<cudaEvent_t> done;                // per task id (local tasks)
     std::vector<cudaEvent_t> t_start, t_end;      // timing events
     cudaEvent_t origin = nullptr, step_end = nullptr, stream_end[S_N] = {};
+    cudaEvent_t step_done[2] = {};  // ring: the host waits for step k-2 before enqueuing step k
     std::vector<double> tl_start, tl_end;
     int step_no = 0;
     int bwd_layers = 0;  // backward layers processed in the current step (scratch set parity)
     bool wgrad_stream = false;
+    bool debug = false;
     std::vector<int> task_c;                      // local stage index of compute tasks
     KernelStats stats;
     struct Mark {
@@ -225,6 +268,7 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
     Impl& I = *impl_;
     I.dev = o.device;
     if (const char* e = getenv("BFPP_WGRAD_STREAM")) I.wgrad_stream = atoi(e) != 0;
+    if (const char* e = getenv("BFPP_EXEC_DEBUG")) I.debug = atoi(e) != 0;
     CK(cudaSetDevice(I.dev));
     // Stream priorities: compute and pipeline hand-offs high, the DP lane (all-gather,
     // reduce-scatter, Adam) low, so bandwidth-bound optimizer blocks fill gaps instead of
@@ -238,30 +282,20 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
                                             s == S_DP ? least : s == S_WGRAD ? wgrad_prio : greatest));
     }
 
-    // ---- NCCL communicators (uid layout: see bfpp_exec_n_comm_ids) ----
+    // ---- NCCL communicators (uid layout: see bfpp_exec_n_comm_ids): world (IPC handle exchange,
+    // teardown barrier) and one DP group per pipeline rank. Pipeline hand-offs do not use NCCL.
     const bool fs = c_.n_dp >= 2 && c_.dp_variant == DpVariant::DP_FS;
     {
         const size_t need = static_cast<size_t>(1 + p_ + 2 * p_ * c_.n_dp);
         if (world > 1 && uids.size() < need) throw SpecError("executor: not enough NCCL unique ids");
-        auto edge = [&](i64 dp, i64 d, int dir) { return static_cast<size_t>(1 + p_ + (dp * p_ + d) * 2 + dir); };
         NK(ncclGroupStart());
+        if (world > 1) NK(ncclCommInitRank(&I.world_comm, world, uids[0], rank));
         if (c_.n_dp >= 2)
             NK(ncclCommInitRank(&I.dp_comm, static_cast<int>(c_.n_dp), uids[static_cast<size_t>(1 + pp_rank_)],
                                 static_cast<int>(dp_rank_)));
-        if (p_ >= 2) {
-            NK(ncclCommInitRank(&I.fwd_out, 2, uids[edge(dp_rank_, pp_rank_, 0)], 0));
-            NK(ncclCommInitRank(&I.fwd_in, 2, uids[edge(dp_rank_, (pp_rank_ - 1 + p_) % p_, 0)], 1));
-            NK(ncclCommInitRank(&I.bwd_out, 2, uids[edge(dp_rank_, pp_rank_, 1)], 0));
-            NK(ncclCommInitRank(&I.bwd_in, 2, uids[edge(dp_rank_, (pp_rank_ + 1) % p_, 1)], 1));
-        }
         NK(ncclGroupEnd());
+        if (I.world_comm) I.comm_ids.push_back({0, I.world_comm});
         if (I.dp_comm) I.comm_ids.push_back({static_cast<size_t>(1 + pp_rank_), I.dp_comm});
-        if (p_ >= 2) {
-            I.comm_ids.push_back({edge(dp_rank_, pp_rank_, 0), I.fwd_out});
-            I.comm_ids.push_back({edge(dp_rank_, (pp_rank_ - 1 + p_) % p_, 0), I.fwd_in});
-            I.comm_ids.push_back({edge(dp_rank_, pp_rank_, 1), I.bwd_out});
-            I.comm_ids.push_back({edge(dp_rank_, (pp_rank_ + 1) % p_, 1), I.bwd_in});
-        }
     }
 
     // ---- parameters, gradients, optimizer shards ----
@@ -318,6 +352,15 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
     const int64_t T = c_.s_mb * m_.s_seq, h = m_.s_hidden, mlp = m_.s_mlp, V = m_.s_voc, H = m_.n_heads;
     const size_t Th = static_cast<size_t>(T * h);
     I.acts.assign(static_cast<size_t>(c_.n_mb), std::vector<StageActs>(static_cast<size_t>(v_)));
+    // receive slot (dir 0 = forward activation, 1 = backward gradient) of (mb, local stage c)
+    auto slot = [&](int dir, i64 mb, i64 cc) { return static_cast<size_t>((mb * v_ + cc) * 2 + dir); };
+    const size_t n_slots = static_cast<size_t>(c_.n_mb * v_ * 2);
+    if (p_ >= 2) {
+        CK(cudaMalloc(&I.recv_arena, n_slots * Th * sizeof(bf16)));
+        CK(cudaMalloc(&I.recv_flags, n_slots * sizeof(uint32_t) + 256));
+        CK(cudaMemset(I.recv_flags, 0, n_slots * sizeof(uint32_t)));
+        total += n_slots * Th * sizeof(bf16);
+    }
     for (i64 mb = 0; mb < c_.n_mb; ++mb) {
         for (i64 cc = 0; cc < v_; ++cc) {
             StageActs& a = I.acts[static_cast<size_t>(mb)][static_cast<size_t>(cc)];
@@ -326,8 +369,10 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
             // input: aliases the previous stage's output when both live on this device
             if (s > 0 && pl_.device_of(s - 1) == pp_rank_)
                 a.in = I.acts[static_cast<size_t>(mb)][static_cast<size_t>(cc - 1)].out;
+            else if (s > 0)
+                a.in = I.recv_arena + slot(0, mb, cc) * Th;  // written by the previous rank's copy engine
             else
-                a.in = I.alloc<bf16>(Th, &total);
+                a.in = I.alloc<bf16>(Th, &total);              // embedding output
             bf16* x = a.in;
             for (size_t l = 0; l < L.layers.size(); ++l) {
                 LayerActs la;
@@ -365,7 +410,7 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
             if (pl_.device_of(s + 1) == pp_rank_)
                 a.gin = I.acts[static_cast<size_t>(mb)][static_cast<size_t>(cc + 1)].gout;
             else
-                a.gin = I.alloc<bf16>(Th, &total);
+                a.gin = I.recv_arena + slot(1, mb, cc) * Th;
         }
     }
     I.tmp_h = I.alloc<bf16>(Th, &total);
@@ -386,6 +431,38 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
     I.row_loss = I.alloc<float>(static_cast<size_t>(c_.n_mb * T), &total);
     I.loss_dev = I.alloc<float>(4, &total);
     CK(cudaMallocHost(&I.loss_pinned, sizeof(float)));
+
+    // ---- CUDA IPC: map the ring neighbours' receive arenas and flags ----
+    if (p_ >= 2) {
+        struct Handles {
+            cudaIpcMemHandle_t arena, flags;
+        };
+        Handles mine{};
+        CK(cudaIpcGetMemHandle(&mine.arena, I.recv_arena));
+        CK(cudaIpcGetMemHandle(&mine.flags, I.recv_flags));
+        uint8_t *d_all = nullptr, *d_mine = nullptr;
+        CK(cudaMalloc(&d_all, sizeof(Handles) * static_cast<size_t>(world)));
+        CK(cudaMalloc(&d_mine, sizeof(Handles)));
+        CK(cudaMemcpy(d_mine, &mine, sizeof(Handles), cudaMemcpyHostToDevice));
+        NK(ncclAllGather(d_mine, d_all, sizeof(Handles), ncclUint8, I.world_comm, I.st[S_COMPUTE]));
+        std::vector<Handles> all(static_cast<size_t>(world));
+        CK(cudaMemcpyAsync(all.data(), d_all, sizeof(Handles) * static_cast<size_t>(world), cudaMemcpyDeviceToHost,
+                           I.st[S_COMPUTE]));
+        CK(cudaStreamSynchronize(I.st[S_COMPUTE]));
+        CK(cudaFree(d_all));
+        CK(cudaFree(d_mine));
+        for (i64 nb : {(pp_rank_ + 1) % p_, (pp_rank_ - 1 + p_) % p_}) {
+            const int r = static_cast<int>(dp_rank_ * p_ + nb);
+            if (I.peer_arena.count(r)) continue;
+            void *pa = nullptr, *pf = nullptr;
+            CK(cudaIpcOpenMemHandle(&pa, all[static_cast<size_t>(r)].arena, cudaIpcMemLazyEnablePeerAccess));
+            CK(cudaIpcOpenMemHandle(&pf, all[static_cast<size_t>(r)].flags, cudaIpcMemLazyEnablePeerAccess));
+            I.peer_arena[r] = static_cast<bf16*>(pa);
+            I.peer_flags[r] = static_cast<uint32_t*>(pf);
+            I.ipc_opened.push_back(pa);
+            I.ipc_opened.push_back(pf);
+        }
+    }
 
     // ---- per-task execution plan ----
     const size_t n = graph_.tasks.size();
@@ -534,6 +611,7 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
     set_flags(o.record_timeline, o.profile_kernels);
     CK(cudaEventCreate(&I.origin));
     CK(cudaEventCreateWithFlags(&I.step_end, cudaEventDisableTiming));
+    for (auto& e : I.step_done) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming | cudaEventBlockingSync));
     for (auto& e : I.stream_end) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CK(cudaEventRecord(I.step_end, I.st[S_COMPUTE]));
     CK(cudaStreamSynchronize(I.st[S_COMPUTE]));
@@ -546,6 +624,17 @@ Executor::~Executor() {
     // Tear communicators down in ascending global id order so that the two members of
     // every 2-rank edge communicator finalise it at the same point (the forward ring
     // d -> d+1 and its wrap cross, so per-rank "out before in" orders would cycle).
+    if (I.world_comm) {  // no peer may still be copying into this rank's arena
+        float* one = nullptr;
+        if (cudaMalloc(&one, sizeof(float)) == cudaSuccess) {
+            ncclAllReduce(one, one, 1, ncclFloat32, ncclSum, I.world_comm, I.st[S_COMPUTE]);
+            cudaStreamSynchronize(I.st[S_COMPUTE]);
+            cudaFree(one);
+        }
+    }
+    for (void* p : I.ipc_opened) cudaIpcCloseMemHandle(p);
+    if (I.recv_arena) cudaFree(I.recv_arena);
+    if (I.recv_flags) cudaFree(I.recv_flags);
     std::vector<std::pair<size_t, ncclComm_t>> comms(I.comm_ids.begin(), I.comm_ids.end());
     std::sort(comms.begin(), comms.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
     for (auto& kv : comms) ncclCommDestroy(kv.second);
@@ -563,6 +652,8 @@ Executor::~Executor() {
             if (e) cudaEventDestroy(e);
     if (I.origin) cudaEventDestroy(I.origin);
     if (I.step_end) cudaEventDestroy(I.step_end);
+    for (auto e : I.step_done)
+        if (e) cudaEventDestroy(e);
     for (auto e : I.stream_end)
         if (e) cudaEventDestroy(e);
     for (void* p : I.allocs) cudaFree(p);
@@ -594,6 +685,41 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
     CK(cudaSetDevice(I.dev));
     cudaStream_t cs = I.st[S_COMPUTE], ds = I.st[S_DP];
     ++I.step_no;
+    ++I.xfer_seq;
+    // Cap the host's run-ahead at two steps ("frequent non-blocking syncs to cap
+    // the kernel queue"): a rank that does not read the loss could otherwise enqueue steps until
+    // its launch queue / NCCL proxy FIFOs fill while its peers still wait for this step's sends.
+    if (I.debug) fprintf(stderr, "[bfpp rank %d] step %d begin\n", rank_, I.step_no);
+    // debug mode: no run-ahead at all, so a stalled step is reported by the watchdog below
+    const int cap_slot = I.debug ? (I.step_no - 1) & 1 : I.step_no & 1;
+    if (I.step_no >= (I.debug ? 2 : 3)) {
+        if (!I.debug) {
+            CK(cudaEventSynchronize(I.step_done[cap_slot]));
+        } else {  // watchdog: report the first unfinished tasks if the device stalls
+            auto t0 = std::chrono::steady_clock::now();
+            while (cudaEventQuery(I.step_done[cap_slot]) == cudaErrorNotReady) {
+                if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(20)) {
+                    fprintf(stderr, "[bfpp rank %d] STALL waiting for step %d; unfinished tasks:\n", rank_,
+                            I.step_no - 2);
+                    int shown = 0;
+                    for (const TaskExec& te : I.order) {
+                        if (cudaEventQuery(I.done[static_cast<size_t>(te.id)]) == cudaErrorNotReady && shown < 12) {
+                            const Task& tt = graph_.tasks[static_cast<size_t>(te.id)];
+                            fprintf(stderr, "  task %d kind %s mb %lld stage %lld stream %d\n", te.id,
+                                    kind_name(tt.kind), (long long)tt.micro_batch, (long long)tt.stage, te.stream);
+                            ++shown;
+                        }
+                    }
+                    for (int q = 0; q < S_N; ++q)
+                        fprintf(stderr, "  stream %d query %d\n", q, static_cast<int>(cudaStreamQuery(I.st[q])));
+                    fflush(stderr);
+                    t0 = std::chrono::steady_clock::now() + std::chrono::seconds(3600);
+                }
+                std::this_thread::sleep_for(std::chrono::milliseconds(1));
+            }
+        }
+    }
+    if (I.debug) fprintf(stderr, "[bfpp rank %d] step %d run-ahead cap passed\n", rank_, I.step_no);
     for (int s = 0; s < S_N; ++s) CK(cudaStreamWaitEvent(I.st[s], I.step_end, 0));
     const int64_t T = c_.s_mb * m_.s_seq, h = m_.s_hidden, mlp = m_.s_mlp, V = m_.s_voc;
     const int H = static_cast<int>(m_.n_heads), S = static_cast<int>(m_.s_seq), B = static_cast<int>(c_.s_mb);
@@ -796,15 +922,28 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
             break;
         }
         case TaskKind::Transfer: {
+            // Copy-engine peer copy straight into the receiver's slot, then a flag write carrying
+            // the step sequence number; the receiver's stream waits for the flag (stream memory
+            // operations: no SM is held while waiting).
             const bool fwd = graph_.tasks[static_cast<size_t>(t.deps[0])].kind == TaskKind::Fwd;
-            const size_t count = static_cast<size_t>(T * h);
+            const size_t bytes = static_cast<size_t>(T * h) * sizeof(bf16);
+            const i64 dst_stage = fwd ? t.stage + 1 : t.stage - 1;
+            const size_t sl = static_cast<size_t>((t.micro_batch * v_ + dst_stage / p_) * 2 + (fwd ? 0 : 1));
+            if (I.debug)
+                fprintf(stderr, "[bfpp rank %d] step %d task %d %s %s mb %lld s %lld\n", rank_, I.step_no, te.id,
+                        te.send ? "send" : "recv", fwd ? "fwd" : "bwd", (long long)t.micro_batch, (long long)t.stage);
             if (te.send) {
                 const StageActs& a = I.acts[static_cast<size_t>(t.micro_batch)][static_cast<size_t>(t.stage / p_)];
-                NK(ncclSend(fwd ? a.out : a.gout, count, ncclBfloat16, 1, fwd ? I.fwd_out : I.bwd_out, st));
+                const int peer = static_cast<int>(dp_rank_ * p_ + t.peer_device);
+                bf16* dst = I.peer_arena.at(peer) + sl * static_cast<size_t>(T * h);
+                CK(cudaMemcpyAsync(dst, fwd ? a.out : a.gout, bytes, cudaMemcpyDeviceToDevice, st));
+                if (memops().write(st, reinterpret_cast<CUdeviceptr>(I.peer_flags.at(peer) + sl), I.xfer_seq,
+                                   CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+                    throw std::runtime_error("executor: cuStreamWriteValue32 failed");
             } else {
-                const i64 dst_stage = fwd ? t.stage + 1 : t.stage - 1;
-                const StageActs& a = I.acts[static_cast<size_t>(t.micro_batch)][static_cast<size_t>(dst_stage / p_)];
-                NK(ncclRecv(fwd ? a.in : a.gin, count, ncclBfloat16, 0, fwd ? I.fwd_in : I.bwd_in, st));
+                if (memops().wait(st, reinterpret_cast<CUdeviceptr>(I.recv_flags + sl), I.xfer_seq,
+                                  CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+                    throw std::runtime_error("executor: cuStreamWaitValue32 failed");
             }
             break;
         }
@@ -843,10 +982,12 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
         CK(cudaStreamWaitEvent(cs, I.stream_end[s], 0));
     }
     CK(cudaEventRecord(I.step_end, cs));
+    CK(cudaEventRecord(I.step_done[I.step_no & 1], cs));
     if (loss_dev && has_last) CK(cudaMemcpyAsync(loss_dev, I.loss_dev, 4, cudaMemcpyDeviceToDevice, cs));
     if (loss_host) {
         if (has_last) {
             CK(cudaMemcpyAsync(I.loss_pinned, I.loss_dev, 4, cudaMemcpyDeviceToHost, cs));
+            if (I.debug) fprintf(stderr, "[bfpp rank %d] step %d loss sync\n", rank_, I.step_no);
             CK(cudaStreamSynchronize(cs));
             *loss_host = *I.loss_pinned;
         } else {
@@ -854,6 +995,7 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
         }
     }
     CK(cudaPeekAtLastError());
+    if (I.debug) fprintf(stderr, "[bfpp rank %d] step %d enqueued\n", rank_, I.step_no);
     if (o_.profile_kernels) {
         CK(cudaEventSynchronize(I.step_end));
         for (const auto& mk : I.marks) {
@@ -898,7 +1040,7 @@ void Executor::sync() {
     CK(cudaSetDevice(impl_->dev));
     CK(cudaStreamSynchronize(impl_->st[S_COMPUTE]));
     ncclResult_t async_err = ncclSuccess;
-    for (ncclComm_t cm : {impl_->dp_comm, impl_->fwd_out, impl_->fwd_in, impl_->bwd_out, impl_->bwd_in})
+    for (ncclComm_t cm : {impl_->world_comm, impl_->dp_comm})
         if (cm && ncclCommGetAsyncError(cm, &async_err) == ncclSuccess && async_err != ncclSuccess)
             throw std::runtime_error(std::string("NCCL async error: ") + ncclGetErrorString(async_err));
 }

@@ -191,8 +191,13 @@ __global__ void __launch_bounds__(192, 1)
             }
             // P buffer and O are free once PV_{j-1} has completed
             if (j > 0) ptx::mbar_wait(o_done, (j - 1) & 1);
-            if (mx > m_used + kRescaleThreshold) {
-                const float alpha = m_used == -INFINITY ? 0.f : ptx::ex2_fast(m_used - mx);
+            // The rescale decision is per row, but tcgen05.ld/st are warp-collective
+            // (.sync.aligned): if any row of the warp needs it, the whole warp rescales (rows
+            // that do not need it use alpha = 1), so the TMEM accesses never diverge.
+            const bool mine = mx > m_used + kRescaleThreshold;
+            if (__any_sync(0xffffffffu, mine)) {
+                const float m_new = mine ? mx : m_used;
+                const float alpha = mine ? (m_used == -INFINITY ? 0.f : ptx::ex2_fast(m_used - mx)) : 1.f;
                 l *= alpha;
                 if (j > 0) {
                     ptx::tc_fence_after();
@@ -207,7 +212,7 @@ __global__ void __launch_bounds__(192, 1)
                     }
                     ptx::tmem_st_wait();
                 }
-                m_used = mx;
+                m_used = m_new;
             }
             float sum = 0.f;
 #pragma unroll

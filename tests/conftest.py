@@ -1,4 +1,5 @@
 import os
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # one hardware queue per executor stream (see executor.py)
 import sys
 
 import pytest

@@ -49,6 +49,19 @@ def test_attention_fwd_bwd(cuda_device, B, S, H):
         _close(dqkv[:, sl], ref_d[:, sl], 2e-2)
 
 
+def test_attention_peaked_rows_regression(cuda_device):
+    """Rows whose running max jumps by more than 2^8 in later key tiles next to rows whose max does
+    not (peaked attention late in training): the lazy O rescale must stay warp-uniform."""
+    ops = _ops()
+    B, S, H = 1, 512, 2
+    torch.manual_seed(11)
+    qkv = (4.0 * torch.randn(B * S, 3 * H * 128, device="cuda")).bfloat16()
+    o, lse = ops.attention_fwd(qkv, B, S, H)
+    ref = _ref_attention(qkv.float(), B, S, H).permute(0, 2, 1, 3).reshape(B * S, H * 128)
+    torch.cuda.synchronize()
+    _close(o, ref, 2e-2)
+
+
 @pytest.mark.parametrize("rows,width", [(64, 128), (300, 2048), (2048, 4096), (16, 8192), (33, 5120)])
 def test_layernorm(cuda_device, rows, width):
     ops = _ops()
