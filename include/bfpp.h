@@ -233,6 +233,16 @@ int bfpp_exec_get_weights16(bfpp_exec* e, int64_t stage, uint16_t* host, int64_t
 /* measured [start, end] (seconds from the step origin) of this rank's tasks in the last
  * step; tasks of other devices are NaN. Arrays have bfpp_graph_n_tasks entries. */
 int bfpp_exec_timeline(const bfpp_exec* e, double* start, double* end);
+/* The executor's per-rank plan (host only, no GPU needed): for pipeline rank pp_rank of a
+ * build_tasks graph, the local tasks in host enqueue order with their stream
+ * (0 compute, 1 DP, 2/3 forward send/receive, 4/5 backward send/receive), flags
+ * (1 send, 2 first reduce unit, 4 last reduce unit, 8 optimizer after, 16 first gradient
+ * contribution of its unit, 32 last optimizer update of the step), DP_FS weight slot and the
+ * cross-stream waits (CSR). Call with cap = 0 to get *n_tasks and *n_waits. */
+int bfpp_plan_rank(const bfpp_graph* g, int64_t pp_rank, int64_t n_dp, int64_t cap, int32_t* ids, int32_t* streams,
+                   int32_t* flags, int32_t* slots, int32_t* wait_offsets, int32_t* wait_ids, int64_t* n_tasks,
+                   int64_t* n_waits);
+
 /* toggles per-task timeline events and per-kernel profiling for subsequent steps */
 int bfpp_exec_set_flags(bfpp_exec* e, int32_t record_timeline, int32_t profile_kernels);
 /* the executor's compute stream (cudaStream_t); every step starts and ends on it */

@@ -80,6 +80,7 @@ _PROTOS = {
     "bfpp_bubble_fraction": (C.c_double, [_P]),
     "bfpp_peak_inflight": (C.c_int, [_P, _P, C.c_int64, _I64P]),
     "bfpp_compute_per_gpu": (C.c_double, [C.POINTER(ModelSpecC), C.POINTER(ParallelConfigC)]),
+    "bfpp_plan_rank": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64] + [_I32P] * 6 + [_I64P, _I64P]),
 }
 
 _lib = None

@@ -7,6 +7,7 @@
 #include "../../../include/bfpp.h"
 #include "../sched/capi_util.hpp"
 #include "executor.hpp"
+#include "plan.hpp"
 
 struct bfpp_exec {
     std::unique_ptr<bfpp::Executor> x;
@@ -94,6 +95,33 @@ int bfpp_exec_zero_grads(bfpp_exec* e) {
 }
 int bfpp_exec_timeline(const bfpp_exec* e, double* start, double* end) {
     return guarded([&] { e->x->timeline(start, end); });
+}
+
+int bfpp_plan_rank(const bfpp_graph* g, int64_t pp_rank, int64_t n_dp, int64_t cap, int32_t* ids, int32_t* streams,
+                   int32_t* flags, int32_t* slots, int32_t* wait_offsets, int32_t* wait_ids, int64_t* n_tasks,
+                   int64_t* n_waits) {
+    return guarded([&] {
+        if (pp_rank < 0 || pp_rank >= g->g.n_devices) throw SpecError("plan: pipeline rank out of range");
+        const std::vector<PlanTask> plan = plan_rank(g->g, pp_rank, n_dp);
+        int64_t nw = 0;
+        for (const PlanTask& p : plan) nw += static_cast<int64_t>(p.waits.size());
+        *n_tasks = static_cast<int64_t>(plan.size());
+        *n_waits = nw;
+        if (cap == 0) return;
+        if (cap < static_cast<int64_t>(plan.size())) throw SpecError("plan: output buffer too small");
+        int32_t k = 0;
+        for (size_t i = 0; i < plan.size(); ++i) {
+            const PlanTask& p = plan[i];
+            ids[i] = p.id;
+            streams[i] = p.stream;
+            flags[i] = (p.send ? 1 : 0) | (p.first_unit ? 2 : 0) | (p.last_unit ? 4 : 0) | (p.adam_after ? 8 : 0) |
+                       (p.first_in_unit ? 16 : 0) | (p.adam_tail ? 32 : 0);
+            slots[i] = p.slot;
+            wait_offsets[i] = k;
+            for (TaskId w : p.waits) wait_ids[k++] = w;
+        }
+        wait_offsets[plan.size()] = k;
+    });
 }
 
 int bfpp_exec_set_flags(bfpp_exec* e, int32_t record_timeline, int32_t profile_kernels) {

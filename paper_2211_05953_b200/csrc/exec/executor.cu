@@ -21,6 +21,7 @@
 
 #include "../kernels/gemm.hpp"
 #include "../kernels/kernels.hpp"
+#include "plan.hpp"
 
 namespace bfpp {
 
@@ -172,23 +173,7 @@ struct LocalStage {
     bf16* w16_shard = nullptr;
 };
 
-enum StreamId {
-    S_COMPUTE = 0, S_DP = 1, S_FWD_SEND = 2, S_FWD_RECV = 3, S_BWD_SEND = 4, S_BWD_RECV = 5,
-    S_WGRAD = 6,  // weight-gradient GEMMs of backward tasks, overlapping the data-gradient chain
-    S_N = 7
-};
-
-struct TaskExec {
-    TaskId id;
-    int stream;
-    bool send = false;          // Transfer: this rank sends (else receives)
-    int slot = -1;              // DP_FS weight slot used (compute) or filled (reconstruct)
-    bool first_unit = false, last_unit = false;  // Reduce
-    bool adam_after = false;    // Bwd (n_dp == 1) or Reduce (last unit): run the optimizer for this stage
-    bool first_in_unit = false; // Bwd: first gradient contribution of its reduction unit (overwrite, no zeroing)
-    bool adam_tail = false;     // the step's last optimizer update (nothing left to overlap: full-chip grid)
-    std::vector<TaskId> waits;  // events to wait on (deps on other streams + resource deps)
-};
+using TaskExec = PlanTask;
 
 struct Executor::Impl {
     int dev = 0;
@@ -473,140 +458,13 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
     I.task_c.assign(n, -1);
     I.tl_start.assign(n, NAN);
     I.tl_end.assign(n, NAN);
-    // enqueue order = start order of a simulation with positive durations (a topological order
-    // consistent with every lane's program/priority order on this device)
-    TimingModel tm;
-    tm.t_fwd_stage = 1.0;
-    tm.bwd_ratio = 2.0;
-    tm.t_pp_transfer = 0.01;
-    tm.t_dp_reduce_stage = 0.05;
-    tm.t_dp_reconstruct_stage = 0.05;
-    const Timeline sim = simulate(graph_, tm);
-    std::vector<TaskId> mine;
-    for (const Task& t : graph_.tasks) {
-        const bool local = t.device == pp_rank_ || (t.kind == TaskKind::Transfer && t.peer_device == pp_rank_);
-        if (local) mine.push_back(t.id);
-    }
-    std::stable_sort(mine.begin(), mine.end(), [&](TaskId a, TaskId b) {
-        return sim.events[static_cast<size_t>(a)].start < sim.events[static_cast<size_t>(b)].start;
-    });
-    // reconstruct slot numbering (creation order per device) and Reduce unit bookkeeping
-    std::map<TaskId, int> rec_slot;
-    {
-        int k = 0;
-        for (const Task& t : graph_.tasks)
-            if (t.kind == TaskKind::Reconstruct && t.device == pp_rank_) rec_slot[t.id] = (k++) & 1;
-    }
-    std::map<TaskId, TaskId> reduce_of_last_bwd;      // last Bwd of a unit -> its Reduce
-    std::map<i64, std::vector<TaskId>> reduces_of_stage;
-    for (const Task& t : graph_.tasks)
-        if (t.kind == TaskKind::Reduce && t.device == pp_rank_) {
-            reduce_of_last_bwd[t.deps[0]] = t.id;
-            reduces_of_stage[t.stage].push_back(t.id);
-        }
-    for (auto& kv : reduces_of_stage)
-        std::sort(kv.second.begin(), kv.second.end(), [&](TaskId a, TaskId b) {
-            return graph_.tasks[static_cast<size_t>(a)].priority < graph_.tasks[static_cast<size_t>(b)].priority;
-        });
-    std::map<i64, TaskId> last_bwd_of_stage, prev_bwd;
-    for (TaskId id : graph_.compute_program[static_cast<size_t>(pp_rank_)]) {
-        const Task& t = graph_.tasks[static_cast<size_t>(id)];
-        if (t.kind == TaskKind::Bwd) last_bwd_of_stage[t.stage] = id;
-    }
-    auto stream_of = [&](const Task& t, bool* send) {
-        if (t.lane == Lane::Compute) return static_cast<int>(S_COMPUTE);
-        if (t.lane == Lane::DpNet) return static_cast<int>(S_DP);
-        const bool fwd = graph_.tasks[static_cast<size_t>(t.deps[0])].kind == TaskKind::Fwd;
-        *send = t.device == pp_rank_;
-        return static_cast<int>(fwd ? (*send ? S_FWD_SEND : S_FWD_RECV) : (*send ? S_BWD_SEND : S_BWD_RECV));
-    };
-    std::vector<int> stream_of_task(n, -1);
-    for (TaskId id : mine) {
-        bool send = false;
-        stream_of_task[static_cast<size_t>(id)] = stream_of(graph_.tasks[static_cast<size_t>(id)], &send);
-    }
-    for (TaskId id : mine) {
-        const Task& t = graph_.tasks[static_cast<size_t>(id)];
-        TaskExec te;
-        te.id = id;
-        te.stream = stream_of(t, &te.send);
-        if (t.lane == Lane::Compute) I.task_c[static_cast<size_t>(id)] = static_cast<int>(t.stage / p_);
-        for (TaskId d : t.deps) {
-            const Task& dt = graph_.tasks[static_cast<size_t>(d)];
-            if (t.kind == TaskKind::Transfer && !te.send) continue;  // the receive side has no local deps
-            if (dt.kind == TaskKind::Reconstruct && t.lane == Lane::Compute) te.slot = rec_slot[d];
-            if (stream_of_task[static_cast<size_t>(d)] == te.stream) continue;  // same stream: FIFO order
-            if (stream_of_task[static_cast<size_t>(d)] < 0) continue;           // remote (reached via a transfer)
-            te.waits.push_back(d);
-        }
-        if (t.kind == TaskKind::Reconstruct) te.slot = rec_slot[id];
-        if (t.kind == TaskKind::Bwd) {
-            // a new reduction unit of this stage may only start once the previous unit's
-            // reduce-scatter has drained (and re-zeroed) the stage's gradient buffer
-            auto pb = prev_bwd.find(t.stage);
-            if (pb == prev_bwd.end()) te.first_in_unit = true;
-            if (pb != prev_bwd.end()) {
-                auto r = reduce_of_last_bwd.find(pb->second);
-                if (r != reduce_of_last_bwd.end()) {
-                    te.waits.push_back(r->second);
-                    te.first_in_unit = true;
-                }
-            }
-            prev_bwd[t.stage] = id;
-            if (c_.n_dp < 2 && last_bwd_of_stage[t.stage] == id) te.adam_after = true;
-        }
-        if (t.kind == TaskKind::Reduce) {
-            const auto& rs = reduces_of_stage[t.stage];
-            te.first_unit = rs.front() == id;
-            te.last_unit = rs.back() == id;
-            te.adam_after = te.last_unit;
-        }
-        I.order.push_back(te);
-        CK(cudaEventCreateWithFlags(&I.done[static_cast<size_t>(id)], cudaEventDisableTiming));
+    I.order = plan_rank(graph_, pp_rank_, c_.n_dp);
+    for (const TaskExec& te : I.order) {
+        const Task& t = graph_.tasks[static_cast<size_t>(te.id)];
+        if (t.lane == Lane::Compute) I.task_c[static_cast<size_t>(te.id)] = static_cast<int>(t.stage / p_);
+        CK(cudaEventCreateWithFlags(&I.done[static_cast<size_t>(te.id)], cudaEventDisableTiming));
         if (t.kind == TaskKind::Bwd)
-            CK(cudaEventCreateWithFlags(&I.done_g[static_cast<size_t>(id)], cudaEventDisableTiming));
-    }
-    // Host enqueue order: a topological order of this rank's tasks over the explicit waits
-    // (graph deps on other streams + the executor's gradient-buffer resource deps) and the
-    // per-stream FIFO order, ties broken by simulated start. Every event is then recorded
-    // before any stream waits on it.
-    {
-        const size_t m = I.order.size();
-        std::map<TaskId, size_t> pos;
-        for (size_t i = 0; i < m; ++i) pos[I.order[i].id] = i;
-        std::vector<std::vector<size_t>> succ(m);
-        std::vector<int> indeg(m, 0);
-        std::vector<long> last(S_N, -1);
-        for (size_t i = 0; i < m; ++i) {
-            const TaskExec& te = I.order[i];
-            if (last[te.stream] >= 0) {
-                succ[static_cast<size_t>(last[te.stream])].push_back(i);
-                ++indeg[i];
-            }
-            last[te.stream] = static_cast<long>(i);
-            for (TaskId w : te.waits) {
-                succ[pos.at(w)].push_back(i);
-                ++indeg[i];
-            }
-        }
-        std::set<size_t> ready;
-        for (size_t i = 0; i < m; ++i)
-            if (indeg[i] == 0) ready.insert(i);
-        std::vector<TaskExec> sorted;
-        while (!ready.empty()) {
-            const size_t i = *ready.begin();
-            ready.erase(ready.begin());
-            sorted.push_back(I.order[i]);
-            for (size_t j : succ[i])
-                if (--indeg[j] == 0) ready.insert(j);
-        }
-        if (sorted.size() != m) throw SimError("executor: cyclic local dependencies");
-        I.order = std::move(sorted);
-        for (size_t i = I.order.size(); i-- > 0;)
-            if (I.order[i].adam_after) {
-                I.order[i].adam_tail = true;
-                break;
-            }
+            CK(cudaEventCreateWithFlags(&I.done_g[static_cast<size_t>(te.id)], cudaEventDisableTiming));
     }
     set_flags(o.record_timeline, o.profile_kernels);
     CK(cudaEventCreate(&I.origin));

@@ -158,11 +158,29 @@ class Executor:
             pass
 
 
+STREAMS = ("compute", "dp", "fwd_send", "fwd_recv", "bwd_send", "bwd_recv", "wgrad")
+
+
+def plan_rank(graph: ps.TaskGraph, pp_rank: int, n_dp: int):
+    """The executor's per-rank plan (host only): [(task id, stream, flags, slot, waits)] in enqueue order."""
+    L = N.lib()
+    nt, nw = C.c_int64(), C.c_int64()
+    z = C.POINTER(C.c_int32)()
+    _check(L.bfpp_plan_rank(graph.handle, pp_rank, n_dp, 0, z, z, z, z, z, z, C.byref(nt), C.byref(nw)))
+    n, m = nt.value, nw.value
+    arr = lambda k: (C.c_int32 * max(1, k))()  # noqa: E731
+    ids, streams, flags, slots, woff, wids = arr(n), arr(n), arr(n), arr(n), arr(n + 1), arr(m)
+    _check(L.bfpp_plan_rank(graph.handle, pp_rank, n_dp, n, ids, streams, flags, slots, woff, wids, C.byref(nt),
+                            C.byref(nw)))
+    return [(ids[i], streams[i], flags[i], slots[i], list(wids[woff[i]:woff[i + 1]])) for i in range(n)]
+
+
 def measured_timeline(graph: ps.TaskGraph, starts: Sequence[np.ndarray], ends: Sequence[np.ndarray]) -> ps.Timeline:
     """Merges per-rank task times (NaN where a rank does not own a task) into one Timeline."""
     s = np.full(len(graph.tasks), np.nan)
     e = np.full(len(graph.tasks), np.nan)
     for a, b in zip(starts, ends):
+        a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
         m = ~np.isnan(a)
         s[m] = a[m]
         e[m] = b[m]
