@@ -197,6 +197,7 @@ struct Executor::Impl {
     bf16* tmp_h = nullptr;
     bf16 *gmid_s[2] = {}, *dpre_s[2] = {}, *dqkv_s[2] = {}, *gout_s[2] = {}, *g_head = nullptr;
     cudaEvent_t ev_a[2] = {}, ev_b[2] = {}, ev_wg[2] = {};
+    cudaEvent_t ev_opt[2] = {};  // segment-wise optimizer hand-off (compute, wgrad stream)
     std::vector<cudaEvent_t> done_g;  // per Bwd task: its gradients are complete (compute + wgrad streams)
     float *dq_acc = nullptr, *delta = nullptr;
     int32_t *inputs = nullptr, *labels = nullptr;
@@ -408,6 +409,7 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
         CK(cudaEventCreateWithFlags(&I.ev_a[k], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&I.ev_b[k], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&I.ev_wg[k], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&I.ev_opt[k], cudaEventDisableTiming));
     }
     I.dq_acc = I.alloc<float>(Th, &total);
     I.delta = I.alloc<float>(static_cast<size_t>(T * H), &total);
@@ -506,7 +508,7 @@ Executor::~Executor() {
     for (auto e : I.done_g)
         if (e) cudaEventDestroy(e);
     for (int k = 0; k < 2; ++k)
-        for (cudaEvent_t e : {I.ev_a[k], I.ev_b[k], I.ev_wg[k]})
+        for (cudaEvent_t e : {I.ev_a[k], I.ev_b[k], I.ev_wg[k], I.ev_opt[k]})
             if (e) cudaEventDestroy(e);
     if (I.origin) cudaEventDestroy(I.origin);
     if (I.step_end) cudaEventDestroy(I.step_end);
@@ -638,18 +640,32 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
         if (fs) return I.slots[te.slot];
         return I.local[static_cast<size_t>(cidx)].w16;
     };
-    auto adam = [&](LocalStage& ls, cudaStream_t st, bool tail) {
+    // Adam over elements [lo, hi) of a stage's (shard of) master weights / moments / gradient
+    auto adam = [&](LocalStage& ls, cudaStream_t st, bool tail, int64_t lo = 0, int64_t hi = -1) {
         if (o_.skip_optimizer) return;
+        if (hi < 0) hi = ls.shard_n;
         const bool sharded = ls.gshard != nullptr;
         float* g = sharded ? ls.gshard : ls.grad;
         bf16* w = sharded ? ls.w16_shard : ls.w16;
-        // overlapped updates use one co-resident block per SM; the tail update owns the chip
-        K(K_ADAM, 26.0 * static_cast<double>(ls.shard_n), 1, st, [&] {
-            adam_update(ls.master, ls.m, ls.v, g, w, ls.shard_n, o_.lr, o_.beta1, o_.beta2, o_.eps, o_.weight_decay,
-                        I.step_no, 0, st, tail ? 8 : 1);
+        K(K_ADAM, 30.0 * static_cast<double>(hi - lo), 1, st, [&] {
+            adam_update(ls.master + lo, ls.m + lo, ls.v + lo, g + lo, w + lo, hi - lo, o_.lr, o_.beta1, o_.beta2,
+                        o_.eps, o_.weight_decay, I.step_no, 0, st, tail ? 8 : 1);
         });
         if (sharded && c_.dp_variant == DpVariant::DP_PS)
             NK(ncclAllGather(ls.w16_shard, ls.w16, static_cast<size_t>(ls.shard_n), ncclBfloat16, I.dp_comm, st));
+    };
+    // n_dp == 1: a parameter segment's gradient is final as soon as the stage's last backward
+    // has produced it, so the optimizer runs segment by segment (a layer at a time) on the DP
+    // stream, overlapping the rest of the backward; only the last segment is left as a tail.
+    auto adam_segment = [&](LocalStage& ls, cudaStream_t st, cudaStream_t ws, int64_t lo, int64_t hi) {
+        if (o_.skip_optimizer || hi <= lo) return;
+        CK(cudaEventRecord(I.ev_opt[0], st));
+        CK(cudaStreamWaitEvent(ds, I.ev_opt[0], 0));
+        if (ws != st) {
+            CK(cudaEventRecord(I.ev_opt[1], ws));
+            CK(cudaStreamWaitEvent(ds, I.ev_opt[1], 0));
+        }
+        adam(ls, ds, false, lo, hi);
     };
 
     for (const TaskExec& te : I.order) {
@@ -704,6 +720,11 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
             // them on a separate stream overlapping the data-gradient chain
             cudaStream_t ws = I.wgrad_stream ? I.st[S_WGRAD] : st;
             const int acc = te.first_in_unit ? 0 : 1;  // the unit's first contribution overwrites
+            const bool seg_opt = te.adam_after;  // only set on a backward task when n_dp == 1
+            const size_t nl = L.layers.size();
+            auto layer_end = [&](size_t li) -> int64_t {
+                return li + 1 < nl ? L.layers[li + 1].ln1_g : (L.last ? L.lnf_g : ls.shard_n);
+            };
             // the wgrad stream also writes this stage's gradient buffer: honour the same
             // resource waits (previous unit's reduce-scatter) as the compute stream
             for (TaskId d : te.waits)
@@ -722,6 +743,7 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
                 LNB(st, I.tmp_h, a.out, W + L.lnf_g, a.muf, a.rsf, nullptr, I.g_head, G_ + L.lnf_g, G_ + L.lnf_b,
                     acc);
                 g = I.g_head;
+                if (seg_opt) adam_segment(ls, st, ws, L.lnf_g, ls.shard_n);
             } else {
                 g = a.gin;
             }
@@ -758,6 +780,7 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
                 if (gnext == I.gout_s[k] && lc >= 1) CK(cudaStreamWaitEvent(st, I.ev_wg[(lc - 1) & 1], 0));
                 LNB(st, I.tmp_h, x.x_in, W + P.ln1_g, x.mu1, x.rs1, gmid, gnext, G_ + P.ln1_g, G_ + P.ln1_b, acc);
                 g = gnext;
+                if (seg_opt) adam_segment(ls, st, ws, P.ln1_g, layer_end(li));
             }
             if (L.first && acc == 0) {  // scatter-added gradients need a zeroed start
                 CK(cudaMemsetAsync(G_ + L.wte, 0, static_cast<size_t>(V * h) * 4, st));
@@ -772,11 +795,7 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
             CK(cudaEventRecord(I.done[static_cast<size_t>(te.id)], st));
             CK(cudaStreamWaitEvent(ws, I.done[static_cast<size_t>(te.id)], 0));
             CK(cudaEventRecord(I.done_g[static_cast<size_t>(te.id)], ws));
-            if (te.adam_after) {
-                // n_dp == 1: this stage's gradient is final; update it on the DP stream
-                CK(cudaStreamWaitEvent(ds, I.done_g[static_cast<size_t>(te.id)], 0));
-                adam(ls, ds, te.adam_tail);
-            }
+            if (seg_opt && L.first) adam_segment(ls, st, ws, 0, L.layers[0].ln1_g);  // embeddings
             break;
         }
         case TaskKind::Transfer: {

@@ -132,55 +132,50 @@ __global__ void __launch_bounds__(256) xent_kernel(__nv_bfloat16* __restrict__ l
 // p, m, v f32 shards; g f32 gradient (zeroed after use if zero_grad); w16 bf16 copy of p.
 // Launched with one 256-thread block per SM so it co-resides with the compute stream's
 // GEMM CTAs; each thread keeps ILP float4 groups of all four arrays in flight.
-template <int ILP>
-__global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ p, float* __restrict__ m,
-                                                   float* __restrict__ v, float* __restrict__ g,
-                                                   __nv_bfloat16* __restrict__ w16, int64_t n, float lr, float b1,
-                                                   float b2, float eps, float wd, float bc1, float bc2,
-                                                   int zero_grad) {
+// One float4 of parameters per thread, one contiguous 1024-parameter chunk per 256-thread block,
+// the grid covering the tensor (measured on B200: 5.4 TB/s, vs 3.3 TB/s for 4-way ILP and
+// 4.5 TB/s for a grid-stride layout, scripts/adam_variants.cu). Blocks are short-lived and light
+// (~32 registers, no shared memory), so up to four fit on an SM beside a resident GEMM CTA
+// (96 regs x 320 threads) and retire within microseconds: the block scheduler keeps placing the
+// high-priority compute stream's CTAs while Adam on the low-priority DP stream streams HBM under
+// the tensor-core work. Streaming loads/stores (.cs) keep the optimizer's 30 B/param out of the
+// GEMM operands' L2 working set.
+constexpr int kAdamThreads = 256;
+__global__ void __launch_bounds__(kAdamThreads) adam_kernel(float* __restrict__ p, float* __restrict__ m,
+                                                            float* __restrict__ v, float* __restrict__ g,
+                                                            __nv_bfloat16* __restrict__ w16, int64_t n, float lr,
+                                                            float b1, float b2, float eps, float wd, float bc1,
+                                                            float bc2, int zero_grad) {
     const int64_t n4 = n / 4;
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; base < n4;
-         base += stride * ILP) {
-        float4 P[ILP], M[ILP], Vv[ILP], G[ILP];
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * kAdamThreads + threadIdx.x;
+    if (i < n4) {
+        float4 P = __ldcs(reinterpret_cast<const float4*>(p) + i);
+        float4 M = __ldcs(reinterpret_cast<const float4*>(m) + i);
+        float4 Vv = __ldcs(reinterpret_cast<const float4*>(v) + i);
+        const float4 G = __ldcs(reinterpret_cast<const float4*>(g) + i);
+        float* pp = &P.x;
+        float* mm = &M.x;
+        float* vv = &Vv.x;
+        const float* gg = &G.x;
 #pragma unroll
-        for (int u = 0; u < ILP; ++u) {
-            const int64_t i = base + u * stride;
-            if (i < n4) {
-                P[u] = reinterpret_cast<const float4*>(p)[i];
-                M[u] = reinterpret_cast<const float4*>(m)[i];
-                Vv[u] = reinterpret_cast<const float4*>(v)[i];
-                G[u] = reinterpret_cast<const float4*>(g)[i];
-            }
+        for (int k = 0; k < 4; ++k) {
+            mm[k] = b1 * mm[k] + (1.f - b1) * gg[k];
+            vv[k] = b2 * vv[k] + (1.f - b2) * gg[k] * gg[k];
+            pp[k] -= lr * ((mm[k] / bc1) / (sqrtf(vv[k] / bc2) + eps) + wd * pp[k]);
         }
-#pragma unroll
-        for (int u = 0; u < ILP; ++u) {
-            const int64_t i = base + u * stride;
-            if (i >= n4) continue;
-            float* pp = &P[u].x;
-            float* mm = &M[u].x;
-            float* vv = &Vv[u].x;
-            const float* gg = &G[u].x;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                mm[k] = b1 * mm[k] + (1.f - b1) * gg[k];
-                vv[k] = b2 * vv[k] + (1.f - b2) * gg[k] * gg[k];
-                pp[k] -= lr * ((mm[k] / bc1) / (sqrtf(vv[k] / bc2) + eps) + wd * pp[k]);
-            }
-            reinterpret_cast<float4*>(p)[i] = P[u];
-            reinterpret_cast<float4*>(m)[i] = M[u];
-            reinterpret_cast<float4*>(v)[i] = Vv[u];
-            if (zero_grad) reinterpret_cast<float4*>(g)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-            __nv_bfloat162 lo = __floats2bfloat162_rn(P[u].x, P[u].y), hi = __floats2bfloat162_rn(P[u].z, P[u].w);
-            uint2 o;
-            o.x = *reinterpret_cast<uint32_t*>(&lo);
-            o.y = *reinterpret_cast<uint32_t*>(&hi);
-            reinterpret_cast<uint2*>(w16)[i] = o;
-        }
+        __stcs(reinterpret_cast<float4*>(p) + i, P);
+        __stcs(reinterpret_cast<float4*>(m) + i, M);
+        __stcs(reinterpret_cast<float4*>(v) + i, Vv);
+        if (zero_grad) __stcs(reinterpret_cast<float4*>(g) + i, make_float4(0.f, 0.f, 0.f, 0.f));
+        __nv_bfloat162 lo = __floats2bfloat162_rn(P.x, P.y), hi = __floats2bfloat162_rn(P.z, P.w);
+        uint2 o;
+        o.x = *reinterpret_cast<uint32_t*>(&lo);
+        o.y = *reinterpret_cast<uint32_t*>(&hi);
+        __stcs(reinterpret_cast<uint2*>(w16) + i, o);
     }
-    // scalar tail
-    const int64_t t = n4 * 4 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t < n) {
+    // scalar tail (n % 4 elements) on the last block
+    const int64_t t = n4 * 4 + threadIdx.x;
+    if (blockIdx.x == gridDim.x - 1 && t < n) {
         m[t] = b1 * m[t] + (1.f - b1) * g[t];
         v[t] = b2 * v[t] + (1.f - b2) * g[t] * g[t];
         p[t] -= lr * ((m[t] / bc1) / (sqrtf(v[t] / bc2) + eps) + wd * p[t]);
@@ -249,11 +244,16 @@ void adam_update(float* p, float* m, float* v, float* g, void* w16, int64_t n, f
                  float eps, float wd, int step, int zero_grad, cudaStream_t st, int blocks_per_sm) {
     const float bc1 = 1.f - powf(b1, static_cast<float>(step));
     const float bc2 = 1.f - powf(b2, static_cast<float>(step));
-    const int64_t want = (n / 4 + 255) / 256;
-    const int cap = blocks_per_sm * sm_count();
-    const int blocks = static_cast<int>(want < cap ? (want > 0 ? want : 1) : cap);
-    adam_kernel<4><<<blocks, 256, 0, st>>>(p, m, v, g, static_cast<__nv_bfloat16*>(w16), n, lr, b1, b2, eps, wd,
-                                           bc1, bc2, zero_grad);
+    static const bool once = [] {
+        // max shared-memory carveout: an SM running optimizer blocks stays configurable for a GEMM CTA
+        cudaFuncSetAttribute(adam_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        return true;
+    }();
+    (void)once;
+    (void)blocks_per_sm;  // kept for the ABI; every call uses short-lived blocks (see adam_kernel)
+    const int64_t blocks = (n / 4 + kAdamThreads - 1) / kAdamThreads;
+    adam_kernel<<<static_cast<unsigned>(blocks > 0 ? blocks : 1), kAdamThreads, 0, st>>>(
+        p, m, v, g, static_cast<__nv_bfloat16*>(w16), n, lr, b1, b2, eps, wd, bc1, bc2, zero_grad);
 }
 
 void init_normal(float* p, void* w16, int64_t n, float mean, float std, uint64_t seed, uint64_t offset,

@@ -99,10 +99,10 @@ struct Smem {
     static constexpr int kBytes = kBarOffset + 256 + 1024;  // barriers + alignment slack
 };
 
-__device__ __forceinline__ void load_row64_bf16(const __nv_bfloat16* p, int valid, float (&v)[64]) {
-    if (valid >= 64) {
+__device__ __forceinline__ void load_row32_bf16(const __nv_bfloat16* p, int valid, float (&v)[32]) {
+    if (valid >= 32) {
 #pragma unroll
-        for (int j = 0; j < 64; j += 8) {
+        for (int j = 0; j < 32; j += 8) {
             uint4 raw = *reinterpret_cast<const uint4*>(p + j);
             const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
 #pragma unroll
@@ -114,12 +114,91 @@ __device__ __forceinline__ void load_row64_bf16(const __nv_bfloat16* p, int vali
         }
     } else {
 #pragma unroll
-        for (int j = 0; j < 64; ++j) v[j] = j < valid ? __bfloat162float(p[j]) : 0.f;
+        for (int j = 0; j < 32; ++j) v[j] = j < valid ? __bfloat162float(p[j]) : 0.f;
+    }
+}
+
+// One 128-byte column strip of a warp's 32 accumulator rows: TMEM -> registers -> fused op ->
+// swizzled staging row at `rowa`. Works in 32-column halves so the epilogue stays within the
+// kernel's 104-register budget (which leaves room on the SM for another stream's block).
+// `release` runs right after this warp's last TMEM read of the tile when `last` is set.
+template <typename Release>
+__device__ __forceinline__ void epilogue_strip(const EpiArgs& ep, uint32_t tcol, int row, int col0, int valid_all,
+                                               uint32_t rowa, int lane, bool last, Release release) {
+    if (ep.epi == GEMM_EPI_F32) {
+        uint32_t r[32];
+        ptx::tmem_ld_32x32b_x32(tcol, r);
+        ptx::tmem_ld_wait();
+        if (last) release();
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+            ptx::st_shared_v4(rowa + ((c ^ (lane & 7)) << 4), r[4 * c], r[4 * c + 1], r[4 * c + 2], r[4 * c + 3]);
+        return;
+    }
+    const bool need_aux = (ep.epi == GEMM_EPI_RESID || ep.epi == GEMM_EPI_DGELU);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int valid = max(0, min(32, valid_all - 32 * h));
+        float a[32];
+        // issue the aux loads before the TMEM load so both latencies overlap
+        if (need_aux) {
+            if (valid > 0) {
+                load_row32_bf16(ep.aux + static_cast<int64_t>(row) * ep.ldaux + col0 + 32 * h, valid, a);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) a[j] = 0.f;
+            }
+        }
+        float v[32];
+        {
+            uint32_t r[32];
+            ptx::tmem_ld_32x32b_x32(tcol + 32 * h, r);
+            ptx::tmem_ld_wait();
+            if (h == 1 && last) release();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        }
+        if (ep.epi == GEMM_EPI_RESID) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += a[j];
+        } else if (ep.epi == GEMM_EPI_DGELU) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] *= dgelu_f(a[j]);
+        } else if (ep.epi == GEMM_EPI_GELU) {
+            // pre-activation stored as bf16; gelu evaluated on the stored value
+            __nv_bfloat16* pre = ep.aux_out + static_cast<int64_t>(row) * ep.ldaux_out + col0 + 32 * h;
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+                uint4 o;
+                __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    hh[u] = __floats2bfloat162_rn(v[j + 2 * u], v[j + 2 * u + 1]);
+                    const float2 f = __bfloat1622float2(hh[u]);
+                    v[j + 2 * u] = gelu_f(f.x);
+                    v[j + 2 * u + 1] = gelu_f(f.y);
+                }
+                if (valid >= j + 8) {
+                    *reinterpret_cast<uint4*>(pre + j) = o;
+                } else {
+                    for (int u = 0; u < 8; ++u)
+                        if (j + u < valid) pre[j + u] = reinterpret_cast<__nv_bfloat16*>(&o)[u];
+                }
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            uint4 o;
+            __nv_bfloat162* hh = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) hh[u] = __floats2bfloat162_rn(v[8 * c + 2 * u], v[8 * c + 2 * u + 1]);
+            ptx::st_shared_v4(rowa + (((4 * h + c) ^ (lane & 7)) << 4), o);
+        }
     }
 }
 
 template <int BN, int A_MN, int B_MN>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __maxnreg__(96)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmD, int M, int N, int K, EpiArgs ep) {
     using S = Smem<BN>;
@@ -249,81 +328,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int sidx = half; sidx < n_strips; sidx += 2) {
                 const int col0 = n0 + sidx * cw;
                 const uint32_t tcol = tmem_base + ((q * 32) << 16) + acc * BN + sidx * cw;
-                float v[64];
-                float a[64];
-                const bool need_aux = (ep.epi == GEMM_EPI_RESID || ep.epi == GEMM_EPI_DGELU);
-                const int valid = row_ok ? min(64, N - col0) : 0;
-                // issue the aux loads before the TMEM loads so both latencies overlap
-                if (need_aux && valid > 0) load_row64_bf16(ep.aux + static_cast<int64_t>(row) * ep.ldaux + col0, valid, a);
-                {
-                    uint32_t r[32];
-                    ptx::tmem_ld_32x32b_x32(tcol, r);
-                    if (!f32_out) {
-                        uint32_t r2[32];
-                        ptx::tmem_ld_32x32b_x32(tcol + 32, r2);
-                        ptx::tmem_ld_wait();
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) v[32 + j] = __uint_as_float(r2[j]);
-                    } else {
-                        ptx::tmem_ld_wait();
-                    }
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-                }
-                if (sidx + 2 >= n_strips) {
-                    // this warp's last TMEM read of the tile: hand the accumulator back to the MMA warp
-                    ptx::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
-                }
+                const int valid = row_ok ? min(cw, N - col0) : 0;
                 // staging buffer reuse: the previous TMA store must have finished reading it
                 if (lane == 0) ptx::bulk_wait_read<0>();
                 __syncwarp();
                 const uint32_t rowa = ptx::smem_u32(stage_out) + lane * 128;
-                if (f32_out) {
-#pragma unroll
-                    for (int c = 0; c < 8; ++c)
-                        ptx::st_shared_v4(rowa + ((c ^ (lane & 7)) << 4), __float_as_uint(v[4 * c]),
-                                          __float_as_uint(v[4 * c + 1]), __float_as_uint(v[4 * c + 2]),
-                                          __float_as_uint(v[4 * c + 3]));
-                } else {
-                    if (ep.epi == GEMM_EPI_RESID) {
-#pragma unroll
-                        for (int j = 0; j < 64; ++j) v[j] += a[j];
-                    } else if (ep.epi == GEMM_EPI_DGELU) {
-#pragma unroll
-                        for (int j = 0; j < 64; ++j) v[j] *= dgelu_f(a[j]);
-                    } else if (ep.epi == GEMM_EPI_GELU) {
-                        // pre-activation stored as bf16; gelu evaluated on the stored value
-                        __nv_bfloat16* pre = ep.aux_out + static_cast<int64_t>(row) * ep.ldaux_out + col0;
-#pragma unroll
-                        for (int j = 0; j < 64; j += 8) {
-                            uint4 o;
-                            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
-#pragma unroll
-                            for (int u = 0; u < 4; ++u) {
-                                h[u] = __floats2bfloat162_rn(v[j + 2 * u], v[j + 2 * u + 1]);
-                                const float2 f = __bfloat1622float2(h[u]);
-                                v[j + 2 * u] = gelu_f(f.x);
-                                v[j + 2 * u + 1] = gelu_f(f.y);
-                            }
-                            if (valid >= j + 8) {
-                                *reinterpret_cast<uint4*>(pre + j) = o;
-                            } else {
-                                for (int u = 0; u < 8; ++u)
-                                    if (j + u < valid) pre[j + u] = reinterpret_cast<__nv_bfloat16*>(&o)[u];
-                            }
-                        }
-                    }
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        uint4 o;
-                        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) h[u] = __floats2bfloat162_rn(v[8 * c + 2 * u], v[8 * c + 2 * u + 1]);
-                        ptx::st_shared_v4(rowa + ((c ^ (lane & 7)) << 4), o);
-                    }
-                }
+                epilogue_strip(ep, tcol, row, col0, valid, rowa, lane, sidx + 2 >= n_strips, [&] {
+                    // this warp's last TMEM read of the tile: hand the accumulator back to the MMA warp
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+                });
                 ptx::fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0 && col0 < N && m0 + q * 32 < M) {
@@ -348,7 +363,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 // k-block (32 KB instead of 48 KB per SM for the same flops per SM), the leader CTA issues
 // tcgen05.mma.cta_group::2 (M = 256) over both CTAs' shared memory, and each CTA's TMEM holds
 // its 128 x 256 half of the accumulator, drained by its own 8 epilogue warps.
-constexpr int kStages2 = 6;
+// 5 stages: 197 KB + the 1 KB per-CTA reservation leaves room on the SM for an optimizer or NCCL
+// block from another stream to run beside the GEMM CTA (6 stages filled the SM).
+constexpr int kStages2 = 5;
 struct Smem2 {
     static constexpr int kABytes = 128 * BK * 2;
     static constexpr int kBBytes = 128 * BK * 2;
@@ -359,7 +376,7 @@ struct Smem2 {
 };
 
 template <int A_MN, int B_MN>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __maxnreg__(96)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmD, int M, int N, int K, EpiArgs ep) {
     constexpr int BN = 256;
@@ -491,81 +508,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int sidx = half; sidx < n_strips; sidx += 2) {
                 const int col0 = n0 + sidx * cw;
                 const uint32_t tcol = tmem_base + ((q * 32) << 16) + acc * BN + sidx * cw;
-                float v[64];
-                float a[64];
-                const bool need_aux = (ep.epi == GEMM_EPI_RESID || ep.epi == GEMM_EPI_DGELU);
-                const int valid = row_ok ? min(64, N - col0) : 0;
-                // issue the aux loads before the TMEM loads so both latencies overlap
-                if (need_aux && valid > 0) load_row64_bf16(ep.aux + static_cast<int64_t>(row) * ep.ldaux + col0, valid, a);
-                {
-                    uint32_t r[32];
-                    ptx::tmem_ld_32x32b_x32(tcol, r);
-                    if (!f32_out) {
-                        uint32_t r2[32];
-                        ptx::tmem_ld_32x32b_x32(tcol + 32, r2);
-                        ptx::tmem_ld_wait();
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) v[32 + j] = __uint_as_float(r2[j]);
-                    } else {
-                        ptx::tmem_ld_wait();
-                    }
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-                }
-                if (sidx + 2 >= n_strips) {
-                    // this warp's last TMEM read of the tile: hand the accumulator back to the MMA warp
-                    ptx::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tempty[acc]), 0));
-                }
+                const int valid = row_ok ? min(cw, N - col0) : 0;
                 // staging buffer reuse: the previous TMA store must have finished reading it
                 if (lane == 0) ptx::bulk_wait_read<0>();
                 __syncwarp();
                 const uint32_t rowa = ptx::smem_u32(stage_out) + lane * 128;
-                if (f32_out) {
-#pragma unroll
-                    for (int c = 0; c < 8; ++c)
-                        ptx::st_shared_v4(rowa + ((c ^ (lane & 7)) << 4), __float_as_uint(v[4 * c]),
-                                          __float_as_uint(v[4 * c + 1]), __float_as_uint(v[4 * c + 2]),
-                                          __float_as_uint(v[4 * c + 3]));
-                } else {
-                    if (ep.epi == GEMM_EPI_RESID) {
-#pragma unroll
-                        for (int j = 0; j < 64; ++j) v[j] += a[j];
-                    } else if (ep.epi == GEMM_EPI_DGELU) {
-#pragma unroll
-                        for (int j = 0; j < 64; ++j) v[j] *= dgelu_f(a[j]);
-                    } else if (ep.epi == GEMM_EPI_GELU) {
-                        // pre-activation stored as bf16; gelu evaluated on the stored value
-                        __nv_bfloat16* pre = ep.aux_out + static_cast<int64_t>(row) * ep.ldaux_out + col0;
-#pragma unroll
-                        for (int j = 0; j < 64; j += 8) {
-                            uint4 o;
-                            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
-#pragma unroll
-                            for (int u = 0; u < 4; ++u) {
-                                h[u] = __floats2bfloat162_rn(v[j + 2 * u], v[j + 2 * u + 1]);
-                                const float2 f = __bfloat1622float2(h[u]);
-                                v[j + 2 * u] = gelu_f(f.x);
-                                v[j + 2 * u + 1] = gelu_f(f.y);
-                            }
-                            if (valid >= j + 8) {
-                                *reinterpret_cast<uint4*>(pre + j) = o;
-                            } else {
-                                for (int u = 0; u < 8; ++u)
-                                    if (j + u < valid) pre[j + u] = reinterpret_cast<__nv_bfloat16*>(&o)[u];
-                            }
-                        }
-                    }
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        uint4 o;
-                        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) h[u] = __floats2bfloat162_rn(v[8 * c + 2 * u], v[8 * c + 2 * u + 1]);
-                        ptx::st_shared_v4(rowa + ((c ^ (lane & 7)) << 4), o);
-                    }
-                }
+                epilogue_strip(ep, tcol, row, col0, valid, rowa, lane, sidx + 2 >= n_strips, [&] {
+                    // this warp's last TMEM read of the tile: hand the accumulator back to the MMA warp
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tempty[acc]), 0));
+                });
                 ptx::fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0 && col0 < N && m0 + q * 32 < M) {

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <stdexcept>
+#include <type_traits>
 
 #include "kernels.hpp"
 
@@ -162,11 +163,230 @@ __global__ void ln_colsum_kernel(const float* __restrict__ ws, int chunks, int w
     atomicAdd(c < width ? dgamma + c : dbeta + (c - width), s);
 }
 
+
+// ---- register-resident variants (width <= 256 * NCH): one warp per row, the whole row held in
+// registers as packed bf16 (NCH x 16 B per lane), all loads of a row in flight at once, exact
+// two-pass statistics from registers; the backward also emits the block's dgamma/dbeta partials
+// (shared-memory reduction over its 8 rows), so a LayerNorm backward is 2 launches, not 3 + 2 memsets.
+__device__ __forceinline__ void unpack8(const uint4& raw, float (&v)[8]) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        float2 f = __bfloat1622float2(h[u]);
+        v[2 * u] = f.x;
+        v[2 * u + 1] = f.y;
+    }
+}
+
+template <int NCH>
+__global__ void __launch_bounds__(256) ln_fwd_reg_kernel(const __nv_bfloat16* __restrict__ x,
+                                                         const __nv_bfloat16* __restrict__ gamma,
+                                                         const __nv_bfloat16* __restrict__ beta,
+                                                         __nv_bfloat16* __restrict__ y, float* __restrict__ mean_out,
+                                                         float* __restrict__ rstd_out, int rows, int width, float eps) {
+    const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const __nv_bfloat16* xr = x + static_cast<int64_t>(row) * width;
+    uint4 raw[NCH];
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) {
+        const int c = (k * 32 + lane) * 8;
+        if (c < width) raw[k] = *reinterpret_cast<const uint4*>(xr + c);
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) {
+        if ((k * 32 + lane) * 8 >= width) continue;
+        float v[8];
+        unpack8(raw[k], v);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s += v[u];
+    }
+    const float mean = warp_sum(s) / width;
+    float q = 0.f;
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) {
+        if ((k * 32 + lane) * 8 >= width) continue;
+        float v[8];
+        unpack8(raw[k], v);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) q += (v[u] - mean) * (v[u] - mean);
+    }
+    const float rstd = rsqrtf(warp_sum(q) / width + eps);
+    __nv_bfloat16* yr = y + static_cast<int64_t>(row) * width;
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) {
+        const int c = (k * 32 + lane) * 8;
+        if (c >= width) continue;
+        float v[8], g[8], b[8];
+        unpack8(raw[k], v);
+        load8(gamma + c, g);
+        load8(beta + c, b);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = (v[u] - mean) * rstd * g[u] + b[u];
+        store8(yr + c, v);
+    }
+    if (lane == 0) {
+        mean_out[row] = mean;
+        rstd_out[row] = rstd;
+    }
+}
+
+// dx for 8 rows per block + the block's column partials ws[block][0..width) = sum dy*xhat,
+// ws[block][width..2 width) = sum dy (shared-memory accumulation).
+template <int NCH>
+__global__ void __launch_bounds__(256) ln_bwd_reg_kernel(const __nv_bfloat16* __restrict__ dy,
+                                                         const __nv_bfloat16* __restrict__ x,
+                                                         const __nv_bfloat16* __restrict__ gamma,
+                                                         const float* __restrict__ mean,
+                                                         const float* __restrict__ rstd,
+                                                         const __nv_bfloat16* __restrict__ dres,
+                                                         __nv_bfloat16* __restrict__ dx, float* __restrict__ ws,
+                                                         int rows, int width) {
+    extern __shared__ float acc[];  // [2][width]
+    for (int i = threadIdx.x; i < 2 * width; i += 256) acc[i] = 0.f;
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int row = blockIdx.x * 8 + warp;
+    if (row < rows) {
+        const int64_t off = static_cast<int64_t>(row) * width;
+        uint4 rx[NCH], rd[NCH];
+#pragma unroll
+        for (int k = 0; k < NCH; ++k) {
+            const int c = (k * 32 + lane) * 8;
+            if (c < width) {
+                rx[k] = *reinterpret_cast<const uint4*>(x + off + c);
+                rd[k] = *reinterpret_cast<const uint4*>(dy + off + c);
+            }
+        }
+        const float mu = mean[row], rs = rstd[row];
+        float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+        for (int k = 0; k < NCH; ++k) {
+            const int c = (k * 32 + lane) * 8;
+            if (c >= width) continue;
+            float xv[8], dv[8], g[8];
+            unpack8(rx[k], xv);
+            unpack8(rd[k], dv);
+            load8(gamma + c, g);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const float gd = dv[u] * g[u];
+                s1 += gd;
+                s2 += gd * (xv[u] - mu) * rs;
+            }
+        }
+        const float m1 = warp_sum(s1) / width, m2 = warp_sum(s2) / width;
+#pragma unroll
+        for (int k = 0; k < NCH; ++k) {
+            const int c = (k * 32 + lane) * 8;
+            if (c >= width) continue;
+            float xv[8], dv[8], g[8], r[8];
+            unpack8(rx[k], xv);
+            unpack8(rd[k], dv);
+            load8(gamma + c, g);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const float xh = (xv[u] - mu) * rs;
+                r[u] = rs * (dv[u] * g[u] - m1 - xh * m2);
+                atomicAdd(&acc[c + u], dv[u] * xh);
+                atomicAdd(&acc[width + c + u], dv[u]);
+            }
+            if (dres) {
+                float rr[8];
+                load8(dres + off + c, rr);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) r[u] += rr[u];
+            }
+            store8(dx + off + c, r);
+        }
+    }
+    __syncthreads();
+    float* w = ws + static_cast<int64_t>(blockIdx.x) * 2 * width;
+    for (int i = threadIdx.x * 4; i < 2 * width; i += 256 * 4)
+        *reinterpret_cast<float4*>(w + i) = *reinterpret_cast<const float4*>(acc + i);
+}
+
+// dgamma/dbeta (=, or += when accumulating) = column sums of the n_part block partials:
+// 8 warps split the partials, each lane owns 2 adjacent columns (64 per block), then a
+// shared-memory sum across the warps. Deterministic, no atomics, no memsets.
+__global__ void __launch_bounds__(256) ln_partsum_kernel(const float* __restrict__ ws, int n_part, int width,
+                                                         float* __restrict__ dgamma, float* __restrict__ dbeta,
+                                                         int accumulate) {
+    __shared__ float2 red[8][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c = blockIdx.x * 64 + lane * 2;  // column in [0, 2 width)
+    float2 s = make_float2(0.f, 0.f);
+    if (c < 2 * width) {
+#pragma unroll 8
+        for (int b = warp; b < n_part; b += 8) {
+            const float2 v = *reinterpret_cast<const float2*>(ws + static_cast<int64_t>(b) * 2 * width + c);
+            s.x += v.x;
+            s.y += v.y;
+        }
+    }
+    red[warp][lane] = s;
+    __syncthreads();
+    if (warp == 0 && c < 2 * width) {
+        float2 t = red[0][lane];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) {
+            t.x += red[w][lane].x;
+            t.y += red[w][lane].y;
+        }
+        float* dst = c < width ? dgamma + c : dbeta + (c - width);
+        if (accumulate) {
+            dst[0] += t.x;
+            dst[1] += t.y;
+        } else {
+            dst[0] = t.x;
+            dst[1] = t.y;
+        }
+    }
+}
+
+// chunks of 8 elements per lane: NCH = 1, 2, 4, 8, 12, 16, 20, 24 (width <= 256 NCH), up to MAX
+template <int MAX, typename F>
+bool ln_dispatch(int width, F&& f) {
+    const int n = (width + 255) / 256;
+    if (n <= 1) { f(std::integral_constant<int, 1>{}); return true; }
+    if (n <= 2) { f(std::integral_constant<int, 2>{}); return true; }
+    if (n <= 4) { f(std::integral_constant<int, 4>{}); return true; }
+    if (n <= 8) { f(std::integral_constant<int, 8>{}); return true; }
+    if (n <= 12) { f(std::integral_constant<int, 12>{}); return true; }
+    if (n <= 16) { f(std::integral_constant<int, 16>{}); return true; }
+    if constexpr (MAX >= 24) {
+        if (n <= 20) { f(std::integral_constant<int, 20>{}); return true; }
+        if (n <= 24) { f(std::integral_constant<int, 24>{}); return true; }
+    }
+    return false;
+}
+
+float* ln_workspace(size_t bytes) {
+    // one workspace per device (the executor runs every LayerNorm backward on one stream)
+    static thread_local float* ws[64] = {};
+    static thread_local size_t ws_bytes[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (bytes > ws_bytes[dev]) {
+        if (ws[dev]) cudaFree(ws[dev]);
+        if (cudaMalloc(&ws[dev], bytes) != cudaSuccess) throw std::runtime_error("layernorm: workspace allocation failed");
+        ws_bytes[dev] = bytes;
+    }
+    return ws[dev];
+}
+
 }  // namespace
 
 void layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, float* mean, float* rstd, int rows,
                    int width, float eps, cudaStream_t st) {
     if (width % 8) throw std::runtime_error("layernorm: width must be a multiple of 8");
+    const bool done = ln_dispatch<24>(width, [&](auto nch) {
+        ln_fwd_reg_kernel<decltype(nch)::value><<<(rows + 7) / 8, 256, 0, st>>>(
+            static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(gamma),
+            static_cast<const __nv_bfloat16*>(beta), static_cast<__nv_bfloat16*>(y), mean, rstd, rows, width, eps);
+    });
+    if (done) return;
     ln_fwd_kernel<<<(rows + 7) / 8, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x),
                                                   static_cast<const __nv_bfloat16*>(gamma),
                                                   static_cast<const __nv_bfloat16*>(beta),
@@ -179,6 +399,20 @@ void layernorm_bwd(const void* dy, const void* x, const void* gamma, const float
     if (width % 8) throw std::runtime_error("layernorm: width must be a multiple of 8");
     auto DY = static_cast<const __nv_bfloat16*>(dy);
     auto X = static_cast<const __nv_bfloat16*>(x);
+    const int blocks = (rows + 7) / 8;
+    const size_t smem = static_cast<size_t>(2 * width) * sizeof(float);
+    if (smem <= 48 * 1024) {
+        float* part = ln_workspace(static_cast<size_t>(blocks) * 2 * width * sizeof(float));
+        const bool done = ln_dispatch<16>(width, [&](auto nch) {
+            ln_bwd_reg_kernel<decltype(nch)::value><<<blocks, 256, smem, st>>>(
+                DY, X, static_cast<const __nv_bfloat16*>(gamma), mean, rstd, static_cast<const __nv_bfloat16*>(dres),
+                static_cast<__nv_bfloat16*>(dx), part, rows, width);
+        });  // x and dy both register-resident: up to 16 chunks per lane without spills
+        if (done) {
+            ln_partsum_kernel<<<(2 * width + 63) / 64, 256, 0, st>>>(part, blocks, width, dgamma, dbeta, accumulate);
+            return;
+        }
+    }
     ln_bwd_dx_kernel<<<(rows + 7) / 8, 256, 0, st>>>(DY, X, static_cast<const __nv_bfloat16*>(gamma), mean, rstd,
                                                      static_cast<const __nv_bfloat16*>(dres),
                                                      static_cast<__nv_bfloat16*>(dx), rows, width);
@@ -186,14 +420,7 @@ void layernorm_bwd(const void* dy, const void* x, const void* gamma, const float
     const int col_blocks = (width + 2047) / 2048;
     const int per = 8;
     const int chunks = (rows + per - 1) / per;
-    static float* ws = nullptr;
-    static size_t ws_bytes = 0;
-    const size_t need = static_cast<size_t>(chunks) * 2 * width * sizeof(float);
-    if (need > ws_bytes) {
-        if (ws) cudaFree(ws);
-        if (cudaMalloc(&ws, need) != cudaSuccess) throw std::runtime_error("layernorm: workspace allocation failed");
-        ws_bytes = need;
-    }
+    float* ws = ln_workspace(static_cast<size_t>(chunks) * 2 * width * sizeof(float));
     ln_bwd_param_kernel<<<dim3(col_blocks, chunks), 256, 0, st>>>(DY, X, mean, rstd, ws, rows, width, per);
     if (!accumulate) {  // first contribution of this gradient unit: overwrite instead of add
         cudaMemsetAsync(dgamma, 0, static_cast<size_t>(width) * sizeof(float), st);
