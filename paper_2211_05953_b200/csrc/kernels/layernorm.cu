@@ -233,9 +233,10 @@ __global__ void __launch_bounds__(256) ln_fwd_reg_kernel(const __nv_bfloat16* __
 }
 
 // dx for 8 rows per block + the block's column partials ws[block][0..width) = sum dy*xhat,
-// ws[block][width..2 width) = sum dy (shared-memory accumulation).
+// ws[block][width..2 width) = sum dy: per 256-column chunk the 8 warps stage their values in
+// shared memory and each thread sums one column over the block's rows (no atomics).
 template <int NCH>
-__global__ void __launch_bounds__(256) ln_bwd_reg_kernel(const __nv_bfloat16* __restrict__ dy,
+__global__ void __launch_bounds__(256, 1) ln_bwd_reg_kernel(const __nv_bfloat16* __restrict__ dy,
                                                          const __nv_bfloat16* __restrict__ x,
                                                          const __nv_bfloat16* __restrict__ gamma,
                                                          const float* __restrict__ mean,
@@ -243,40 +244,51 @@ __global__ void __launch_bounds__(256) ln_bwd_reg_kernel(const __nv_bfloat16* __
                                                          const __nv_bfloat16* __restrict__ dres,
                                                          __nv_bfloat16* __restrict__ dx, float* __restrict__ ws,
                                                          int rows, int width) {
-    extern __shared__ float acc[];  // [2][width]
-    for (int i = threadIdx.x; i < 2 * width; i += 256) acc[i] = 0.f;
-    __syncthreads();
+    __shared__ __align__(16) float red[8][2][256];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int row = blockIdx.x * 8 + warp;
-    if (row < rows) {
-        const int64_t off = static_cast<int64_t>(row) * width;
-        uint4 rx[NCH], rd[NCH];
+    const bool valid = row < rows;
+    const int64_t off = static_cast<int64_t>(valid ? row : 0) * width;
+    // every load of the row up front (x, dy, gamma, and the residual gradient for small rows)
+    constexpr bool kPrefetch = NCH <= 8;
+    uint4 rx[NCH], rd[NCH], rg[kPrefetch ? NCH : 1], rr[kPrefetch ? NCH : 1];
 #pragma unroll
-        for (int k = 0; k < NCH; ++k) {
-            const int c = (k * 32 + lane) * 8;
-            if (c < width) {
-                rx[k] = *reinterpret_cast<const uint4*>(x + off + c);
-                rd[k] = *reinterpret_cast<const uint4*>(dy + off + c);
-            }
+    for (int k = 0; k < NCH; ++k) {
+        const int c = (k * 32 + lane) * 8;
+        if (valid && c < width) {
+            rx[k] = *reinterpret_cast<const uint4*>(x + off + c);
+            rd[k] = *reinterpret_cast<const uint4*>(dy + off + c);
+        } else {
+            rx[k] = make_uint4(0, 0, 0, 0);
+            rd[k] = make_uint4(0, 0, 0, 0);
         }
-        const float mu = mean[row], rs = rstd[row];
-        float s1 = 0.f, s2 = 0.f;
-#pragma unroll
-        for (int k = 0; k < NCH; ++k) {
-            const int c = (k * 32 + lane) * 8;
-            if (c >= width) continue;
-            float xv[8], dv[8], g[8];
-            unpack8(rx[k], xv);
-            unpack8(rd[k], dv);
-            load8(gamma + c, g);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const float gd = dv[u] * g[u];
-                s1 += gd;
-                s2 += gd * (xv[u] - mu) * rs;
-            }
+        if constexpr (kPrefetch) {
+            rg[k] = c < width ? *reinterpret_cast<const uint4*>(gamma + c) : make_uint4(0, 0, 0, 0);
+            rr[k] = (dres && valid && c < width) ? *reinterpret_cast<const uint4*>(dres + off + c)
+                                                 : make_uint4(0, 0, 0, 0);
         }
-        const float m1 = warp_sum(s1) / width, m2 = warp_sum(s2) / width;
+    }
+    const float mu = valid ? mean[row] : 0.f, rs = valid ? rstd[row] : 0.f;
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) {
+        const int c = (k * 32 + lane) * 8;
+        if (c >= width) continue;
+        float xv[8], dv[8], g[8];
+        unpack8(rx[k], xv);
+        unpack8(rd[k], dv);
+        if constexpr (kPrefetch) unpack8(rg[k], g);
+        else load8(gamma + c, g);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const float gd = dv[u] * g[u];
+            s1 += gd;
+            s2 += gd * (xv[u] - mu) * rs;
+        }
+    }
+    const float m1 = warp_sum(s1) / width, m2 = warp_sum(s2) / width;
+    // dx: independent chunks (no barriers), so the residual-gradient loads are all in flight together
+    if (valid) {
 #pragma unroll
         for (int k = 0; k < NCH; ++k) {
             const int c = (k * 32 + lane) * 8;
@@ -284,27 +296,50 @@ __global__ void __launch_bounds__(256) ln_bwd_reg_kernel(const __nv_bfloat16* __
             float xv[8], dv[8], g[8], r[8];
             unpack8(rx[k], xv);
             unpack8(rd[k], dv);
-            load8(gamma + c, g);
+            if constexpr (kPrefetch) unpack8(rg[k], g);
+            else load8(gamma + c, g);
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const float xh = (xv[u] - mu) * rs;
-                r[u] = rs * (dv[u] * g[u] - m1 - xh * m2);
-                atomicAdd(&acc[c + u], dv[u] * xh);
-                atomicAdd(&acc[width + c + u], dv[u]);
-            }
+            for (int u = 0; u < 8; ++u) r[u] = rs * (dv[u] * g[u] - m1 - (xv[u] - mu) * rs * m2);
             if (dres) {
-                float rr[8];
-                load8(dres + off + c, rr);
+                float rv[8];
+                if constexpr (kPrefetch) unpack8(rr[k], rv);
+                else load8(dres + off + c, rv);
 #pragma unroll
-                for (int u = 0; u < 8; ++u) r[u] += rr[u];
+                for (int u = 0; u < 8; ++u) r[u] += rv[u];
             }
             store8(dx + off + c, r);
         }
     }
-    __syncthreads();
-    float* w = ws + static_cast<int64_t>(blockIdx.x) * 2 * width;
-    for (int i = threadIdx.x * 4; i < 2 * width; i += 256 * 4)
-        *reinterpret_cast<float4*>(w + i) = *reinterpret_cast<const float4*>(acc + i);
+    // column partials over the block's 8 rows, one 256-column chunk at a time
+    float* wout = ws + static_cast<int64_t>(blockIdx.x) * 2 * width;
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) {
+        float xv[8], dv[8];
+        unpack8(rx[k], xv);
+        unpack8(rd[k], dv);
+        float4* rg = reinterpret_cast<float4*>(&red[warp][0][lane * 8]);
+        float4* rb = reinterpret_cast<float4*>(&red[warp][1][lane * 8]);
+        // rows past the end hold zeros in rx/rd, so they contribute nothing
+        rg[0] = make_float4(dv[0] * (xv[0] - mu) * rs, dv[1] * (xv[1] - mu) * rs, dv[2] * (xv[2] - mu) * rs,
+                            dv[3] * (xv[3] - mu) * rs);
+        rg[1] = make_float4(dv[4] * (xv[4] - mu) * rs, dv[5] * (xv[5] - mu) * rs, dv[6] * (xv[6] - mu) * rs,
+                            dv[7] * (xv[7] - mu) * rs);
+        rb[0] = make_float4(dv[0], dv[1], dv[2], dv[3]);
+        rb[1] = make_float4(dv[4], dv[5], dv[6], dv[7]);
+        __syncthreads();
+        const int col = k * 256 + threadIdx.x;
+        if (col < width) {
+            float tg = 0.f, tb = 0.f;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) {
+                tg += red[w][0][threadIdx.x];
+                tb += red[w][1][threadIdx.x];
+            }
+            wout[col] = tg;
+            wout[width + col] = tb;
+        }
+        __syncthreads();
+    }
 }
 
 // dgamma/dbeta (=, or += when accumulating) = column sums of the n_part block partials:
@@ -400,11 +435,10 @@ void layernorm_bwd(const void* dy, const void* x, const void* gamma, const float
     auto DY = static_cast<const __nv_bfloat16*>(dy);
     auto X = static_cast<const __nv_bfloat16*>(x);
     const int blocks = (rows + 7) / 8;
-    const size_t smem = static_cast<size_t>(2 * width) * sizeof(float);
-    if (smem <= 48 * 1024) {
+    {
         float* part = ln_workspace(static_cast<size_t>(blocks) * 2 * width * sizeof(float));
         const bool done = ln_dispatch<16>(width, [&](auto nch) {
-            ln_bwd_reg_kernel<decltype(nch)::value><<<blocks, 256, smem, st>>>(
+            ln_bwd_reg_kernel<decltype(nch)::value><<<blocks, 256, 0, st>>>(
                 DY, X, static_cast<const __nv_bfloat16*>(gamma), mean, rstd, static_cast<const __nv_bfloat16*>(dres),
                 static_cast<__nv_bfloat16*>(dx), part, rows, width);
         });  // x and dy both register-resident: up to 16 chunks per lane without spills

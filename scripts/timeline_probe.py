@@ -43,4 +43,9 @@ for _ in range(5):
 e1.record(stream)
 torch.cuda.synchronize()
 print("ms/step", e0.elapsed_time(e1) / 5)
+ex.set_flags(False, True)
+ex.step_device(tok, loss)
+ex.sync()
+for k, (n, ms, work) in ex.kernel_stats().items():
+    print(f"{k:14s} launches {n:5d}  {ms:8.3f} ms  {work / ms / 1e9 if ms else 0:10.1f} (G work/s)")
 ex.close()
