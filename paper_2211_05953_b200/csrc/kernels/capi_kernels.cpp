@@ -20,6 +20,14 @@ void check_launch() {
 
 extern "C" {
 
+int bfpp_gemm_config(int32_t mode, int32_t bn2) {
+    return guarded([&] {
+        if (mode != -1 && mode != 1 && mode != 2) throw SpecError("gemm_config: mode must be -1, 1 or 2");
+        if (bn2 != 0 && bn2 != 128 && bn2 != 256) throw SpecError("gemm_config: bn2 must be 0, 128 or 256");
+        bfpp::gemm_bf16_configure(mode, bn2);
+    });
+}
+
 int bfpp_gemm_bf16(const bfpp_gemm_args* a, void* stream) {
     return guarded([&] {
         GemmArgs g;

@@ -365,22 +365,24 @@ __global__ void __maxnreg__(96)
 // its 128 x 256 half of the accumulator, drained by its own 8 epilogue warps.
 // 5 stages: 197 KB + the 1 KB per-CTA reservation leaves room on the SM for an optimizer or NCCL
 // block from another stream to run beside the GEMM CTA (6 stages filled the SM).
-constexpr int kStages2 = 5;
+// BN = 128 (each CTA stages 64 rows of B, 24 KB/stage, 7 stages): opt-in variant (see gemm_bf16).
+template <int BN>
 struct Smem2 {
+    static constexpr int kStages = BN == 256 ? 5 : 7;
     static constexpr int kABytes = 128 * BK * 2;
-    static constexpr int kBBytes = 128 * BK * 2;
+    static constexpr int kBBytes = (BN / 2) * BK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kOutOffset = kStages2 * kStageBytes;
+    static constexpr int kOutOffset = kStages * kStageBytes;
     static constexpr int kBarOffset = kOutOffset + kEpiWarps * kStageBytesOut;
     static constexpr int kBytes = kBarOffset + 256 + 1024;
 };
 
-template <int A_MN, int B_MN>
+template <int BN, int A_MN, int B_MN>
 __global__ void __maxnreg__(96)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmD, int M, int N, int K, EpiArgs ep) {
-    constexpr int BN = 256;
-    using S = Smem2;
+    using S = Smem2<BN>;
+    constexpr int kStages2 = S::kStages;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kBarOffset);
@@ -424,7 +426,7 @@ __global__ void __maxnreg__(96)
             int stage = 0;
             uint32_t phase = 0;
             for (int t = pair; t < num_tiles; t += n_pairs) {
-                const int m0 = (t % m_tiles) * 256 + 128 * rank, n0 = (t / m_tiles) * BN + 128 * rank;
+                const int m0 = (t % m_tiles) * 256 + 128 * rank, n0 = (t / m_tiles) * BN + (BN / 2) * rank;
                 for (int kb = 0; kb < nk; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* sa = smem + stage * S::kStageBytes;
@@ -440,7 +442,7 @@ __global__ void __maxnreg__(96)
                     }
                     if (B_MN) {
 #pragma unroll
-                        for (int i = 0; i < 2; ++i)
+                        for (int i = 0; i < BN / 128; ++i)
                             ptx::tma_load_2d_2sm(sb + i * 64 * BK * 2, &tmB, &full[stage], n0 + 64 * i, k0);
                     } else {
                         ptx::tma_load_2d_2sm(sb, &tmB, &full[stage], k0, n0);
@@ -567,26 +569,27 @@ void launch(const GemmArgs& g, cudaStream_t st) {
                                                    static_cast<int>(g.K), ep);
 }
 
-template <int A_MN, int B_MN>
+template <int BN, int A_MN, int B_MN>
 void launch2(const GemmArgs& g, cudaStream_t st) {
     CUtensorMap ta = A_MN ? make_tma_2d(g.A, g.M, g.K, g.lda, BK, false) : make_tma_2d(g.A, g.K, g.M, g.lda, 128, false);
-    CUtensorMap tb = B_MN ? make_tma_2d(g.B, g.N, g.K, g.ldb, BK, false) : make_tma_2d(g.B, g.K, g.N, g.ldb, 128, false);
+    CUtensorMap tb = B_MN ? make_tma_2d(g.B, g.N, g.K, g.ldb, BK, false)
+                          : make_tma_2d(g.B, g.K, g.N, g.ldb, BN / 2, false);
     const bool f32 = g.epilogue == GEMM_EPI_F32;
     CUtensorMap td = make_tma_2d(g.D, g.N, g.M, g.ldd, 32, f32);
     EpiArgs ep{static_cast<const __nv_bfloat16*>(g.aux), g.ldaux, static_cast<__nv_bfloat16*>(g.aux_out),
                g.ldaux_out, g.epilogue, g.accumulate};
-    auto kern = gemm2_kernel<A_MN, B_MN>;
+    auto kern = gemm2_kernel<BN, A_MN, B_MN>;
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem2::kBytes);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem2<BN>::kBytes);
         configured = true;
     }
-    const int tiles = static_cast<int>(((g.M + 255) / 256) * ((g.N + 255) / 256));
+    const int tiles = static_cast<int>(((g.M + 255) / 256) * ((g.N + BN - 1) / BN));
     const int pairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * pairs);
     cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = Smem2::kBytes;
+    cfg.dynamicSmemBytes = Smem2<BN>::kBytes;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -602,11 +605,20 @@ void launch2(const GemmArgs& g, cudaStream_t st) {
 }  // namespace
 
 int gemm_mode = -1;  // -1 auto, 1 force 1-CTA, 2 force 2-CTA (benchmarks / tests)
+int gemm_bn2 = 0;    // 2-CTA pair-tile width: 0 / 256 default, 128 opt-in (BFPP_GEMM_BN2; tests)
+
+static bool env_read = false;
+
+void gemm_bf16_configure(int mode, int bn2) {
+    env_read = true;
+    gemm_mode = mode;
+    gemm_bn2 = bn2;
+}
 
 void gemm_bf16(const GemmArgs& g, cudaStream_t st) {
-    static bool env_read = false;
     if (!env_read) {
         if (const char* e = getenv("BFPP_GEMM_MODE")) gemm_mode = atoi(e);
+        if (const char* e = getenv("BFPP_GEMM_BN2")) gemm_bn2 = atoi(e);
         env_read = true;
     }
     if (g.M <= 0 || g.N <= 0 || g.K <= 0) throw std::runtime_error("gemm: empty problem");
@@ -615,10 +627,19 @@ void gemm_bf16(const GemmArgs& g, cudaStream_t st) {
     const int a = g.a_mn_major ? 1 : 0, b = g.b_mn_major ? 1 : 0;
     const bool pair = gemm_mode == 2 || (gemm_mode < 0 && g.M >= 256 && g.N >= 256);
     if (pair) {
-        if (a == 0 && b == 0) return launch2<0, 0>(g, st);
-        if (a == 0 && b == 1) return launch2<0, 1>(g, st);
-        if (a == 1 && b == 0) return launch2<1, 0>(g, st);
-        return launch2<1, 1>(g, st);
+        // 256 x 128 pair tiles even out wave counts but measured 25-30 % slower per flop than
+        // 256 x 256 on the 2048 x 8192 GEMMs (scripts/gemm_bench.py), so they are opt-in only
+        const bool narrow = gemm_bn2 == 128;
+        if (narrow) {
+            if (a == 0 && b == 0) return launch2<128, 0, 0>(g, st);
+            if (a == 0 && b == 1) return launch2<128, 0, 1>(g, st);
+            if (a == 1 && b == 0) return launch2<128, 1, 0>(g, st);
+            return launch2<128, 1, 1>(g, st);
+        }
+        if (a == 0 && b == 0) return launch2<256, 0, 0>(g, st);
+        if (a == 0 && b == 1) return launch2<256, 0, 1>(g, st);
+        if (a == 1 && b == 0) return launch2<256, 1, 0>(g, st);
+        return launch2<256, 1, 1>(g, st);
     }
 #define BFPP_GEMM_CASE(BN_, A_, B_) \
     if (a == A_ && b == B_) return launch<BN_, A_, B_>(g, st);

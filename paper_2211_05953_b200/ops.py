@@ -52,6 +52,12 @@ def gemm(a: torch.Tensor, b: torch.Tensor, *, a_mn_major=False, b_mn_major=False
     return out
 
 
+def gemm_config(mode: int = -1, bn2: int = 0):
+    """Process-wide GEMM variant selection (tests / benchmarks): mode -1 auto, 1 one-CTA, 2 two-CTA;
+    bn2 = two-CTA tile width (0 auto, 128, 256)."""
+    _check(_nat.lib().bfpp_gemm_config(mode, bn2))
+
+
 def attention_fwd(qkv, batch, seq, heads, head_dim=128):
     T = batch * seq
     o = torch.empty(T, heads * head_dim, device=qkv.device, dtype=torch.bfloat16)

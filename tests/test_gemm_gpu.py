@@ -20,11 +20,23 @@ def _close(got, ref, rtol):
     assert err <= rtol * scale, (err, scale)
 
 
+# (mode, bn2): auto; one-CTA tiles; two-CTA 256x128 and 256x256 pair tiles (forced)
+VARIANTS = [(-1, 0), (1, 0), (2, 128), (2, 256)]
+
+
+@pytest.fixture(params=VARIANTS, ids=lambda v: f"mode{v[0]}-bn{v[1]}")
+def variant(request, cuda_device):
+    ops = _ops()
+    ops.gemm_config(*request.param)
+    yield request.param
+    ops.gemm_config(-1, 0)
+
+
 @pytest.mark.parametrize("a_mn", [False, True])
 @pytest.mark.parametrize("b_mn", [False, True])
 @pytest.mark.parametrize("shape", [(256, 512, 128), (128, 256, 64), (384, 768, 320), (64, 1000, 128),
-                                   (2048, 2048, 2048), (200, 136, 72)])
-def test_gemm_layouts(cuda_device, a_mn, b_mn, shape):
+                                   (2048, 2048, 2048), (200, 136, 72), (512, 8192, 256)])
+def test_gemm_layouts(variant, a_mn, b_mn, shape):
     ops = _ops()
     M, N, K = shape
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
@@ -41,7 +53,7 @@ def test_gemm_layouts(cuda_device, a_mn, b_mn, shape):
     _close(out32, ref, 1e-4)
 
 
-def test_gemm_epilogues(cuda_device):
+def test_gemm_epilogues(variant):
     ops = _ops()
     M, N, K = 256, 768, 192
     A = torch.randn(M, K, device="cuda").bfloat16()
