@@ -264,6 +264,8 @@ def main():
     kst = ex.kernel_stats()
     bubble = None
     sim_bubble = None
+    replay_bubble = None
+    peak_layers = None
     _progress('timeline')
     if not args.no_timeline:
         ex.set_flags(record_timeline=True, profile_kernels=False)
@@ -279,6 +281,9 @@ def main():
         tl = measured_timeline(ex.graph, [a for a, _ in rep0], [b for _, b in rep0])
         bubble = ps.bubble_fraction(tl)
         sim_bubble = (pp - 1) / (n_mb * loops)
+        # the same graph simulated with the measured per-kind task durations
+        replay_bubble = ps.bubble_fraction(ps.simulate(ex.graph, ps.measured_timing_model(ex.graph, tl)))
+        peak_layers = max(ps.peak_inflight(tl, ex.graph, ps.place_stages(ex.model, config)))
     ex.set_flags(False, False)
 
     pk, pk_kind = peaks()
@@ -347,7 +352,9 @@ def main():
                        "l2": "inputs larger than L2 (bf16 weights + activations >> 126 MB)"},
             "mfu": {"vs_spec_2250TF": mfu, "vs_measured_burst": mfu_meas,
                     "model_flops_per_token": fpt, "eq11_tflops_per_gpu": eq11 / 1e12},
-            "bubble_fraction": {"measured": bubble, "eq7": sim_bubble},
+            "bubble_fraction": {"measured": bubble, "eq7": sim_bubble,
+                                "simulated_with_measured_timing": replay_bubble,
+                                "peak_inflight_layers_measured": peak_layers},
             "loss": loss_val,
             "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clocks, "roofline": roofline,
             "cpu_baseline": cpu,

@@ -111,6 +111,14 @@ void bfpp_timeline_destroy(bfpp_timeline* tl);
 
 /* replaces bubble_fraction (simulate.cpp:160-164) */
 double bfpp_bubble_fraction(const bfpp_timeline* tl);
+/* replace chrome_trace_json (report.cpp:160-212; pybind module.cpp:375) and gantt_svg
+ * (report.cpp:248-290; module.cpp:376) for any timeline, simulated or measured. Two-call text
+ * pattern: *len = length without the terminator; up to cap-1 bytes + NUL written to buf (may be NULL). */
+int bfpp_chrome_trace_json(const bfpp_timeline* tl, const bfpp_graph* g, char* buf, int64_t cap, int64_t* len);
+int bfpp_gantt_svg(const bfpp_timeline* tl, const bfpp_graph* g, char* buf, int64_t cap, int64_t* len);
+/* Per-kind mean durations of a measured timeline as a TimingModel (closes the loop of
+ * TimingModel::derive, schedule.cpp:43-86: simulate the same graph with measured timings). */
+int bfpp_measured_timing_model(const bfpp_graph* g, const bfpp_timeline* tl, bfpp_timing_model* out);
 /* replaces peak_inflight (simulate.cpp:166-191); out[n_devices] */
 int bfpp_peak_inflight(const bfpp_timeline* tl, const bfpp_graph* g, int64_t layers_per_stage, int64_t* out);
 /* replaces compute_per_gpu (types.cpp:136-146; Eq. 11) */

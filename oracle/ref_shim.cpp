@@ -1,12 +1,13 @@
 // TEST INFRASTRUCTURE ONLY — the checker, never the product.
 //
 // extern "C" shim over the UNMODIFIED reference schedule/simulator sources
-// (/root/reference/proj/src/{types,memory,network,perf,schedule,simulate}.cpp),
+// (/root/reference/proj/src/{types,memory,network,perf,schedule,simulate,report}.cpp),
 // compiled by oracle/Makefile into oracle/_ref/libpipesim_ref.so. It exposes the
 // reference's build_tasks / simulate results (including Task::priority, which
 // the reference's own Python binding omits, bindings/module.cpp:185-193) with
 // the same POD layout as include/bfpp.h so tests can compare field by field.
 // Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg load it.
+#include <algorithm>
 #include <chrono>
 #include <cstring>
 #include <exception>
@@ -14,6 +15,7 @@
 
 #include "../include/bfpp.h"
 #include "pipesim/perf.hpp"
+#include "pipesim/report.hpp"
 #include "pipesim/schedule.hpp"
 #include "pipesim/simulate.hpp"
 
@@ -160,6 +162,22 @@ int ref_simulate(void* g, const bfpp_timing_model* t, double* start, double* end
             for (int l = 0; l < 3; ++l) lane_busy[d * 3 + l] = tl.lane_busy[d][static_cast<size_t>(l)];
         *makespan = tl.makespan;
         *bubble = bubble_fraction(tl);
+    });
+}
+
+// The reference's chrome_trace_json / gantt_svg of the simulated timeline of graph g
+// (which: 0 trace JSON, 1 SVG). Two-call pattern like the product's text exporters.
+int ref_timeline_text(void* g, const bfpp_timing_model* t, int32_t which, char* buf, int64_t cap, int64_t* len) {
+    return guard([&] {
+        const TaskGraph& graph = *static_cast<TaskGraph*>(g);
+        Timeline tl = simulate(graph, timing_of(t));
+        const std::string text = which == 0 ? chrome_trace_json(tl, graph) : gantt_svg(tl, graph);
+        *len = static_cast<int64_t>(text.size());
+        if (buf && cap > 0) {
+            const size_t n = std::min(static_cast<size_t>(cap - 1), text.size());
+            std::memcpy(buf, text.data(), n);
+            buf[n] = 0;
+        }
     });
 }
 

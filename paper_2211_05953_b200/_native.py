@@ -80,6 +80,9 @@ _PROTOS = {
     "bfpp_bubble_fraction": (C.c_double, [_P]),
     "bfpp_peak_inflight": (C.c_int, [_P, _P, C.c_int64, _I64P]),
     "bfpp_compute_per_gpu": (C.c_double, [C.POINTER(ModelSpecC), C.POINTER(ParallelConfigC)]),
+    "bfpp_chrome_trace_json": (C.c_int, [_P, _P, C.c_char_p, C.c_int64, _I64P]),
+    "bfpp_gantt_svg": (C.c_int, [_P, _P, C.c_char_p, C.c_int64, _I64P]),
+    "bfpp_measured_timing_model": (C.c_int, [_P, _P, C.POINTER(TimingModelC)]),
     "bfpp_plan_rank": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64] + [_I32P] * 6 + [_I64P, _I64P]),
 }
 

@@ -1,9 +1,11 @@
 // extern "C" boundary for the schedule layer (include/bfpp.h, schedule section).
+#include <algorithm>
 #include <cstring>
 #include <string>
 
 #include "../../../include/bfpp.h"
 #include "capi_util.hpp"
+#include "report.hpp"
 #include "schedule.hpp"
 
 namespace bfpp {
@@ -220,6 +222,38 @@ int bfpp_timeline_from_arrays(const bfpp_graph* g, const double* start, const do
 void bfpp_timeline_destroy(bfpp_timeline* tl) { delete tl; }
 
 double bfpp_bubble_fraction(const bfpp_timeline* tl) { return bubble_fraction(tl->tl); }
+
+namespace {
+int copy_text(const std::string& text, char* buf, int64_t cap, int64_t* len) {
+    *len = static_cast<int64_t>(text.size());
+    if (buf && cap > 0) {
+        const size_t n = std::min(static_cast<size_t>(cap - 1), text.size());
+        std::memcpy(buf, text.data(), n);
+        buf[n] = 0;
+    }
+    return 0;
+}
+}  // namespace
+
+int bfpp_chrome_trace_json(const bfpp_timeline* tl, const bfpp_graph* g, char* buf, int64_t cap, int64_t* len) {
+    return guarded([&] { copy_text(chrome_trace_json(tl->tl, g->g), buf, cap, len); });
+}
+
+int bfpp_gantt_svg(const bfpp_timeline* tl, const bfpp_graph* g, char* buf, int64_t cap, int64_t* len) {
+    return guarded([&] { copy_text(gantt_svg(tl->tl, g->g), buf, cap, len); });
+}
+
+int bfpp_measured_timing_model(const bfpp_graph* g, const bfpp_timeline* tl, bfpp_timing_model* out) {
+    return guarded([&] {
+        const TimingModel tm = measured_timing_model(g->g, tl->tl);
+        out->t_fwd_stage = tm.t_fwd_stage;
+        out->bwd_ratio = tm.bwd_ratio;
+        out->t_pp_transfer = tm.t_pp_transfer;
+        out->pp_latency = tm.pp_latency;
+        out->t_dp_reduce_stage = tm.t_dp_reduce_stage;
+        out->t_dp_reconstruct_stage = tm.t_dp_reconstruct_stage;
+    });
+}
 
 int bfpp_peak_inflight(const bfpp_timeline* tl, const bfpp_graph* g, int64_t layers_per_stage, int64_t* out) {
     return guarded([&] {

@@ -356,6 +356,32 @@ def peak_inflight(timeline: Timeline, graph: TaskGraph, placement: StagePlacemen
     return list(out)
 
 
+def _text(fn, timeline: Timeline, graph: TaskGraph) -> str:
+    n = C.c_int64()
+    _check(fn(timeline.handle, graph.handle, None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    _check(fn(timeline.handle, graph.handle, buf, n.value + 1, C.byref(n)))
+    return buf.value.decode()
+
+
+def chrome_trace_json(timeline: Timeline, graph: TaskGraph) -> str:
+    """Chrome trace-event JSON of a simulated or measured timeline (reference report.cpp:160-212)."""
+    return _text(N.lib().bfpp_chrome_trace_json, timeline, graph)
+
+
+def gantt_svg(timeline: Timeline, graph: TaskGraph) -> str:
+    """SVG Gantt chart, one row per device lane (reference report.cpp:248-290)."""
+    return _text(N.lib().bfpp_gantt_svg, timeline, graph)
+
+
+def measured_timing_model(graph: TaskGraph, timeline: Timeline) -> TimingModel:
+    """Per-kind mean task durations of a (measured) timeline as a TimingModel."""
+    t = N.TimingModelC()
+    _check(N.lib().bfpp_measured_timing_model(graph.handle, timeline.handle, C.byref(t)))
+    return TimingModel(t.t_fwd_stage, t.bwd_ratio, t.t_pp_transfer, t.pp_latency, t.t_dp_reduce_stage,
+                       t.t_dp_reconstruct_stage)
+
+
 def compute_per_gpu(model: ModelSpec, config: ParallelConfig) -> float:
     return float(N.lib().bfpp_compute_per_gpu(C.byref(model._c()), C.byref(config._c())))
 

@@ -45,6 +45,7 @@ def ref():
             "ref_simulate": (C.c_int, [P, T] + [C.POINTER(C.c_double)] * 5),
             "ref_peak_inflight": (C.c_int, [M, Cf, T, C.POINTER(C.c_int64)]),
             "ref_compute_per_gpu": (C.c_double, [M, Cf]),
+            "ref_timeline_text": (C.c_int, [P, T, C.c_int32, C.c_char_p, C.c_int64, C.POINTER(C.c_int64)]),
             "ref_time_schedule_path": (C.c_int, [M, Cf, T, C.c_int, C.POINTER(C.c_double),
                                                  C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
         }
@@ -112,3 +113,13 @@ def ref_simulate(h, t: N.TimingModelC, n_tasks: int, n_dev: int):
     if status != 0:
         return status, L.ref_last_error().decode()
     return 0, (list(st[:n_tasks]), list(en[:n_tasks]), list(lb), mk.value, bub.value)
+
+
+def ref_timeline_text(h, t: N.TimingModelC, which: int) -> str:
+    """The reference's chrome_trace_json (which=0) / gantt_svg (1) of the simulated timeline."""
+    L = ref()
+    n = C.c_int64()
+    assert L.ref_timeline_text(h, C.byref(t), which, None, 0, C.byref(n)) == 0, L.ref_last_error()
+    buf = C.create_string_buffer(n.value + 1)
+    assert L.ref_timeline_text(h, C.byref(t), which, buf, n.value + 1, C.byref(n)) == 0, L.ref_last_error()
+    return buf.value.decode()

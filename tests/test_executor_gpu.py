@@ -69,3 +69,19 @@ def test_measured_timeline_contract(cuda_device):
     for a, b in zip(prog, prog[1:]):
         assert tl.events[a].end <= tl.events[b].start + 1e-6
     assert 0 <= ps.bubble_fraction(tl) < 1.0
+
+
+@pytest.mark.gpu
+def test_cli_execute_writes_measured_trace(tmp_path, capsys, cuda_device):
+    """`python -m paper_2211_05953_b200 execute`: measured timeline -> bubble, replayed bubble, trace, Gantt."""
+    import json
+    from paper_2211_05953_b200.__main__ import main
+    trace, svg = tmp_path / "t.json", tmp_path / "g.svg"
+    assert main(["execute", "--model", "tiny", "--pp", "1", "--loops", "2", "--n-mb", "2", "--steps", "2",
+                 "--trace", str(trace), "--gantt", str(svg)]) == 0
+    out = dict(line.split(",", 1) for line in capsys.readouterr().out.splitlines())
+    assert float(out["tokens_per_second"]) > 0 and 0.0 <= float(out["bubble_fraction"]) < 1.0
+    assert 0.0 <= float(out["bubble_fraction_simulated_with_measured_timing"]) < 1.0
+    doc = json.loads(trace.read_text())
+    assert sum(e["ph"] == "X" for e in doc["traceEvents"]) == 2 * 2 * 2  # (fwd + bwd) x 2 stages x 2 mb
+    assert svg.read_text().startswith("<svg")
