@@ -218,6 +218,12 @@ int bfpp_nccl_unique_id(void* out);
 int64_t bfpp_exec_n_comm_ids(const bfpp_parallel_config* c);
 int bfpp_exec_create(const bfpp_model_spec* m, const bfpp_parallel_config* c, const bfpp_exec_opts* o,
                      int32_t rank, int32_t world, const void* uids, bfpp_exec** out);
+/* Same, running the given task graph instead of build_tasks(m, c) -- e.g. the gradient-accumulation
+ * graphs of bfpp_build_accumulation_tasks (schedule.cpp:454-500, PAPER Appendix C), executed with
+ * c = {n_pp 1, n_loop n_layers, n_mb, n_dp = ranks, dp_variant}. Validated against c (status 2). */
+int bfpp_exec_create_graph(const bfpp_model_spec* m, const bfpp_parallel_config* c, const bfpp_graph* g,
+                           const bfpp_exec_opts* o, int32_t rank, int32_t world, const void* uids,
+                           bfpp_exec** out);
 /* One training step (forward, backward, gradient reduction, Adam) over this replica's
  * tokens [n_mb][s_mb][s_seq+1] int32 (inputs = [..., :-1], labels = [..., 1:]).
  * bfpp_exec_step takes HOST tokens and returns the replica's mean token loss on the

@@ -50,6 +50,8 @@ PROTOS.update({
     "bfpp_exec_n_comm_ids": (_I64, [C.POINTER(ParallelConfigC)]),
     "bfpp_exec_create": (C.c_int, [C.POINTER(ModelSpecC), C.POINTER(ParallelConfigC), C.POINTER(ExecOptsC), _I32,
                                    _I32, _P, C.POINTER(_P)]),
+    "bfpp_exec_create_graph": (C.c_int, [C.POINTER(ModelSpecC), C.POINTER(ParallelConfigC), _P, C.POINTER(ExecOptsC),
+                                         _I32, _I32, _P, C.POINTER(_P)]),
     "bfpp_exec_step": (C.c_int, [_P, _P, C.POINTER(C.c_float)]),
     "bfpp_exec_step_device": (C.c_int, [_P, _P, _P]),
     "bfpp_exec_sync": (C.c_int, [_P]),

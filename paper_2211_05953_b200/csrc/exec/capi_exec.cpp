@@ -28,8 +28,9 @@ int bfpp_nccl_unique_id(void* out) {
 
 int64_t bfpp_exec_n_comm_ids(const bfpp_parallel_config* c) { return 1 + c->n_pp + 2 * c->n_pp * c->n_dp; }
 
-int bfpp_exec_create(const bfpp_model_spec* m, const bfpp_parallel_config* c, const bfpp_exec_opts* o, int32_t rank,
-                     int32_t world, const void* uids, bfpp_exec** out) {
+namespace {
+int create(const bfpp_model_spec* m, const bfpp_parallel_config* c, const bfpp_graph* g, const bfpp_exec_opts* o,
+           int32_t rank, int32_t world, const void* uids, bfpp_exec** out) {
     *out = nullptr;
     return guarded([&] {
         ExecOptions eo;
@@ -50,8 +51,21 @@ int bfpp_exec_create(const bfpp_model_spec* m, const bfpp_parallel_config* c, co
             ids.resize(static_cast<size_t>(n));
             std::memcpy(ids.data(), uids, static_cast<size_t>(n) * sizeof(ncclUniqueId));
         }
-        *out = new bfpp_exec{std::make_unique<Executor>(to_model(m), to_config(c), eo, rank, world, ids)};
+        *out = new bfpp_exec{
+            std::make_unique<Executor>(to_model(m), to_config(c), eo, rank, world, ids, g ? &g->g : nullptr)};
     });
+}
+}  // namespace
+
+int bfpp_exec_create(const bfpp_model_spec* m, const bfpp_parallel_config* c, const bfpp_exec_opts* o, int32_t rank,
+                     int32_t world, const void* uids, bfpp_exec** out) {
+    return create(m, c, nullptr, o, rank, world, uids, out);
+}
+
+int bfpp_exec_create_graph(const bfpp_model_spec* m, const bfpp_parallel_config* c, const bfpp_graph* g,
+                           const bfpp_exec_opts* o, int32_t rank, int32_t world, const void* uids,
+                           bfpp_exec** out) {
+    return create(m, c, g, o, rank, world, uids, out);
 }
 
 int bfpp_exec_step(bfpp_exec* e, const int32_t* tokens_host, float* loss) {

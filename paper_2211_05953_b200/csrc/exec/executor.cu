@@ -234,7 +234,7 @@ struct Executor::Impl {
 };
 
 Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOptions& o, int rank, int world,
-                   const std::vector<ncclUniqueId>& uids)
+                   const std::vector<ncclUniqueId>& uids, const TaskGraph* graph)
     : impl_(new Impl), m_(m), c_(c), o_(o), rank_(rank), world_(world) {
     c_.validate(m_);
     if (c_.n_tp != 1) throw SpecError("executor: tensor parallelism (n_tp > 1) is not supported");
@@ -247,7 +247,31 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
     pp_rank_ = rank % p_;
     dp_rank_ = rank / p_;
     pl_ = place_stages(m_, c_);
-    graph_ = build_tasks(m_, c_, pl_);
+    if (graph) {
+        // an externally built graph (e.g. the breadth-/depth-first gradient-accumulation graphs of
+        // build_accumulation_tasks, schedule.cpp:454-500) must match the placement of c
+        if (graph->n_devices != p_ || graph->compute_program.size() != static_cast<size_t>(p_))
+            throw SpecError("executor: graph has " + std::to_string(graph->n_devices) + " devices, config n_pp = " +
+                            std::to_string(p_));
+        i64 n_compute = 0;
+        for (const Task& t : graph->tasks) {
+            if (t.stage < 0 || t.stage >= pl_.n_stage)
+                throw SpecError("executor: graph stage " + std::to_string(t.stage) + " outside the config's " +
+                                std::to_string(pl_.n_stage) + " stages");
+            if (t.micro_batch >= c_.n_mb)
+                throw SpecError("executor: graph micro-batch outside the config's n_mb");
+            if ((t.kind == TaskKind::Reduce || t.kind == TaskKind::Reconstruct) && c_.n_dp < 2)
+                throw SpecError("executor: graph has data-parallel tasks but n_dp < 2");
+            if (t.kind == TaskKind::Reconstruct && c_.dp_variant != DpVariant::DP_FS)
+                throw SpecError("executor: graph reconstructs weights but the config is not DP_FS");
+            if (t.lane == Lane::Compute) ++n_compute;
+        }
+        if (n_compute != 2 * pl_.n_stage * c_.n_mb)
+            throw SpecError("executor: graph must hold one Fwd and one Bwd per (stage, micro-batch)");
+        graph_ = *graph;
+    } else {
+        graph_ = build_tasks(m_, c_, pl_);
+    }
     for (i64 s = 0; s < pl_.n_stage; ++s)
         layouts_.push_back(make_stage_layout(m_, s, pl_.n_stage, pl_.layers_per_stage, c_.n_dp));
 

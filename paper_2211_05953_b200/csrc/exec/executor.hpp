@@ -55,8 +55,10 @@ StageLayout make_stage_layout(const ModelSpec& m, i64 stage, i64 n_stage, i64 la
 
 class Executor {
 public:
+    // graph: run this task graph instead of build_tasks(m, c) (e.g. build_accumulation_tasks);
+    // c must describe its placement (n_pp, n_loop, n_mb, n_dp, dp_variant).
     Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOptions& o, int rank, int world,
-             const std::vector<ncclUniqueId>& uids);
+             const std::vector<ncclUniqueId>& uids, const TaskGraph* graph = nullptr);
     ~Executor();
 
     // tokens: [n_mb][s_mb][seq+1] int32 of this rank's DP replica (host or device pointer).

@@ -52,7 +52,11 @@ class Executor:
                  device: Optional[int] = None, uids: Optional[bytes] = None, record_timeline: bool = False,
                  seed: int = 1234, lr: float = 1e-4, beta1: float = 0.9, beta2: float = 0.95,
                  eps: float = 1e-8, weight_decay: float = 0.0, init_std: float = 0.02,
-                 skip_optimizer: bool = False, profile_kernels: bool = False):
+                 skip_optimizer: bool = False, profile_kernels: bool = False,
+                 graph: Optional[ps.TaskGraph] = None):
+        """graph: run this task graph (e.g. ``ps.build_accumulation_tasks``) instead of
+        ``build_tasks(model, config)``; ``config`` then describes its placement (see
+        ``accumulation_config``)."""
         if isinstance(model, GPTConfig):
             model = model_spec(model)
         self.model, self.config, self.rank, self.world = model, config, rank, world
@@ -62,8 +66,12 @@ class Executor:
                            (SKIP_OPTIMIZER if skip_optimizer else 0) | (PROFILE_KERNELS if profile_kernels else 0))
         h = C.c_void_p()
         ubuf = C.create_string_buffer(uids, len(uids)) if uids else None
-        _check(N.lib().bfpp_exec_create(C.byref(model._c()), C.byref(config._c()), C.byref(opts), rank, world,
-                                        ubuf, C.byref(h)))
+        if graph is None:
+            _check(N.lib().bfpp_exec_create(C.byref(model._c()), C.byref(config._c()), C.byref(opts), rank, world,
+                                            ubuf, C.byref(h)))
+        else:
+            _check(N.lib().bfpp_exec_create_graph(C.byref(model._c()), C.byref(config._c()), graph.handle,
+                                                  C.byref(opts), rank, world, ubuf, C.byref(h)))
         self._h = h
         g = C.c_void_p()
         _check(N.lib().bfpp_exec_graph(self._h, C.byref(g)))
@@ -187,6 +195,15 @@ def measured_timeline(graph: ps.TaskGraph, starts: Sequence[np.ndarray], ends: S
     if np.isnan(s).any():
         raise ps.SimError("measured timeline is missing tasks")
     return ps.Timeline.from_intervals(graph, list(s), list(e))
+
+
+def accumulation_config(model, dp_variant: ps.DpVariant, n_mb: int, n_dp: int) -> ps.ParallelConfig:
+    """Placement of ``build_accumulation_tasks`` graphs (schedule.cpp:454-500): one device, one layer
+    per stage (n_loop = n_layers), n_mb micro-batches, data parallel over n_dp ranks."""
+    if isinstance(model, GPTConfig):
+        model = model_spec(model)
+    return ps.ParallelConfig(n_dp=n_dp, n_pp=1, n_loop=model.n_layers, n_mb=n_mb, dp_variant=dp_variant,
+                             schedule=ps.Schedule.BreadthFirst)
 
 
 def execute_distributed(model, config: ps.ParallelConfig, **kw) -> Executor:

@@ -27,11 +27,29 @@ CASES = {
     "df_pp2x2_dp2_fs": dict(n_dp=2, n_pp=2, n_loop=2, n_mb=4, dp_variant="DP_FS", schedule="DepthFirst"),
     "bf_pp4x1_mb4": dict(n_dp=1, n_pp=4, n_loop=1, n_mb=4, dp_variant="DP0", schedule="BreadthFirst"),
     "1f1b_pp2_dp2_fs": dict(n_dp=2, n_pp=2, n_loop=1, n_mb=2, dp_variant="DP_FS", schedule="OneFOneB"),
+    # gradient-accumulation graphs (build_accumulation_tasks, schedule.cpp:454-500; PAPER App. C):
+    # one layer per stage, data parallel; breadth-first reduces per layer, depth-first per micro-batch
+    "acc_bf_dp2_fs_mb3": dict(n_dp=2, n_mb=3, dp_variant="DP_FS", accumulation="BreadthFirst"),
+    "acc_df_dp2_fs_mb2": dict(n_dp=2, n_mb=2, dp_variant="DP_FS", accumulation="DepthFirst"),
+    "acc_bf_dp2_dp0_mb2": dict(n_dp=2, n_mb=2, dp_variant="DP0", accumulation="BreadthFirst"),
 }
+
+
+def accumulation_graph(name):
+    """The gradient-accumulation task graph of an accumulation case (None for build_tasks cases)."""
+    c = CASES[name]
+    if "accumulation" not in c:
+        return None
+    from paper_2211_05953_b200.executor import model_spec
+    return ps.build_accumulation_tasks(model_spec(H.TINY), ps.DpVariant[c["dp_variant"]],
+                                       ps.AccumulationOrder[c["accumulation"]], c["n_mb"])
 
 
 def config_of(name):
     c = dict(CASES[name])
+    if "accumulation" in c:
+        from paper_2211_05953_b200.executor import accumulation_config
+        return accumulation_config(H.TINY, ps.DpVariant[c["dp_variant"]], c["n_mb"], c["n_dp"])
     c["dp_variant"] = ps.DpVariant[c["dp_variant"]]
     c["schedule"] = ps.Schedule[c["schedule"]]
     return ps.ParallelConfig(**c)
@@ -58,7 +76,8 @@ def main():
     def factory(**kw):
         obj = [comm_ids(config) if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        return Executor(cfg, config, rank=rank, world=world, device=local, uids=obj[0], **kw)
+        return Executor(cfg, config, rank=rank, world=world, device=local, uids=obj[0],
+                        graph=accumulation_graph(a.case), **kw)
 
     res = H.run_rank(factory, cfg, config, params, tokens, rank)
     with open(os.path.join(a.out, f"rank{rank}.pkl"), "wb") as f:

@@ -36,7 +36,19 @@ CASES = {
     "1f1b_pp4_dp1": (4, 1, 1, 6, V.DP0, S.OneFOneB),
     "df_pp4x2_dp1": (4, 1, 2, 8, V.DP0, S.DepthFirst),
     "np_pp1_dp2_ps": (1, 2, 1, 3, V.DP_PS, S.NoPipeline),
+    # gradient-accumulation graphs (build_accumulation_tasks; the schedule field is the order)
+    "acc_bf_dp2_fs": (1, 2, None, 3, V.DP_FS, ps.AccumulationOrder.BreadthFirst),
+    "acc_df_dp2_fs": (1, 2, None, 2, V.DP_FS, ps.AccumulationOrder.DepthFirst),
 }
+
+
+def _case_graph(name):
+    n_pp, n_dp, loops, n_mb, variant, sched = CASES[name]
+    if loops is None:  # accumulation: one layer per stage
+        model = _model(1, 4)
+        return ps.build_accumulation_tasks(model, variant, sched, n_mb)
+    cfg = ps.ParallelConfig(n_dp=n_dp, n_pp=n_pp, n_loop=loops, n_mb=n_mb, dp_variant=variant, schedule=sched)
+    return ps.build_tasks(_model(n_pp, loops), cfg)
 
 
 def _free_port():
@@ -118,8 +130,9 @@ def _worker(rank, world, port, name, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         n_pp, n_dp, loops, n_mb, variant, sched = CASES[name]
-        cfg = ps.ParallelConfig(n_dp=n_dp, n_pp=n_pp, n_loop=loops, n_mb=n_mb, dp_variant=variant, schedule=sched)
-        graph = ps.build_tasks(_model(n_pp, loops), cfg)
+        graph = _case_graph(name)
+        cfg = ps.ParallelConfig(n_dp=n_dp, n_pp=n_pp, n_loop=loops or 8, n_mb=n_mb, dp_variant=variant,
+                                schedule=ps.Schedule.BreadthFirst if loops is None else sched)
         ids = [comm_ids(cfg) if rank == 0 else None]      # NCCL unique ids, as execute_distributed
         dist.broadcast_object_list(ids, src=0)
         plan = plan_rank(graph, rank % n_pp, n_dp)
@@ -164,9 +177,8 @@ def test_multirank_plan_emulation(name):
 
 
 def _local_plans(name):
-    n_pp, n_dp, loops, n_mb, variant, sched = CASES[name]
-    cfg = ps.ParallelConfig(n_dp=n_dp, n_pp=n_pp, n_loop=loops, n_mb=n_mb, dp_variant=variant, schedule=sched)
-    graph = ps.build_tasks(_model(n_pp, loops), cfg)
+    n_pp, n_dp = CASES[name][:2]
+    graph = _case_graph(name)
     return graph, {r: plan_rank(graph, r % n_pp, n_dp) for r in range(n_pp * n_dp)}, n_pp, n_dp
 
 
