@@ -138,8 +138,30 @@ __global__ void __launch_bounds__(256) xent_kernel(__nv_bfloat16* __restrict__ l
 // (~32 registers, no shared memory), so up to four fit on an SM beside a resident GEMM CTA
 // (96 regs x 320 threads) and retire within microseconds: the block scheduler keeps placing the
 // high-priority compute stream's CTAs while Adam on the low-priority DP stream streams HBM under
-// the tensor-core work. Streaming loads/stores (.cs) keep the optimizer's 30 B/param out of the
-// GEMM operands' L2 working set.
+// the tensor-core work.
+
+// Optimizer streams: L1 bypass + an L2 evict-first policy (measured 6.1 TB/s for Adam alone vs
+// 5.4 TB/s with .cs hints and 5.6 TB/s with default caching; scripts/overlap_bench.py).
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ float4 ld4_stream(const float4* p, uint64_t pol) {
+    float4 v;
+    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void st4_stream(float4* p, float4 v, uint64_t pol) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;"
+                 :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st2_stream(uint2* p, uint2 v, uint64_t pol) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.u32 [%0], {%1,%2}, %3;"
+                 :: "l"(p), "r"(v.x), "r"(v.y), "l"(pol) : "memory");
+}
+
 constexpr int kAdamThreads = 256;
 __global__ void __launch_bounds__(kAdamThreads) adam_kernel(float* __restrict__ p, float* __restrict__ m,
                                                             float* __restrict__ v, float* __restrict__ g,
@@ -147,12 +169,13 @@ __global__ void __launch_bounds__(kAdamThreads) adam_kernel(float* __restrict__ 
                                                             float b1, float b2, float eps, float wd, float bc1,
                                                             float bc2, int zero_grad) {
     const int64_t n4 = n / 4;
+    const uint64_t pol = evict_first_policy();
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * kAdamThreads + threadIdx.x; i < n4;
          i += static_cast<int64_t>(gridDim.x) * kAdamThreads) {
-        float4 P = __ldcs(reinterpret_cast<const float4*>(p) + i);
-        float4 M = __ldcs(reinterpret_cast<const float4*>(m) + i);
-        float4 Vv = __ldcs(reinterpret_cast<const float4*>(v) + i);
-        const float4 G = __ldcs(reinterpret_cast<const float4*>(g) + i);
+        float4 P = ld4_stream(reinterpret_cast<const float4*>(p) + i, pol);
+        float4 M = ld4_stream(reinterpret_cast<const float4*>(m) + i, pol);
+        float4 Vv = ld4_stream(reinterpret_cast<const float4*>(v) + i, pol);
+        const float4 G = ld4_stream(reinterpret_cast<const float4*>(g) + i, pol);
         float* pp = &P.x;
         float* mm = &M.x;
         float* vv = &Vv.x;
@@ -163,15 +186,15 @@ __global__ void __launch_bounds__(kAdamThreads) adam_kernel(float* __restrict__ 
             vv[k] = b2 * vv[k] + (1.f - b2) * gg[k] * gg[k];
             pp[k] -= lr * ((mm[k] / bc1) / (sqrtf(vv[k] / bc2) + eps) + wd * pp[k]);
         }
-        __stcs(reinterpret_cast<float4*>(p) + i, P);
-        __stcs(reinterpret_cast<float4*>(m) + i, M);
-        __stcs(reinterpret_cast<float4*>(v) + i, Vv);
-        if (zero_grad) __stcs(reinterpret_cast<float4*>(g) + i, make_float4(0.f, 0.f, 0.f, 0.f));
+        st4_stream(reinterpret_cast<float4*>(p) + i, P, pol);
+        st4_stream(reinterpret_cast<float4*>(m) + i, M, pol);
+        st4_stream(reinterpret_cast<float4*>(v) + i, Vv, pol);
+        if (zero_grad) st4_stream(reinterpret_cast<float4*>(g) + i, make_float4(0.f, 0.f, 0.f, 0.f), pol);
         __nv_bfloat162 lo = __floats2bfloat162_rn(P.x, P.y), hi = __floats2bfloat162_rn(P.z, P.w);
         uint2 o;
         o.x = *reinterpret_cast<uint32_t*>(&lo);
         o.y = *reinterpret_cast<uint32_t*>(&hi);
-        __stcs(reinterpret_cast<uint2*>(w16) + i, o);
+        st2_stream(reinterpret_cast<uint2*>(w16) + i, o, pol);
     }
     // scalar tail (n % 4 elements) on the last block
     const int64_t t = n4 * 4 + threadIdx.x;
@@ -251,7 +274,6 @@ void adam_update(float* p, float* m, float* v, float* g, void* w16, int64_t n, f
     }();
     (void)once;
     (void)blocks_per_sm;  // kept for the ABI; every call uses short-lived blocks (see adam_kernel)
-    // grid covers the tensor (persistent grids measured slower and delay GEMM CTAs more)
     const int64_t blocks = (n / 4 + kAdamThreads - 1) / kAdamThreads;
     adam_kernel<<<static_cast<unsigned>(blocks > 0 ? blocks : 1), kAdamThreads, 0, st>>>(
         p, m, v, g, static_cast<__nv_bfloat16*>(w16), n, lr, b1, b2, eps, wd, bc1, bc2, zero_grad);
