@@ -615,7 +615,15 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
         CK(cudaMemcpy2DAsync(I.inputs, w, tokens, pitch, w, rows, k, cs));
         CK(cudaMemcpy2DAsync(I.labels, w, tokens + 1, pitch, w, rows, k, cs));
     }
-    if (o_.record_timeline) CK(cudaEventRecord(I.origin, cs));
+    if (o_.record_timeline) {
+        // A common time origin for the ranks' timelines: every compute stream passes a 1-float
+        // all-reduce on the world communicator before recording its origin (residual skew = the
+        // all-reduce's completion skew, microseconds), and this rank's other streams start after it.
+        if (I.world_comm)
+            NK(ncclAllReduce(I.loss_dev + 2, I.loss_dev + 2, 1, ncclFloat32, ncclSum, I.world_comm, cs));
+        CK(cudaEventRecord(I.origin, cs));
+        for (int s = 1; s < S_N; ++s) CK(cudaStreamWaitEvent(I.st[s], I.origin, 0));
+    }
     const float grad_scale = 1.f / static_cast<float>(c_.n_dp * c_.n_mb * T);
     const bool fs = c_.n_dp >= 2 && c_.dp_variant == DpVariant::DP_FS;
 
