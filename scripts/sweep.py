@@ -31,10 +31,11 @@ def main():
         for beta in a.betas:
             for sched in a.schedules:
                 port += 1
+                loops = a.loops if sched in ("breadth_first", "depth_first") else 1  # GPipe / 1F1B: no loops
                 cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
                        "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(ROOT, "bench.py"),
                        "--gpus", str(a.gpus), "--model", a.model, "--schedule", sched, "--pp", str(a.pp),
-                       "--loops", str(a.loops), "--beta", str(beta), "--dp-variant", a.dp_variant,
+                       "--loops", str(loops), "--beta", str(beta), "--dp-variant", a.dp_variant,
                        "--steps", str(a.steps), "--warmup", str(a.warmup), "--no-e2e", "--no-cpu-baseline"]
                 if a.gpus == 1:
                     cmd = cmd[:1] + cmd[cmd.index(os.path.join(ROOT, "bench.py")):]
