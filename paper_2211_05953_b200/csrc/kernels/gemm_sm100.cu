@@ -236,6 +236,9 @@ __global__ void __maxnreg__(96)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // PDL: everything above overlapped the previous kernel's tail; inputs/outputs are touched below
+    ptx::griddep_wait();
+    ptx::griddep_launch_dependents();
 
     if (warp == 0) {
         if (lane == 0) {
@@ -419,6 +422,9 @@ __global__ void __maxnreg__(96)
     ptx::cluster_sync();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // PDL: everything above overlapped the previous kernel's tail; inputs/outputs are touched below
+    ptx::griddep_wait();
+    ptx::griddep_launch_dependents();
 
     if (warp == 0) {
         if (lane == 0) {
@@ -565,8 +571,18 @@ void launch(const GemmArgs& g, cudaStream_t st) {
     }
     const int tiles = static_cast<int>(((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN));
     const int grid = tiles < num_sms() ? tiles : num_sms();
-    kern<<<grid, kThreads, Smem<BN>::kBytes, st>>>(ta, tb, td, static_cast<int>(g.M), static_cast<int>(g.N),
-                                                   static_cast<int>(g.K), ep);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = Smem<BN>::kBytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = gemm_pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, ta, tb, td, static_cast<int>(g.M), static_cast<int>(g.N), static_cast<int>(g.K),
+                       ep);
 }
 
 template <int BN, int A_MN, int B_MN>
@@ -591,13 +607,15 @@ void launch2(const GemmArgs& g, cudaStream_t st) {
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = Smem2<BN>::kBytes;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (see griddep_wait)
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = gemm_pdl ? 2 : 1;
     cudaLaunchKernelEx(&cfg, kern, ta, tb, td, static_cast<int>(g.M), static_cast<int>(g.N), static_cast<int>(g.K),
                        ep);
 }
@@ -605,6 +623,7 @@ void launch2(const GemmArgs& g, cudaStream_t st) {
 }  // namespace
 
 int gemm_mode = -1;  // -1 auto, 1 force 1-CTA, 2 force 2-CTA (benchmarks / tests)
+int gemm_pdl = 1;    // programmatic dependent launch (BFPP_GEMM_PDL=0 disables; A/B measurements)
 int gemm_bn2 = 0;    // 2-CTA pair-tile width: 0 / 256 default, 128 opt-in (BFPP_GEMM_BN2; tests)
 
 static bool env_read = false;
@@ -619,6 +638,7 @@ void gemm_bf16(const GemmArgs& g, cudaStream_t st) {
     if (!env_read) {
         if (const char* e = getenv("BFPP_GEMM_MODE")) gemm_mode = atoi(e);
         if (const char* e = getenv("BFPP_GEMM_BN2")) gemm_bn2 = atoi(e);
+        if (const char* e = getenv("BFPP_GEMM_PDL")) gemm_pdl = atoi(e);
         env_read = true;
     }
     if (g.M <= 0 || g.N <= 0 || g.K <= 0) throw std::runtime_error("gemm: empty problem");

@@ -397,6 +397,195 @@ bool ln_dispatch(int width, F&& f) {
     return false;
 }
 
+
+// ---- wide rows (2048 < width <= 8192): W warps per row, 8 chunks of 8 elements per lane each,
+// R = 8 / W rows per block; the row statistics are combined through shared memory.
+template <int W>
+struct MwShape {
+    static constexpr int R = W == 3 ? 2 : 8 / W;  // rows per block
+    static constexpr int kThreads = 32 * W * R;
+};
+
+template <int W>
+__global__ void __launch_bounds__(MwShape<W>::kThreads) ln_fwd_mw_kernel(
+    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ gamma,
+    const __nv_bfloat16* __restrict__ beta, __nv_bfloat16* __restrict__ y, float* __restrict__ mean_out,
+    float* __restrict__ rstd_out, int rows, int width, float eps) {
+    constexpr int R = MwShape<W>::R;
+    __shared__ float red[R][W];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int part = warp % W, ri = warp / W;
+    const int row = blockIdx.x * R + ri;
+    const bool valid = row < rows;
+    const __nv_bfloat16* xr = x + static_cast<int64_t>(valid ? row : 0) * width;
+    uint4 raw[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int c = ((part * 8 + k) * 32 + lane) * 8;
+        raw[k] = (valid && c < width) ? *reinterpret_cast<const uint4*>(xr + c) : make_uint4(0, 0, 0, 0);
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        float v[8];
+        unpack8(raw[k], v);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s += v[u];
+    }
+    s = warp_sum(s);
+    if (lane == 0) red[ri][part] = s;
+    __syncthreads();
+    float tot = 0.f;
+#pragma unroll
+    for (int w = 0; w < W; ++w) tot += red[ri][w];
+    const float mean = tot / width;
+    __syncthreads();
+    float q = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        if (((part * 8 + k) * 32 + lane) * 8 >= width) continue;
+        float v[8];
+        unpack8(raw[k], v);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) q += (v[u] - mean) * (v[u] - mean);
+    }
+    q = warp_sum(q);
+    if (lane == 0) red[ri][part] = q;
+    __syncthreads();
+    float qt = 0.f;
+#pragma unroll
+    for (int w = 0; w < W; ++w) qt += red[ri][w];
+    const float rstd = rsqrtf(qt / width + eps);
+    if (!valid) return;
+    __nv_bfloat16* yr = y + static_cast<int64_t>(row) * width;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int c = ((part * 8 + k) * 32 + lane) * 8;
+        if (c >= width) continue;
+        float v[8], g[8], b[8];
+        unpack8(raw[k], v);
+        load8(gamma + c, g);
+        load8(beta + c, b);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = (v[u] - mean) * rstd * g[u] + b[u];
+        store8(yr + c, v);
+    }
+    if (lane == 0 && part == 0) {
+        mean_out[row] = mean;
+        rstd_out[row] = rstd;
+    }
+}
+
+template <int W>
+__global__ void __launch_bounds__(MwShape<W>::kThreads, 1) ln_bwd_mw_kernel(
+    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ gamma,
+    const float* __restrict__ mean, const float* __restrict__ rstd, const __nv_bfloat16* __restrict__ dres,
+    __nv_bfloat16* __restrict__ dx, float* __restrict__ ws, int rows, int width) {
+    constexpr int R = MwShape<W>::R;
+    __shared__ float st[R][W][2];
+    __shared__ __align__(16) float red[W * R][2][256];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int part = warp % W, ri = warp / W;
+    const int row = blockIdx.x * R + ri;
+    const bool valid = row < rows;
+    const int64_t off = static_cast<int64_t>(valid ? row : 0) * width;
+    uint4 rx[8], rd[8], rg[8], rr[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int c = ((part * 8 + k) * 32 + lane) * 8;
+        const bool in = valid && c < width;
+        rx[k] = in ? *reinterpret_cast<const uint4*>(x + off + c) : make_uint4(0, 0, 0, 0);
+        rd[k] = in ? *reinterpret_cast<const uint4*>(dy + off + c) : make_uint4(0, 0, 0, 0);
+        rg[k] = c < width ? *reinterpret_cast<const uint4*>(gamma + c) : make_uint4(0, 0, 0, 0);
+        rr[k] = (dres && in) ? *reinterpret_cast<const uint4*>(dres + off + c) : make_uint4(0, 0, 0, 0);
+    }
+    const float mu = valid ? mean[row] : 0.f, rs = valid ? rstd[row] : 0.f;
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        float xv[8], dv[8], g[8];
+        unpack8(rx[k], xv);
+        unpack8(rd[k], dv);
+        unpack8(rg[k], g);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const float gd = dv[u] * g[u];
+            s1 += gd;
+            s2 += gd * (xv[u] - mu) * rs;
+        }
+    }
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    if (lane == 0) {
+        st[ri][part][0] = s1;
+        st[ri][part][1] = s2;
+    }
+    __syncthreads();
+    float t1 = 0.f, t2 = 0.f;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        t1 += st[ri][w][0];
+        t2 += st[ri][w][1];
+    }
+    const float m1 = t1 / width, m2 = t2 / width;
+    if (valid) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int c = ((part * 8 + k) * 32 + lane) * 8;
+            if (c >= width) continue;
+            float xv[8], dv[8], g[8], r[8], rv[8];
+            unpack8(rx[k], xv);
+            unpack8(rd[k], dv);
+            unpack8(rg[k], g);
+            unpack8(rr[k], rv);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) r[u] = rs * (dv[u] * g[u] - m1 - (xv[u] - mu) * rs * m2) + rv[u];
+            store8(dx + off + c, r);
+        }
+    }
+    // column partials over the block's R rows: round k covers chunk (w * 8 + k) of every part w
+    float* wout = ws + static_cast<int64_t>(blockIdx.x) * 2 * width;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        float xv[8], dv[8];
+        unpack8(rx[k], xv);
+        unpack8(rd[k], dv);
+        float4* pg = reinterpret_cast<float4*>(&red[warp][0][lane * 8]);
+        float4* pb = reinterpret_cast<float4*>(&red[warp][1][lane * 8]);
+        pg[0] = make_float4(dv[0] * (xv[0] - mu) * rs, dv[1] * (xv[1] - mu) * rs, dv[2] * (xv[2] - mu) * rs,
+                            dv[3] * (xv[3] - mu) * rs);
+        pg[1] = make_float4(dv[4] * (xv[4] - mu) * rs, dv[5] * (xv[5] - mu) * rs, dv[6] * (xv[6] - mu) * rs,
+                            dv[7] * (xv[7] - mu) * rs);
+        pb[0] = make_float4(dv[0], dv[1], dv[2], dv[3]);
+        pb[1] = make_float4(dv[4], dv[5], dv[6], dv[7]);
+        __syncthreads();
+        for (int i = threadIdx.x; i < W * 256; i += MwShape<W>::kThreads) {
+            const int w = i / 256, t = i % 256;
+            const int col = (w * 8 + k) * 256 + t;
+            if (col < width) {
+                float tg = 0.f, tb = 0.f;
+#pragma unroll
+                for (int r2 = 0; r2 < R; ++r2) {
+                    tg += red[r2 * W + w][0][t];
+                    tb += red[r2 * W + w][1][t];
+                }
+                wout[col] = tg;
+                wout[width + col] = tb;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+template <typename F>
+bool ln_dispatch_wide(int width, F&& f) {
+    if (width <= 2048) return false;
+    if (width <= 4096) { f(std::integral_constant<int, 2>{}); return true; }
+    if (width <= 6144) { f(std::integral_constant<int, 3>{}); return true; }
+    if (width <= 8192) { f(std::integral_constant<int, 4>{}); return true; }
+    return false;
+}
+
 float* ln_workspace(size_t bytes) {
     // one workspace per device (the executor runs every LayerNorm backward on one stream)
     static thread_local float* ws[64] = {};
@@ -416,6 +605,14 @@ float* ln_workspace(size_t bytes) {
 void layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, float* mean, float* rstd, int rows,
                    int width, float eps, cudaStream_t st) {
     if (width % 8) throw std::runtime_error("layernorm: width must be a multiple of 8");
+    const bool wide = ln_dispatch_wide(width, [&](auto w) {
+        constexpr int W = decltype(w)::value;
+        using Sh = MwShape<W>;
+        ln_fwd_mw_kernel<W><<<(rows + Sh::R - 1) / Sh::R, Sh::kThreads, 0, st>>>(
+            static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(gamma),
+            static_cast<const __nv_bfloat16*>(beta), static_cast<__nv_bfloat16*>(y), mean, rstd, rows, width, eps);
+    });
+    if (wide) return;
     const bool done = ln_dispatch<24>(width, [&](auto nch) {
         ln_fwd_reg_kernel<decltype(nch)::value><<<(rows + 7) / 8, 256, 0, st>>>(
             static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(gamma),
@@ -434,6 +631,20 @@ void layernorm_bwd(const void* dy, const void* x, const void* gamma, const float
     if (width % 8) throw std::runtime_error("layernorm: width must be a multiple of 8");
     auto DY = static_cast<const __nv_bfloat16*>(dy);
     auto X = static_cast<const __nv_bfloat16*>(x);
+    {
+        int parts = 0;
+        const bool wide = ln_dispatch_wide(width, [&](auto w) {
+            constexpr int W = decltype(w)::value;
+            using Sh = MwShape<W>;
+            parts = (rows + Sh::R - 1) / Sh::R;
+            float* part = ln_workspace(static_cast<size_t>(parts) * 2 * width * sizeof(float));
+            ln_bwd_mw_kernel<W><<<parts, Sh::kThreads, 0, st>>>(
+                DY, X, static_cast<const __nv_bfloat16*>(gamma), mean, rstd, static_cast<const __nv_bfloat16*>(dres),
+                static_cast<__nv_bfloat16*>(dx), part, rows, width);
+            ln_partsum_kernel<<<(2 * width + 63) / 64, 256, 0, st>>>(part, parts, width, dgamma, dbeta, accumulate);
+        });
+        if (wide) return;
+    }
     const int blocks = (rows + 7) / 8;
     {
         float* part = ln_workspace(static_cast<size_t>(blocks) * 2 * width * sizeof(float));

@@ -254,5 +254,13 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(uint32_t M, uint32_t N, ui
            | ((M >> 4) << 24);  // m_dim
 }
 
+// Programmatic dependent launch: wait for the preceding grid of the stream (no-op when the
+// kernel was not launched with programmatic stream serialization), and let the next grid be
+// scheduled (its own prologue then overlaps this grid's tail).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 }  // namespace ptx
 }  // namespace bfpp
