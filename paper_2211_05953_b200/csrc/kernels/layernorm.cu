@@ -398,7 +398,7 @@ bool ln_dispatch(int width, F&& f) {
 }
 
 
-// ---- wide rows (2048 < width <= 8192): W warps per row, 8 chunks of 8 elements per lane each,
+// ---- wide rows (2048 < width <= 4096): W warps per row, 8 chunks of 8 elements per lane each,
 // R = 8 / W rows per block; the row statistics are combined through shared memory.
 template <int W>
 struct MwShape {
@@ -581,8 +581,8 @@ template <typename F>
 bool ln_dispatch_wide(int width, F&& f) {
     if (width <= 2048) return false;
     if (width <= 4096) { f(std::integral_constant<int, 2>{}); return true; }
-    if (width <= 6144) { f(std::integral_constant<int, 3>{}); return true; }
-    if (width <= 8192) { f(std::integral_constant<int, 4>{}); return true; }
+    // W = 3 measured slower than the two-pass kernels at width 5120 (scripts/ln_bench.py); wider
+    // rows keep the generic path
     return false;
 }
 
