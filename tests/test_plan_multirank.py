@@ -32,6 +32,7 @@ CASES = {
     "bf_pp2_dp1": (2, 1, 2, 4, V.DP_FS, S.BreadthFirst),
     "df_pp2_dp1": (2, 1, 2, 4, V.DP0, S.DepthFirst),
     "bf_pp2x2_dp2_fs": (2, 2, 2, 4, V.DP_FS, S.BreadthFirst),   # BASELINE configs[0] layout
+    "bf_pp2x4_dp4_fs": (2, 4, 4, 2, V.DP_FS, S.BreadthFirst),   # bench.py layout at N = 8 (world 8)
     "gpipe_pp2_dp2_fs": (2, 2, 1, 2, V.DP_FS, S.GPipe),
     "1f1b_pp4_dp1": (4, 1, 1, 6, V.DP0, S.OneFOneB),
     "df_pp4x2_dp1": (4, 1, 2, 8, V.DP0, S.DepthFirst),
