@@ -623,7 +623,7 @@ void launch2(const GemmArgs& g, cudaStream_t st) {
 }  // namespace
 
 int gemm_mode = -1;  // -1 auto, 1 force 1-CTA, 2 force 2-CTA (benchmarks / tests)
-int gemm_pdl = 1;    // programmatic dependent launch (BFPP_GEMM_PDL=0 disables; A/B measurements)
+int gemm_pdl = 0;    // programmatic dependent launch (BFPP_GEMM_PDL=1): measured no gain in-step (optimizer co-running)
 int gemm_bn2 = 0;    // 2-CTA pair-tile width: 0 / 256 default, 128 opt-in (BFPP_GEMM_BN2; tests)
 
 static bool env_read = false;
