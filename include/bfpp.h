@@ -149,9 +149,10 @@ typedef struct bfpp_gemm_args {
 /* D[M,N] = sum_k A[m,k] B[n,k] on tcgen05 (TMA + TMEM), bf16 in, f32 accumulate */
 int bfpp_gemm_bf16(const bfpp_gemm_args* args, void* stream);
 /* GEMM variant selection for benchmarks and tests (process-wide): mode -1 auto, 1 one-CTA
- * 128-row tiles, 2 two-CTA 256-row tiles; bn2 = pair-tile width (0 default = 256,
- * 128 or 256). Defaults come from BFPP_GEMM_MODE / BFPP_GEMM_BN2. */
-int bfpp_gemm_config(int32_t mode, int32_t bn2);
+ * 128-row tiles, 2 two-CTA 256-row tiles; bn2 = pair-tile width (0 default = 256, 128 opt-in);
+ * stream_k = 0 off (default), 1 forced, -1 auto (only when the last tile wave leaves pairs idle).
+ * Defaults come from BFPP_GEMM_MODE / BFPP_GEMM_BN2 / BFPP_GEMM_SK. */
+int bfpp_gemm_config(int32_t mode, int32_t bn2, int32_t stream_k);
 
 /* causal multi-head attention, head_dim 128 (flash-style; never materialises T x T).
  * qkv [B*S][3*H*128] bf16 (Q | K | V column blocks), o [B*S][H*128] bf16,

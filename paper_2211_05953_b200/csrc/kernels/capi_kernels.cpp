@@ -20,11 +20,12 @@ void check_launch() {
 
 extern "C" {
 
-int bfpp_gemm_config(int32_t mode, int32_t bn2) {
+int bfpp_gemm_config(int32_t mode, int32_t bn2, int32_t stream_k) {
     return guarded([&] {
         if (mode != -1 && mode != 1 && mode != 2) throw SpecError("gemm_config: mode must be -1, 1 or 2");
         if (bn2 != 0 && bn2 != 128 && bn2 != 256) throw SpecError("gemm_config: bn2 must be 0, 128 or 256");
-        bfpp::gemm_bf16_configure(mode, bn2);
+        if (stream_k < -1 || stream_k > 1) throw SpecError("gemm_config: stream_k must be -1, 0 or 1");
+        bfpp::gemm_bf16_configure(mode, bn2, stream_k);
     });
 }
 

@@ -35,9 +35,10 @@ struct GemmArgs {
 
 void gemm_bf16(const GemmArgs& g, cudaStream_t stream);
 extern int gemm_mode;  // -1 auto (2-CTA tiles when M, N >= 256), 1 force 1-CTA, 2 force 2-CTA
-void gemm_bf16_configure(int mode, int bn2);  // overrides the environment defaults
+void gemm_bf16_configure(int mode, int bn2, int stream_k);  // overrides the environment defaults
 extern int gemm_bn2;   // 2-CTA pair-tile width: 0 default (256), 128 opt-in
 extern int gemm_pdl;   // programmatic dependent launch of the GEMM kernels (default 0, BFPP_GEMM_PDL=1)
+extern int gemm_sk;    // stream-K in the 2-CTA kernel: -1 auto, 0 off, 1 forced (BFPP_GEMM_SK)
 
 // 2-D TMA descriptor over a row-major [rows][ld] matrix (bf16, or f32 if `f32`) with `inner`
 // valid columns; box = {128 bytes of the inner dimension, box_rows}, SWIZZLE_128B, OOB -> 0.

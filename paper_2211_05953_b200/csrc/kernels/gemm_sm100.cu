@@ -20,6 +20,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <map>
 #include <stdexcept>
 #include <string>
 
@@ -89,6 +90,62 @@ struct EpiArgs {
     int accumulate;
 };
 
+// Stream-K (2-CTA kernel; opt-in, BFPP_GEMM_SK=1 / bfpp_gemm_config): correct and tested, but
+// measured 15-90 % slower than data-parallel tiles on the step's shapes (scripts/gemm_sk_check.py):
+// the owner's partial reads/writes are latency-bound at the very end of every pair's range.
+// The (tile, k-block) iteration space is split into one contiguous
+// range per CTA pair, so every pair does the same number of MMA k-blocks (no partially filled
+// last wave). A tile whose k-blocks straddle ranges is finished by the pair holding its last
+// k-block (the "owner"); the other pairs ("producers") write their f32 partial accumulators to
+// a workspace slot and publish a flag. Each pair walks its range backwards, so its producer
+// segment (the end of its range) is published first and its owner segment (the start) is
+// drained last: an owner never waits on a pair that is itself still waiting.
+struct SkArgs {
+    float* ws;    // [pair][cta][128][256] f32 partials (nullptr: data-parallel tiles)
+    int* flags;   // [pair][cta] epoch of the last published partial
+    int epoch;
+};
+
+struct Seg {
+    int tile, kb0, kb1;
+};
+
+struct WorkIter {
+    bool sk;
+    int t, step, num_tiles, nk;  // data-parallel: tiles t, t + step, ...
+    long long u0, u;             // stream-K: this pair's range [u0, u1), walked down from u1
+    __device__ WorkIter(bool sk_, int pair, int n_pairs, int num_tiles_, int nk_)
+        : sk(sk_), t(pair), step(n_pairs), num_tiles(num_tiles_), nk(nk_) {
+        const long long total = static_cast<long long>(num_tiles_) * nk_;
+        u0 = total * pair / n_pairs;
+        u = total * (pair + 1) / n_pairs;
+    }
+    __device__ bool next(Seg& g) {
+        if (!sk) {
+            if (t >= num_tiles) return false;
+            g = {t, 0, nk};
+            t += step;
+            return true;
+        }
+        if (u <= u0) return false;
+        const int tile = static_cast<int>((u - 1) / nk);
+        const long long ts = static_cast<long long>(tile) * nk;
+        const long long lo = u0 > ts ? u0 : ts;
+        g = {tile, static_cast<int>(lo - ts), static_cast<int>(u - ts)};
+        u = lo;
+        return true;
+    }
+};
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 template <int BN>
 struct Smem {
     static constexpr int kABytes = BM * BK * 2;
@@ -122,14 +179,37 @@ __device__ __forceinline__ void load_row32_bf16(const __nv_bfloat16* p, int vali
 // swizzled staging row at `rowa`. Works in 32-column halves so the epilogue stays within the
 // kernel's 104-register budget (which leaves room on the SM for another stream's block).
 // `release` runs right after this warp's last TMEM read of the tile when `last` is set.
+// n_parts stream-K partials (f32 rows, already offset to this strip's first column) are added
+// to the accumulator before the fused op.
+__device__ __forceinline__ void add_part(float (&v)[32], const float* part) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 4) {
+        const float4 w = __ldcg(reinterpret_cast<const float4*>(part + j));
+        v[j] += w.x;
+        v[j + 1] += w.y;
+        v[j + 2] += w.z;
+        v[j + 3] += w.w;
+    }
+}
+
 template <typename Release>
 __device__ __forceinline__ void epilogue_strip(const EpiArgs& ep, uint32_t tcol, int row, int col0, int valid_all,
-                                               uint32_t rowa, int lane, bool last, Release release) {
+                                               uint32_t rowa, int lane, bool last, Release release,
+                                               const float* part0, const float* part1) {
     if (ep.epi == GEMM_EPI_F32) {
         uint32_t r[32];
         ptx::tmem_ld_32x32b_x32(tcol, r);
         ptx::tmem_ld_wait();
         if (last) release();
+        if (part0) {
+            float v[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+            add_part(v, part0);
+            if (part1) add_part(v, part1);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(v[j]);
+        }
 #pragma unroll
         for (int c = 0; c < 8; ++c)
             ptx::st_shared_v4(rowa + ((c ^ (lane & 7)) << 4), r[4 * c], r[4 * c + 1], r[4 * c + 2], r[4 * c + 3]);
@@ -157,6 +237,10 @@ __device__ __forceinline__ void epilogue_strip(const EpiArgs& ep, uint32_t tcol,
             if (h == 1 && last) release();
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        }
+        if (part0) {
+            add_part(v, part0 + 32 * h);
+            if (part1) add_part(v, part1 + 32 * h);
         }
         if (ep.epi == GEMM_EPI_RESID) {
 #pragma unroll
@@ -341,7 +425,7 @@ __global__ void __maxnreg__(96)
                     ptx::tc_fence_before();
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
-                });
+                }, nullptr, nullptr);
                 ptx::fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0 && col0 < N && m0 + q * 32 < M) {
@@ -381,9 +465,10 @@ struct Smem2 {
 };
 
 template <int BN, int A_MN, int B_MN>
-__global__ void __maxnreg__(96)
+// 112 registers x 320 threads still leaves room for two 48-register optimizer blocks
+__global__ void __maxnreg__(112)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                 const __grid_constant__ CUtensorMap tmD, int M, int N, int K, EpiArgs ep) {
+                 const __grid_constant__ CUtensorMap tmD, int M, int N, int K, EpiArgs ep, SkArgs sk) {
     using S = Smem2<BN>;
     constexpr int kStages2 = S::kStages;
     extern __shared__ uint8_t smem_raw[];
@@ -402,6 +487,7 @@ __global__ void __maxnreg__(96)
     const int n_tiles = (N + BN - 1) / BN;
     const int num_tiles = m_tiles * n_tiles;
     const int nk = (K + BK - 1) / BK;
+    const bool use_sk = BN == 256 && sk.ws != nullptr;  // stream-K only for the 256-wide pair tiles
 
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch(&tmA);
@@ -431,9 +517,12 @@ __global__ void __maxnreg__(96)
             // ===== TMA producer (both CTAs): own 128 rows of A and own 128-row half of B =====
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = pair; t < num_tiles; t += n_pairs) {
+            WorkIter wi(use_sk, pair, n_pairs, num_tiles, nk);
+            Seg g;
+            while (wi.next(g)) {
+                const int t = g.tile;
                 const int m0 = (t % m_tiles) * 256 + 128 * rank, n0 = (t / m_tiles) * BN + (BN / 2) * rank;
-                for (int kb = 0; kb < nk; ++kb) {
+                for (int kb = g.kb0; kb < g.kb1; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* sa = smem + stage * S::kStageBytes;
                     uint8_t* sb = sa + S::kABytes;
@@ -467,13 +556,15 @@ __global__ void __maxnreg__(96)
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
-            for (int t = pair; t < num_tiles; t += n_pairs, ++it) {
+            WorkIter wi(use_sk, pair, n_pairs, num_tiles, nk);
+            Seg g;
+            for (; wi.next(g); ++it) {
                 const int acc = it & 1;
                 const uint32_t acc_phase = (it >> 1) & 1;
                 ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
-                for (int kb = 0; kb < nk; ++kb) {
+                for (int kb = g.kb0; kb < g.kb1; ++kb) {
                     ptx::mbar_wait(&full[stage], phase);
                     ptx::tc_fence_after();
                     const uint32_t sa = ptx::smem_u32(smem + stage * S::kStageBytes);
@@ -484,7 +575,7 @@ __global__ void __maxnreg__(96)
                                                  : ptx::sdesc_sw128(sa + k * 32, 16, 1024);
                         const uint64_t bd = B_MN ? ptx::sdesc_sw128(sb + k * 2048, 64 * BK * 2, 1024)
                                                  : ptx::sdesc_sw128(sb + k * 32, 16, 1024);
-                        ptx::umma_f16_2sm(d_tmem, ad, bd, idesc, (kb | k) != 0);
+                        ptx::umma_f16_2sm(d_tmem, ad, bd, idesc, (kb != g.kb0) || k != 0);
                     }
                     ptx::umma_commit_2sm(&empty[stage], 0x3);
                     if (++stage == kStages2) {
@@ -505,7 +596,11 @@ __global__ void __maxnreg__(96)
         const int cw = f32_out ? 32 : 64;  // tile columns per 128-byte strip
         const int n_strips = BN / cw;
         int it = 0;
-        for (int t = pair; t < num_tiles; t += n_pairs, ++it) {
+        const int lr = q * 32 + lane;  // this thread's accumulator row within the CTA's 128 rows
+        WorkIter wi(use_sk, pair, n_pairs, num_tiles, nk);
+        Seg g;
+        for (; wi.next(g); ++it) {
+            const int t = g.tile;
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
             const int m0 = (t % m_tiles) * 256 + 128 * rank, n0 = (t / m_tiles) * BN;
@@ -513,6 +608,48 @@ __global__ void __maxnreg__(96)
             const bool row_ok = row < M;
             ptx::mbar_wait(&tfull[acc], acc_phase);
             ptx::tc_fence_after();
+            auto release = [&] {
+                // this warp's last TMEM read of the segment: hand the accumulator back to the MMA warp
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tempty[acc]), 0));
+            };
+            if (g.kb1 < nk) {
+                // ---- stream-K producer: f32 partial to this pair's workspace slot, then publish ----
+                float* dst = sk.ws + ((static_cast<size_t>(pair) * 2 + rank) * 128 + lr) * 256;
+                for (int sidx = half; sidx < BN / 32; sidx += 2) {
+                    uint32_t r[32];
+                    ptx::tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + acc * BN + sidx * 32, r);
+                    ptx::tmem_ld_wait();
+                    if (sidx + 2 >= BN / 32) release();
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4)
+                        __stcg(reinterpret_cast<float4*>(dst + sidx * 32 + j),
+                               make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                           __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])));
+                }
+                __threadfence();
+                asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+                if (ew == 0 && lane == 0) st_release_gpu(sk.flags + pair * 2 + rank, sk.epoch);
+                continue;
+            }
+            // ---- full tile, or stream-K owner: add the partials of the pairs before this one ----
+            const float* part0 = nullptr;
+            const float* part1 = nullptr;
+            if (g.kb0 > 0) {
+                // producers: pair - 1, and pair - 2 when pair - 1's range starts inside this tile
+                const long long total = static_cast<long long>(num_tiles) * nk, ts = static_cast<long long>(t) * nk;
+                const int q1 = pair - 1;
+                while (ld_acquire_gpu(sk.flags + q1 * 2 + rank) != sk.epoch) {
+                }
+                part0 = sk.ws + ((static_cast<size_t>(q1) * 2 + rank) * 128 + lr) * 256;
+                if (total * q1 / n_pairs > ts) {
+                    const int q2 = pair - 2;
+                    while (ld_acquire_gpu(sk.flags + q2 * 2 + rank) != sk.epoch) {
+                    }
+                    part1 = sk.ws + ((static_cast<size_t>(q2) * 2 + rank) * 128 + lr) * 256;
+                }
+            }
             for (int sidx = half; sidx < n_strips; sidx += 2) {
                 const int col0 = n0 + sidx * cw;
                 const uint32_t tcol = tmem_base + ((q * 32) << 16) + acc * BN + sidx * cw;
@@ -521,12 +658,8 @@ __global__ void __maxnreg__(96)
                 if (lane == 0) ptx::bulk_wait_read<0>();
                 __syncwarp();
                 const uint32_t rowa = ptx::smem_u32(stage_out) + lane * 128;
-                epilogue_strip(ep, tcol, row, col0, valid, rowa, lane, sidx + 2 >= n_strips, [&] {
-                    // this warp's last TMEM read of the tile: hand the accumulator back to the MMA warp
-                    ptx::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tempty[acc]), 0));
-                });
+                epilogue_strip(ep, tcol, row, col0, valid, rowa, lane, sidx + 2 >= n_strips, release,
+                               part0 ? part0 + sidx * cw : nullptr, part1 ? part1 + sidx * cw : nullptr);
                 ptx::fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0 && col0 < N && m0 + q * 32 < M) {
@@ -585,6 +718,27 @@ void launch(const GemmArgs& g, cudaStream_t st) {
                        ep);
 }
 
+// Stream-K partial workspace, one per stream (GEMMs of one stream run in order; two streams
+// never share a slot): [pairs][2 CTAs][128][256] f32 + [pairs][2] int flags, epochs per launch.
+struct SkWorkspace {
+    float* ws = nullptr;
+    int* flags = nullptr;
+    int epoch = 0;
+};
+SkWorkspace& sk_workspace(cudaStream_t st, int pairs) {
+    static std::map<std::pair<int, cudaStream_t>, SkWorkspace> all;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    SkWorkspace& w = all[{dev, st}];
+    if (!w.ws) {
+        if (cudaMalloc(&w.ws, static_cast<size_t>(pairs) * 2 * 128 * 256 * sizeof(float)) != cudaSuccess ||
+            cudaMalloc(&w.flags, static_cast<size_t>(pairs) * 2 * sizeof(int)) != cudaSuccess)
+            throw std::runtime_error("gemm: stream-K workspace allocation failed");
+        cudaMemset(w.flags, 0, static_cast<size_t>(pairs) * 2 * sizeof(int));
+    }
+    return w;
+}
+
 template <int BN, int A_MN, int B_MN>
 void launch2(const GemmArgs& g, cudaStream_t st) {
     CUtensorMap ta = A_MN ? make_tma_2d(g.A, g.M, g.K, g.lda, BK, false) : make_tma_2d(g.A, g.K, g.M, g.lda, 128, false);
@@ -601,7 +755,23 @@ void launch2(const GemmArgs& g, cudaStream_t st) {
         configured = true;
     }
     const int tiles = static_cast<int>(((g.M + 255) / 256) * ((g.N + BN - 1) / BN));
-    const int pairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
+    const int nk = static_cast<int>((g.K + BK - 1) / BK);
+    int pairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
+    SkArgs sk{nullptr, nullptr, 0};
+    {
+        // stream-K when the data-parallel tile waves leave pairs idle and every pair's range is at
+        // least half a tile (so a tile has at most two producers)
+        const int all = num_sms() / 2;
+        const long long total = static_cast<long long>(tiles) * nk;
+        const int waves = (tiles + all - 1) / all;
+        const double eff = static_cast<double>(tiles) / (static_cast<double>(waves) * all);
+        const bool want = gemm_sk == 1 || (gemm_sk < 0 && eff < 0.92);
+        if (want && BN == 256 && total / all >= (nk + 1) / 2 && nk >= 2) {
+            SkWorkspace& w = sk_workspace(st, all);
+            sk = SkArgs{w.ws, w.flags, ++w.epoch};
+            pairs = all;
+        }
+    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * pairs);
     cfg.blockDim = dim3(kThreads);
@@ -617,21 +787,23 @@ void launch2(const GemmArgs& g, cudaStream_t st) {
     cfg.attrs = attr;
     cfg.numAttrs = gemm_pdl ? 2 : 1;
     cudaLaunchKernelEx(&cfg, kern, ta, tb, td, static_cast<int>(g.M), static_cast<int>(g.N), static_cast<int>(g.K),
-                       ep);
+                       ep, sk);
 }
 
 }  // namespace
 
+int gemm_sk = 0;     // stream-K for the 2-CTA kernel: 0 off (default), 1 forced, -1 auto (BFPP_GEMM_SK)
 int gemm_mode = -1;  // -1 auto, 1 force 1-CTA, 2 force 2-CTA (benchmarks / tests)
 int gemm_pdl = 0;    // programmatic dependent launch (BFPP_GEMM_PDL=1): measured no gain in-step (optimizer co-running)
 int gemm_bn2 = 0;    // 2-CTA pair-tile width: 0 / 256 default, 128 opt-in (BFPP_GEMM_BN2; tests)
 
 static bool env_read = false;
 
-void gemm_bf16_configure(int mode, int bn2) {
+void gemm_bf16_configure(int mode, int bn2, int stream_k) {
     env_read = true;
     gemm_mode = mode;
     gemm_bn2 = bn2;
+    gemm_sk = stream_k;
 }
 
 void gemm_bf16(const GemmArgs& g, cudaStream_t st) {
@@ -639,6 +811,7 @@ void gemm_bf16(const GemmArgs& g, cudaStream_t st) {
         if (const char* e = getenv("BFPP_GEMM_MODE")) gemm_mode = atoi(e);
         if (const char* e = getenv("BFPP_GEMM_BN2")) gemm_bn2 = atoi(e);
         if (const char* e = getenv("BFPP_GEMM_PDL")) gemm_pdl = atoi(e);
+        if (const char* e = getenv("BFPP_GEMM_SK")) gemm_sk = atoi(e);
         env_read = true;
     }
     if (g.M <= 0 || g.N <= 0 || g.K <= 0) throw std::runtime_error("gemm: empty problem");

@@ -52,10 +52,10 @@ def gemm(a: torch.Tensor, b: torch.Tensor, *, a_mn_major=False, b_mn_major=False
     return out
 
 
-def gemm_config(mode: int = -1, bn2: int = 0):
+def gemm_config(mode: int = -1, bn2: int = 0, stream_k: int = -1):
     """Process-wide GEMM variant selection (tests / benchmarks): mode -1 auto, 1 one-CTA, 2 two-CTA;
-    bn2 = two-CTA tile width (0 auto, 128, 256)."""
-    _check(_nat.lib().bfpp_gemm_config(mode, bn2))
+    bn2 = two-CTA tile width (0 default 256, 128); stream_k -1 auto, 0 off, 1 forced."""
+    _check(_nat.lib().bfpp_gemm_config(mode, bn2, stream_k))
 
 
 def attention_fwd(qkv, batch, seq, heads, head_dim=128):

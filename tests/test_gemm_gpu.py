@@ -20,22 +20,24 @@ def _close(got, ref, rtol):
     assert err <= rtol * scale, (err, scale)
 
 
-# (mode, bn2): auto; one-CTA tiles; two-CTA 256x128 and 256x256 pair tiles (forced)
-VARIANTS = [(-1, 0), (1, 0), (2, 128), (2, 256)]
+# (mode, bn2, stream_k): auto; one-CTA tiles; two-CTA 256x128 and 256x256 pair tiles (forced),
+# data-parallel and stream-K (forced: a k-split wherever every pair gets >= half a tile)
+VARIANTS = [(-1, 0, -1), (1, 0, 0), (2, 128, 0), (2, 256, 0), (2, 256, 1)]
 
 
-@pytest.fixture(params=VARIANTS, ids=lambda v: f"mode{v[0]}-bn{v[1]}")
+@pytest.fixture(params=VARIANTS, ids=lambda v: f"mode{v[0]}-bn{v[1]}-sk{v[2]}")
 def variant(request, cuda_device):
     ops = _ops()
     ops.gemm_config(*request.param)
     yield request.param
-    ops.gemm_config(-1, 0)
+    ops.gemm_config(-1, 0, -1)
 
 
 @pytest.mark.parametrize("a_mn", [False, True])
 @pytest.mark.parametrize("b_mn", [False, True])
 @pytest.mark.parametrize("shape", [(256, 512, 128), (128, 256, 64), (384, 768, 320), (64, 1000, 128),
-                                   (2048, 2048, 2048), (200, 136, 72), (512, 8192, 256)])
+                                   (2048, 2048, 2048), (200, 136, 72), (512, 8192, 256), (2048, 8192, 2048),
+                                   (768, 1280, 4096)])
 def test_gemm_layouts(variant, a_mn, b_mn, shape):
     ops = _ops()
     M, N, K = shape
