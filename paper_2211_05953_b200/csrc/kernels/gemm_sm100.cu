@@ -464,9 +464,8 @@ struct Smem2 {
     static constexpr int kBytes = kBarOffset + 256 + 1024;
 };
 
-template <int BN, int A_MN, int B_MN>
-// 112 registers x 320 threads still leaves room for two 48-register optimizer blocks
-__global__ void __maxnreg__(112)
+template <int BN, int A_MN, int B_MN, bool SK>
+__global__ void __maxnreg__(96)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmD, int M, int N, int K, EpiArgs ep, SkArgs sk) {
     using S = Smem2<BN>;
@@ -487,7 +486,7 @@ __global__ void __maxnreg__(112)
     const int n_tiles = (N + BN - 1) / BN;
     const int num_tiles = m_tiles * n_tiles;
     const int nk = (K + BK - 1) / BK;
-    const bool use_sk = BN == 256 && sk.ws != nullptr;  // stream-K only for the 256-wide pair tiles
+    const bool use_sk = SK && BN == 256 && sk.ws != nullptr;  // stream-K instantiation only
 
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch(&tmA);
@@ -748,10 +747,12 @@ void launch2(const GemmArgs& g, cudaStream_t st) {
     CUtensorMap td = make_tma_2d(g.D, g.N, g.M, g.ldd, 32, f32);
     EpiArgs ep{static_cast<const __nv_bfloat16*>(g.aux), g.ldaux, static_cast<__nv_bfloat16*>(g.aux_out),
                g.ldaux_out, g.epilogue, g.accumulate};
-    auto kern = gemm2_kernel<BN, A_MN, B_MN>;
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem2<BN>::kBytes);
+        cudaFuncSetAttribute(gemm2_kernel<BN, A_MN, B_MN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Smem2<BN>::kBytes);
+        cudaFuncSetAttribute(gemm2_kernel<BN, A_MN, B_MN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Smem2<BN>::kBytes);
         configured = true;
     }
     const int tiles = static_cast<int>(((g.M + 255) / 256) * ((g.N + BN - 1) / BN));
@@ -786,8 +787,12 @@ void launch2(const GemmArgs& g, cudaStream_t st) {
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = gemm_pdl ? 2 : 1;
-    cudaLaunchKernelEx(&cfg, kern, ta, tb, td, static_cast<int>(g.M), static_cast<int>(g.N), static_cast<int>(g.K),
-                       ep, sk);
+    if (sk.ws)
+        cudaLaunchKernelEx(&cfg, gemm2_kernel<BN, A_MN, B_MN, true>, ta, tb, td, static_cast<int>(g.M),
+                           static_cast<int>(g.N), static_cast<int>(g.K), ep, sk);
+    else
+        cudaLaunchKernelEx(&cfg, gemm2_kernel<BN, A_MN, B_MN, false>, ta, tb, td, static_cast<int>(g.M),
+                           static_cast<int>(g.N), static_cast<int>(g.K), ep, sk);
 }
 
 }  // namespace
