@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbfpp.so")
+LIB_PATH = os.environ.get("BFPP_LIB_PATH", os.path.join(_HERE, "libbfpp.so"))  # override: A/B runs
 
 
 class ModelSpecC(C.Structure):

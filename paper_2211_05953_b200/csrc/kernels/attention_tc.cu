@@ -422,6 +422,17 @@ __global__ void __launch_bounds__(192, 1)
         const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
         const int tid = threadIdx.x - 64;
         const uint32_t sp_base = ptx::smem_u32(sm + BwdSmem::kP), sds_base = ptx::smem_u32(sm + BwdSmem::kS);
+        const int64_t stat_base = (static_cast<int64_t>(b) * H + head) * S;
+        // LSE / delta of the next query block are loaded one iteration ahead (their global-load
+        // latency was exposed at the top of every iteration)
+        float nxt_l = 0.f, nxt_d = 0.f;
+        {
+            const int q = i0 * BQ + tid;
+            if (q < S) {
+                nxt_l = lse[stat_base + q];
+                nxt_d = delta[stat_base + q];
+            }
+        }
         for (int i = i0; i < n_qb; ++i) {
             const int it = i - i0;
             const int q0 = i * BQ;
@@ -429,10 +440,12 @@ __global__ void __launch_bounds__(192, 1)
             // slower warp is still reading (nobody gets two ahead past the barrier below)
             const uint32_t L = s_lse + (it & 1) * 512;
             const uint32_t Dl = s_del + (it & 1) * 512;
-            {
-                const int q = q0 + tid;
-                ptx::st_shared_f32(L + 4 * tid, q < S ? lse[(static_cast<int64_t>(b) * H + head) * S + q] : 0.f);
-                ptx::st_shared_f32(Dl + 4 * tid, q < S ? delta[(static_cast<int64_t>(b) * H + head) * S + q] : 0.f);
+            ptx::st_shared_f32(L + 4 * tid, nxt_l);
+            ptx::st_shared_f32(Dl + 4 * tid, nxt_d);
+            if (i + 1 < n_qb) {
+                const int q = q0 + BQ + tid;
+                nxt_l = q < S ? lse[stat_base + q] : 0.f;
+                nxt_d = q < S ? delta[stat_base + q] : 0.f;
             }
             named_bar_sync(1, 128);
             ptx::mbar_wait(s_full, it & 1);

@@ -254,6 +254,10 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(uint32_t M, uint32_t N, ui
            | ((M >> 4) << 24);  // m_dim
 }
 
+__device__ __forceinline__ void ld_shared_v4(uint32_t addr, uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d) {
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "r"(addr));
+}
+
 // Programmatic dependent launch: wait for the preceding grid of the stream (no-op when the
 // kernel was not launched with programmatic stream serialization), and let the next grid be
 // scheduled (its own prologue then overlaps this grid's tail).
