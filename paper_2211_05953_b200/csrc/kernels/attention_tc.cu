@@ -298,7 +298,7 @@ void attention_fwd_tc(const void* qkv, void* o, float* lse, int batch, int seq, 
 //   warps 2..5  thread = key row: P^T = exp2(S^T*scale_log2 - lse), dS^T = P^T (dP^T - delta),
 //               both to shared memory as bf16 (K-major over q); then drain dQ_i (thread = q row)
 //               with red.global.add.v4.f32; finally write dK, dV.
-// TMEM columns: [0,128) S^T / dQ, [128,256) dP^T, [256,384) dV, [384,512) dK.
+// TMEM columns: [0,128) S^T, [128,256) dP^T / dQ, [256,384) dV, [384,512) dK.
 namespace {
 
 struct BwdSmem {
@@ -392,14 +392,18 @@ __global__ void __launch_bounds__(192, 1)
             ptx::mbar_wait(kv_full, 0);
             for (int i = i0; i < n_qb; ++i) {
                 const int it = i - i0;
+                // S^T_i right away (the tensor pipe runs it while dQ_{i-1} drains); dP^T_i into the
+                // dQ_{i-1} columns once those are drained
                 ptx::mbar_wait(qo_full, it & 1);
+                ptx::tc_fence_after();
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk)
+                    ptx::umma_f16(t_s, kmajor_desc(sk, kk), kmajor_desc(sq, kk), id_kk, kk != 0);
                 if (it > 0) ptx::mbar_wait(dq_empty, (it - 1) & 1);
                 ptx::tc_fence_after();
 #pragma unroll
-                for (int kk = 0; kk < D / 16; ++kk) {
-                    ptx::umma_f16(t_s, kmajor_desc(sk, kk), kmajor_desc(sq, kk), id_kk, kk != 0);
+                for (int kk = 0; kk < D / 16; ++kk)
                     ptx::umma_f16(t_dp, kmajor_desc(sv, kk), kmajor_desc(so, kk), id_kk, kk != 0);
-                }
                 ptx::umma_commit(s_full);
                 ptx::mbar_wait(p_full, it & 1);
                 ptx::tc_fence_after();
@@ -409,9 +413,10 @@ __global__ void __launch_bounds__(192, 1)
                     ptx::umma_f16(t_dk, kmajor_desc(sds, kk), mnmajor_desc(sq, kk), id_kn, (it | kk) != 0);
                 }
                 ptx::umma_commit(qo_empty);
+                // dQ_i into the dP^T columns (consumed once p_full fired)
 #pragma unroll
                 for (int kk = 0; kk < BKV / 16; ++kk)
-                    ptx::umma_f16(t_s, mnmajor_desc(sds, kk), mnmajor_desc(sk, kk), id_nn, kk != 0);
+                    ptx::umma_f16(t_dp, mnmajor_desc(sds, kk), mnmajor_desc(sk, kk), id_nn, kk != 0);
                 ptx::umma_commit(dq_full);
             }
         }
@@ -494,7 +499,7 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll 1
             for (int c = 0; c < 4; ++c) {
                 uint32_t rq[32];
-                ptx::tmem_ld_32x32b_x32(t_s + lane_off + c * 32, rq);
+                ptx::tmem_ld_32x32b_x32(t_dp + lane_off + c * 32, rq);
                 ptx::tmem_ld_wait();
                 if (q < S) {
 #pragma unroll
