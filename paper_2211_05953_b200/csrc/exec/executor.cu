@@ -663,7 +663,7 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
     };
     auto LNB = [&](cudaStream_t st, const bf16* dy, const bf16* x, const bf16* g, const float* mu, const float* rs,
                    const bf16* dres, bf16* dx, float* dg, float* db, int acc) {
-        K(K_LAYERNORM, (dres ? 6 : 5) * Th2, 3, st, [&] {
+        K(K_LAYERNORM, (dres ? 6 : 5) * Th2, layernorm_bwd_launches(static_cast<int>(h)), st, [&] {
             layernorm_bwd(dy, x, g, mu, rs, dres, dx, dg, db, static_cast<int>(T), static_cast<int>(h), st, acc);
         });
     };

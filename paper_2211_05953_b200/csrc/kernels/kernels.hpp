@@ -23,6 +23,8 @@ void layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, 
 void layernorm_bwd(const void* dy, const void* x, const void* gamma, const float* mean, const float* rstd,
                    const void* dres, void* dx, float* dgamma, float* dbeta, int rows, int width, cudaStream_t st,
                    int accumulate = 1);
+// kernel launches of one layernorm_bwd call at this width (register-resident paths: 2; generic: 3)
+int layernorm_bwd_launches(int width);
 
 // elementwise.cu
 void embed_fwd(const int32_t* tok, const void* wte, const void* wpe, void* x, int T, int S, int h, cudaStream_t st);
