@@ -230,6 +230,11 @@ def main():
     tokens_per_step = n_mb * args.s_mb * dp * cfg.s_seq
     value = tokens_per_step / (ms * 1e-3)
     loss_val = float(loss_dev.item())
+    if world > 1:  # the loss lives on each replica's last-stage rank: mean over the DP replicas
+        last = rank % pp == (pp * loops - 1) % pp
+        t = torch.tensor([loss_val if last else 0.0], dtype=torch.float64)
+        dist.all_reduce(t)
+        loss_val = float(t.item()) / dp
 
     # ---- end-to-end through the public API: pinned host tokens in, loss out, every step ----
     _progress('e2e start')
