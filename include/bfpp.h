@@ -241,13 +241,15 @@ int64_t bfpp_exec_local_stage(const bfpp_exec* e, int64_t c);
 int64_t bfpp_exec_stage_numel(const bfpp_exec* e, int64_t stage);
 int64_t bfpp_exec_device_bytes(const bfpp_exec* e);
 /* Parameter I/O in the stage's flat layout. set_params takes the full stage
- * vector on every DP rank; get_params / get_grads write this rank's [lo, hi) range of the
- * f32 master weights / reduced gradients into a full-size buffer. */
+ * vector on every DP rank; get_params / get_grads write the f32 master weights / reduced
+ * gradients this rank holds into a full-size buffer, NaN where another DP rank owns the element
+ * (sharded variants own a 1/n_dp slice of every layer segment); [lo, hi) = [0, numel). */
 int bfpp_exec_set_params(bfpp_exec* e, int64_t stage, const float* host, int64_t n);
 int bfpp_exec_get_params(bfpp_exec* e, int64_t stage, float* host, int64_t n, int64_t* lo, int64_t* hi);
 int bfpp_exec_get_grads(bfpp_exec* e, int64_t stage, float* host, int64_t n, int64_t* lo, int64_t* hi);
 int bfpp_exec_zero_grads(bfpp_exec* e);
-/* bf16 compute weights (resident copy, or this rank's all-gather source shard under DP_FS) */
+/* bf16 compute weights (resident copy, or this rank's all-gather source slices under DP_FS;
+ * bf16 NaN 0x7FC0 where another rank owns the element) */
 int bfpp_exec_get_weights16(bfpp_exec* e, int64_t stage, uint16_t* host, int64_t n, int64_t* lo, int64_t* hi);
 /* measured [start, end] (seconds from the step origin) of this rank's tasks in the last
  * step; tasks of other devices are NaN. Arrays have bfpp_graph_n_tasks entries. */

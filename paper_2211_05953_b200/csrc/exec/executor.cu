@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <limits>
 #include <map>
 #include <set>
 #include <stdexcept>
@@ -164,7 +165,16 @@ struct StageActs {
 
 struct LocalStage {
     i64 stage = 0;
-    int64_t shard_n = 0, shard_lo = 0;
+    int64_t shard_n = 0;
+    // Sharded variants (n_dp >= 2, DP_FS / DP_PS): the stage vector is cut into segments (the
+    // embeddings, each layer, the head) and every segment is sharded across the DP ranks, so a
+    // rank's optimizer shard is the concatenation of its 1/n_dp slice of every segment. One
+    // segment's gradients can then be reduce-scattered (and its weights all-gathered) on their
+    // own, as soon as that layer's backward is done. seg = boundaries in the stage vector;
+    // segment s of rank r = [seg[s] + r * len_s / n_dp, + len_s / n_dp) -> shard offset seg[s] / n_dp.
+    std::vector<int64_t> seg;
+    std::vector<char> seg_done;  // segments already reduced (and updated) in the current step
+    int64_t nd = 1, r = 0;       // shard degree and this rank's slice (1, 0 when not sharded)
     bf16* w16 = nullptr;      // resident compute weights (not DP_FS with n_dp >= 2)
     float* grad = nullptr;    // full f32 gradient (accumulated across micro-batches)
     float *master = nullptr, *m = nullptr, *v = nullptr;  // f32 optimizer shard
@@ -172,6 +182,49 @@ struct LocalStage {
     float* gtmp = nullptr;    // reduce-scatter landing buffer when a stage reduces several times
     bf16* w16_shard = nullptr;
 };
+
+// Segment boundaries of a stage for per-segment sharding: embeddings | each layer | head, when
+// every segment splits into n_dp slices of whole 8-element groups; otherwise the whole stage.
+std::vector<int64_t> shard_segments(const StageLayout& L, i64 n_dp) {
+    std::vector<int64_t> b{0};
+    for (const LayerParams& P : L.layers)
+        if (P.ln1_g > b.back()) b.push_back(P.ln1_g);
+    if (L.last && L.lnf_g > b.back()) b.push_back(L.lnf_g);
+    b.push_back(L.padded);
+    for (size_t i = 0; i + 1 < b.size(); ++i)
+        if ((b[i + 1] - b[i]) % (8 * n_dp) != 0) return {0, L.padded};
+    return b;
+}
+
+// f(full-vector offset, length, shard offset) for each slice this rank owns
+template <class F>
+void for_each_chunk(const LocalStage& ls, F&& f) {
+    for (size_t s = 0; s + 1 < ls.seg.size(); ++s) {
+        const int64_t len = (ls.seg[s + 1] - ls.seg[s]) / ls.nd;
+        f(ls.seg[s] + ls.r * len, len, ls.seg[s] / ls.nd);
+    }
+}
+
+// bf16 weights of segments [s0, s1): every rank's slices -> the full vector dst (all ranks)
+void all_gather_segments(const LocalStage& ls, bf16* dst, size_t s0, size_t s1, ncclComm_t comm, cudaStream_t st) {
+    NK(ncclGroupStart());
+    for (size_t s = s0; s < s1; ++s) {
+        const size_t n = static_cast<size_t>((ls.seg[s + 1] - ls.seg[s]) / ls.nd);
+        NK(ncclAllGather(ls.w16_shard + ls.seg[s] / ls.nd, dst + ls.seg[s], n, ncclBfloat16, comm, st));
+    }
+    NK(ncclGroupEnd());
+}
+
+// f32 gradients of segments [s0, s1): summed over the ranks, this rank's slices -> dst (shard layout)
+void reduce_scatter_segments(const LocalStage& ls, float* dst, size_t s0, size_t s1, ncclComm_t comm,
+                             cudaStream_t st) {
+    NK(ncclGroupStart());
+    for (size_t s = s0; s < s1; ++s) {
+        const size_t n = static_cast<size_t>((ls.seg[s + 1] - ls.seg[s]) / ls.nd);
+        NK(ncclReduceScatter(ls.grad + ls.seg[s], dst + ls.seg[s] / ls.nd, n, ncclFloat32, ncclSum, comm, st));
+    }
+    NK(ncclGroupEnd());
+}
 
 using TaskExec = PlanTask;
 
@@ -318,7 +371,10 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
         max_padded = std::max(max_padded, L.padded);
         const bool sharded = c_.n_dp >= 2 && c_.dp_variant != DpVariant::DP0;
         ls.shard_n = sharded ? L.padded / c_.n_dp : L.padded;
-        ls.shard_lo = sharded ? dp_rank_ * ls.shard_n : 0;
+        ls.seg = sharded ? shard_segments(L, c_.n_dp) : std::vector<int64_t>{0, L.padded};
+        ls.seg_done.assign(ls.seg.size() - 1, 0);
+        ls.nd = sharded ? c_.n_dp : 1;
+        ls.r = sharded ? dp_rank_ : 0;
         if (!fs) ls.w16 = I.alloc<bf16>(static_cast<size_t>(L.padded), &total);
         ls.grad = I.alloc<float>(static_cast<size_t>(L.padded), &total);
         CK(cudaMemset(ls.grad, 0, static_cast<size_t>(L.padded) * 4));
@@ -342,17 +398,17 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
         int64_t gbase = 0;  // global element offset of this stage (model order, split-independent)
         for (i64 s = 0; s < ls.stage; ++s) gbase += layouts_[static_cast<size_t>(s)].numel;
         CK(cudaMemset(ls.master, 0, static_cast<size_t>(ls.shard_n) * 4));
-        for (const Segment& sg : init_segments(L, m_, o.init_std)) {
-            const int64_t lo = std::max(sg.off, ls.shard_lo), hi = std::min(sg.off + sg.n, ls.shard_lo + ls.shard_n);
-            if (lo >= hi) continue;
-            init_normal(ls.master + (lo - ls.shard_lo), nullptr, hi - lo, sg.mean, sg.std, o.seed,
-                        static_cast<uint64_t>(gbase + lo), I.st[S_COMPUTE]);
-        }
+        for (const Segment& sg : init_segments(L, m_, o.init_std))
+            for_each_chunk(ls, [&](int64_t off, int64_t n, int64_t soff) {
+                const int64_t lo = std::max(sg.off, off), hi = std::min(sg.off + sg.n, off + n);
+                if (lo >= hi) return;
+                init_normal(ls.master + soff + (lo - off), nullptr, hi - lo, sg.mean, sg.std, o.seed,
+                            static_cast<uint64_t>(gbase + lo), I.st[S_COMPUTE]);
+            });
         if (ls.w16_shard) f32_to_bf16(ls.master, ls.w16_shard, ls.shard_n, I.st[S_COMPUTE]);
         if (ls.w16) {
             if (ls.w16_shard)  // DP_PS: replicated weights assembled from the optimizer shards
-                NK(ncclAllGather(ls.w16_shard, ls.w16, static_cast<size_t>(ls.shard_n), ncclBfloat16, I.dp_comm,
-                                 I.st[S_COMPUTE]));
+                all_gather_segments(ls, ls.w16, 0, ls.seg.size() - 1, I.dp_comm, I.st[S_COMPUTE]);
             else
                 f32_to_bf16(ls.master, ls.w16, ls.shard_n, I.st[S_COMPUTE]);
         }
@@ -684,7 +740,7 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
                         o_.eps, o_.weight_decay, I.step_no, 0, st, tail ? 8 : 1);
         });
         if (sharded && c_.dp_variant == DpVariant::DP_PS)
-            NK(ncclAllGather(ls.w16_shard, ls.w16, static_cast<size_t>(ls.shard_n), ncclBfloat16, I.dp_comm, st));
+            all_gather_segments(ls, ls.w16, 0, ls.seg.size() - 1, I.dp_comm, st);
     };
     // n_dp == 1: a parameter segment's gradient is final as soon as the stage's last backward
     // has produced it, so the optimizer runs segment by segment (a layer at a time) on the DP
@@ -858,8 +914,7 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
         }
         case TaskKind::Reconstruct: {
             LocalStage& ls = I.local[static_cast<size_t>(t.stage / p_)];
-            NK(ncclAllGather(ls.w16_shard, I.slots[te.slot], static_cast<size_t>(ls.shard_n), ncclBfloat16, I.dp_comm,
-                             st));
+            all_gather_segments(ls, I.slots[te.slot], 0, ls.seg.size() - 1, I.dp_comm, st);
             break;
         }
         case TaskKind::Reduce: {
@@ -869,8 +924,7 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
                 NK(ncclAllReduce(ls.grad, ls.grad, static_cast<size_t>(full), ncclFloat32, ncclSum, I.dp_comm, st));
             } else {
                 float* dst = te.first_unit ? ls.gshard : ls.gtmp;
-                NK(ncclReduceScatter(ls.grad, dst, static_cast<size_t>(ls.shard_n), ncclFloat32, ncclSum, I.dp_comm,
-                                     st));
+                reduce_scatter_segments(ls, dst, 0, ls.seg.size() - 1, I.dp_comm, st);
                 if (!te.first_unit)
                     K(K_MISC, 12.0 * ls.shard_n, 1, st, [&] { add_f32_kernel<<<296, 256, 0, st>>>(ls.gshard, ls.gtmp, ls.shard_n); });
                 // no re-zeroing: the next unit's first backward overwrites the gradient buffer
@@ -962,6 +1016,20 @@ void Executor::timeline(double* start, double* end) const {
 }
 
 namespace {
+// this rank's slices of a device shard -> host[0, numel) (NaN where another rank owns the element)
+void scatter_shard(const LocalStage& ls, const StageLayout& L, const float* dev, float* host, int64_t* lo,
+                   int64_t* hi) {
+    std::vector<float> sh(static_cast<size_t>(ls.shard_n));
+    CK(cudaMemcpy(sh.data(), dev, static_cast<size_t>(ls.shard_n) * 4, cudaMemcpyDeviceToHost));
+    std::fill(host, host + L.numel, std::numeric_limits<float>::quiet_NaN());
+    for_each_chunk(ls, [&](int64_t off, int64_t len, int64_t soff) {
+        const int64_t m = std::max<int64_t>(0, std::min(len, L.numel - off));
+        if (m > 0) std::memcpy(host + off, sh.data() + soff, static_cast<size_t>(m) * 4);
+    });
+    *lo = 0;
+    *hi = L.numel;
+}
+
 LocalStage& find_local(std::vector<LocalStage>& v, i64 stage) {
     for (auto& ls : v)
         if (ls.stage == stage) return ls;
@@ -982,8 +1050,11 @@ void Executor::set_params(i64 stage, const float* host, int64_t n) {
     if (n != L.numel) throw SpecError("set_params: size mismatch with the stage layout");
     std::vector<float> padded(static_cast<size_t>(L.padded), 0.f);
     std::memcpy(padded.data(), host, static_cast<size_t>(n) * 4);
-    CK(cudaMemcpyAsync(ls.master, padded.data() + ls.shard_lo, static_cast<size_t>(ls.shard_n) * 4,
-                       cudaMemcpyHostToDevice, cs));
+    std::vector<float> shard(static_cast<size_t>(ls.shard_n));
+    for_each_chunk(ls, [&](int64_t off, int64_t len, int64_t soff) {
+        std::memcpy(shard.data() + soff, padded.data() + off, static_cast<size_t>(len) * 4);
+    });
+    CK(cudaMemcpyAsync(ls.master, shard.data(), static_cast<size_t>(ls.shard_n) * 4, cudaMemcpyHostToDevice, cs));
     CK(cudaMemsetAsync(ls.m, 0, static_cast<size_t>(ls.shard_n) * 4, cs));
     CK(cudaMemsetAsync(ls.v, 0, static_cast<size_t>(ls.shard_n) * 4, cs));
     if (ls.w16_shard) f32_to_bf16(ls.master, ls.w16_shard, ls.shard_n, cs);
@@ -1008,11 +1079,8 @@ void Executor::get_params(i64 stage, float* host, int64_t n, int64_t* lo, int64_
     CK(cudaDeviceSynchronize());
     LocalStage& ls = find_local(I.local, stage);
     const StageLayout& L = layouts_[static_cast<size_t>(stage)];
-    const int64_t a = ls.shard_lo, b = std::min(ls.shard_lo + ls.shard_n, L.numel);
     if (n < L.numel) throw SpecError("get_params: buffer too small");
-    if (b > a) CK(cudaMemcpy(host + a, ls.master, static_cast<size_t>(b - a) * 4, cudaMemcpyDeviceToHost));
-    *lo = a;
-    *hi = std::max(a, b);
+    scatter_shard(ls, L, ls.master, host, lo, hi);
 }
 
 void Executor::get_grads(i64 stage, float* host, int64_t n, int64_t* lo, int64_t* hi) {
@@ -1023,10 +1091,7 @@ void Executor::get_grads(i64 stage, float* host, int64_t n, int64_t* lo, int64_t
     const StageLayout& L = layouts_[static_cast<size_t>(stage)];
     if (n < L.numel) throw SpecError("get_grads: buffer too small");
     if (ls.gshard) {
-        const int64_t a = ls.shard_lo, b = std::min(ls.shard_lo + ls.shard_n, L.numel);
-        if (b > a) CK(cudaMemcpy(host + a, ls.gshard, static_cast<size_t>(b - a) * 4, cudaMemcpyDeviceToHost));
-        *lo = a;
-        *hi = std::max(a, b);
+        scatter_shard(ls, L, ls.gshard, host, lo, hi);
     } else {
         CK(cudaMemcpy(host, ls.grad, static_cast<size_t>(L.numel) * 4, cudaMemcpyDeviceToHost));
         *lo = 0;
@@ -1046,10 +1111,15 @@ void Executor::get_weights16(i64 stage, uint16_t* host, int64_t n, int64_t* lo, 
         *lo = 0;
         *hi = L.numel;
     } else {
-        const int64_t a = ls.shard_lo, b = std::min(ls.shard_lo + ls.shard_n, L.numel);
-        if (b > a) CK(cudaMemcpy(host + a, ls.w16_shard, static_cast<size_t>(b - a) * 2, cudaMemcpyDeviceToHost));
-        *lo = a;
-        *hi = std::max(a, b);
+        std::vector<uint16_t> sh(static_cast<size_t>(ls.shard_n));
+        CK(cudaMemcpy(sh.data(), ls.w16_shard, static_cast<size_t>(ls.shard_n) * 2, cudaMemcpyDeviceToHost));
+        std::fill(host, host + L.numel, static_cast<uint16_t>(0x7FC0));  // bf16 NaN where not owned
+        for_each_chunk(ls, [&](int64_t off, int64_t len, int64_t soff) {
+            const int64_t m = std::max<int64_t>(0, std::min(len, L.numel - off));
+            if (m > 0) std::memcpy(host + off, sh.data() + soff, static_cast<size_t>(m) * 2);
+        });
+        *lo = 0;
+        *hi = L.numel;
     }
 }
 

@@ -113,14 +113,14 @@ class Executor:
         return out, lo.value, hi.value
 
     def get_stage_params(self, stage: int):
-        """(full-size f32 array with this rank's [lo, hi) filled, lo, hi)."""
+        """(full-size f32 array, NaN where another DP rank owns the element, lo, hi)."""
         return self._get(N.lib().bfpp_exec_get_params, stage)
 
     def get_stage_grads(self, stage: int):
         return self._get(N.lib().bfpp_exec_get_grads, stage)
 
     def get_stage_weights16(self, stage: int):
-        """(bf16 compute weights as float32, lo, hi): the resident copy or this rank's DP_FS shard."""
+        """(bf16 compute weights as float32, lo, hi): the resident copy or this rank's DP_FS slices (NaN elsewhere)."""
         n = self.stage_numel(stage)
         raw = np.zeros(n, dtype=np.uint16)
         lo, hi = C.c_int64(), C.c_int64()

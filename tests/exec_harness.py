@@ -39,8 +39,10 @@ def run_rank(executor_factory, cfg, config, params, tokens, rank):
         flat = flatten_stage(params, cfg, s, n_stage)
         ex.set_stage_params(s, flat)
         w16, lo, hi = ex.get_stage_weights16(s)
+        own = ~np.isnan(w16[lo:hi])  # sharded variants: this rank's slices only
         want = torch_bf16(flat[lo:hi])
-        assert np.array_equal(w16[lo:hi], want), f"stage {s}: bf16 compute weights differ after set_params"
+        assert own.any() and np.array_equal(w16[lo:hi][own], want[own]), \
+            f"stage {s}: bf16 compute weights differ after set_params"
     loss = ex.step(tokens[dp])
     grads = {s: ex.get_stage_grads(s) for s in ex.local_stages}
     ex.close()
@@ -52,8 +54,8 @@ def run_rank(executor_factory, cfg, config, params, tokens, rank):
     for s in ex.local_stages:  # the bf16 copy the next step computes with is the rounded master
         w16, lo, hi = ex.get_stage_weights16(s)
         p, plo, phi = newp[s]
-        a, b = max(lo, plo), min(hi, phi)
-        assert np.array_equal(w16[a:b], torch_bf16(p[a:b])), f"stage {s}: bf16 weights != bf16(master)"
+        own = ~np.isnan(w16) & ~np.isnan(p)
+        assert own.any() and np.array_equal(w16[own], torch_bf16(p[own])), f"stage {s}: bf16 weights != bf16(master)"
     ex.close()
     return {"loss": loss, "loss2": loss2, "grads": grads, "params": newp}
 
@@ -99,9 +101,11 @@ def compare(cfg, config, results, params, tokens):
         for r, res in enumerate(results):
             if s in res["grads"]:
                 g, lo, hi = res["grads"][s]
-                full_g[lo:hi] = g[lo:hi]
+                own = ~np.isnan(g[lo:hi])  # this rank's elements (slices of every segment when sharded)
+                full_g[lo:hi][own] = g[lo:hi][own]
                 p, lo, hi = res["params"][s]
-                full_p[lo:hi] = p[lo:hi]
+                own = ~np.isnan(p[lo:hi])
+                full_p[lo:hi][own] = p[lo:hi][own]
         assert not np.isnan(full_g).any(), f"stage {s}: gradient shards do not cover the stage"
         got_g = unflatten_stage(full_g, cfg, s, n_stage)
         got_p = unflatten_stage(full_p, cfg, s, n_stage)
