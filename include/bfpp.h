@@ -258,7 +258,8 @@ int bfpp_exec_timeline(const bfpp_exec* e, double* start, double* end);
  * build_tasks graph, the local tasks in host enqueue order with their stream
  * (0 compute, 1 DP, 2/3 forward send/receive, 4/5 backward send/receive), flags
  * (1 send, 2 first reduce unit, 4 last reduce unit, 8 optimizer after, 16 first gradient
- * contribution of its unit, 32 last optimizer update of the step), DP_FS weight slot and the
+ * contribution of its unit, 32 last optimizer update of the step, 64 backward completing its
+ * stage's last reduction unit, 128 ... whose reduction is also the first unit), DP_FS weight slot and the
  * cross-stream waits (CSR). Call with cap = 0 to get *n_tasks and *n_waits. */
 int bfpp_plan_rank(const bfpp_graph* g, int64_t pp_rank, int64_t n_dp, int64_t cap, int32_t* ids, int32_t* streams,
                    int32_t* flags, int32_t* slots, int32_t* wait_offsets, int32_t* wait_ids, int64_t* n_tasks,

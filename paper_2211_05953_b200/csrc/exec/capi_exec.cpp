@@ -129,7 +129,8 @@ int bfpp_plan_rank(const bfpp_graph* g, int64_t pp_rank, int64_t n_dp, int64_t c
             ids[i] = p.id;
             streams[i] = p.stream;
             flags[i] = (p.send ? 1 : 0) | (p.first_unit ? 2 : 0) | (p.last_unit ? 4 : 0) | (p.adam_after ? 8 : 0) |
-                       (p.first_in_unit ? 16 : 0) | (p.adam_tail ? 32 : 0);
+                       (p.first_in_unit ? 16 : 0) | (p.adam_tail ? 32 : 0) | (p.last_unit_bwd ? 64 : 0) |
+                       (p.reduce_first_unit ? 128 : 0);
             slots[i] = p.slot;
             wait_offsets[i] = k;
             for (TaskId w : p.waits) wait_ids[k++] = w;

@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstdint>
 #include <cstring>
 #include <limits>
 #include <map>
@@ -729,9 +730,11 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
         return I.local[static_cast<size_t>(cidx)].w16;
     };
     // Adam over elements [lo, hi) of a stage's (shard of) master weights / moments / gradient
-    auto adam = [&](LocalStage& ls, cudaStream_t st, bool tail, int64_t lo = 0, int64_t hi = -1) {
+    auto adam = [&](LocalStage& ls, cudaStream_t st, bool tail, int64_t lo = 0, int64_t hi = -1, size_t s0 = 0,
+                    size_t s1 = SIZE_MAX) {
         if (o_.skip_optimizer) return;
         if (hi < 0) hi = ls.shard_n;
+        if (s1 == SIZE_MAX) s1 = ls.seg.size() - 1;
         const bool sharded = ls.gshard != nullptr;
         float* g = sharded ? ls.gshard : ls.grad;
         bf16* w = sharded ? ls.w16_shard : ls.w16;
@@ -739,8 +742,33 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
             adam_update(ls.master + lo, ls.m + lo, ls.v + lo, g + lo, w + lo, hi - lo, o_.lr, o_.beta1, o_.beta2,
                         o_.eps, o_.weight_decay, I.step_no, 0, st, tail ? 8 : 1);
         });
-        if (sharded && c_.dp_variant == DpVariant::DP_PS)
-            all_gather_segments(ls, ls.w16, 0, ls.seg.size() - 1, I.dp_comm, st);
+        if (sharded && c_.dp_variant == DpVariant::DP_PS) all_gather_segments(ls, ls.w16, s0, s1, I.dp_comm, st);
+    };
+    // Reduction of one stage segment (sharded variants): reduce-scatter its gradients into this
+    // rank's slice, fold in earlier units, and (last unit) update it — on stream st.
+    auto reduce_segment = [&](LocalStage& ls, cudaStream_t st, size_t si, bool first_unit, bool update, bool tail) {
+        const int64_t lo = ls.seg[si] / ls.nd, hi = ls.seg[si + 1] / ls.nd;
+        reduce_scatter_segments(ls, first_unit ? ls.gshard : ls.gtmp, si, si + 1, I.dp_comm, st);
+        if (!first_unit)
+            K(K_MISC, 12.0 * static_cast<double>(hi - lo), 1, st,
+              [&] { add_f32_kernel<<<296, 256, 0, st>>>(ls.gshard + lo, ls.gtmp + lo, hi - lo); });
+        if (update) adam(ls, st, tail, lo, hi, si, si + 1);
+        ls.seg_done[si] = 1;
+    };
+    // Under DP_FS / DP_PS the stage's last reduction unit runs segment by segment inside the
+    // backward that completes it: each layer is reduce-scattered and updated on the DP stream as
+    // soon as its gradients are final, leaving only the last segments for the Reduce task.
+    auto early_segment = [&](LocalStage& ls, cudaStream_t st, cudaStream_t ws, int64_t seg_start, bool first_unit) {
+        size_t si = 0;
+        while (si + 1 < ls.seg.size() && ls.seg[si] != seg_start) ++si;
+        if (si + 1 >= ls.seg.size()) return;  // single-segment layout: the Reduce task does it all
+        CK(cudaEventRecord(I.ev_opt[0], st));
+        CK(cudaStreamWaitEvent(ds, I.ev_opt[0], 0));
+        if (ws != st) {
+            CK(cudaEventRecord(I.ev_opt[1], ws));
+            CK(cudaStreamWaitEvent(ds, I.ev_opt[1], 0));
+        }
+        reduce_segment(ls, ds, si, first_unit, true, false);
     };
     // n_dp == 1: a parameter segment's gradient is final as soon as the stage's last backward
     // has produced it, so the optimizer runs segment by segment (a layer at a time) on the DP
@@ -809,6 +837,7 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
             cudaStream_t ws = I.wgrad_stream ? I.st[S_WGRAD] : st;
             const int acc = te.first_in_unit ? 0 : 1;  // the unit's first contribution overwrites
             const bool seg_opt = te.adam_after;  // only set on a backward task when n_dp == 1
+            const bool early = te.last_unit_bwd && ls.gshard != nullptr && ls.seg.size() > 2;
             const size_t nl = L.layers.size();
             auto layer_end = [&](size_t li) -> int64_t {
                 return li + 1 < nl ? L.layers[li + 1].ln1_g : (L.last ? L.lnf_g : ls.shard_n);
@@ -832,6 +861,7 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
                     acc);
                 g = I.g_head;
                 if (seg_opt) adam_segment(ls, st, ws, L.lnf_g, ls.shard_n);
+                if (early) early_segment(ls, st, ws, L.lnf_g, te.reduce_first_unit);
             } else {
                 g = a.gin;
             }
@@ -869,6 +899,7 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
                 LNB(st, I.tmp_h, x.x_in, W + P.ln1_g, x.mu1, x.rs1, gmid, gnext, G_ + P.ln1_g, G_ + P.ln1_b, acc);
                 g = gnext;
                 if (seg_opt) adam_segment(ls, st, ws, P.ln1_g, layer_end(li));
+                if (early) early_segment(ls, st, ws, P.ln1_g, te.reduce_first_unit);
             }
             if (L.first && acc == 0) {  // scatter-added gradients need a zeroed start
                 CK(cudaMemsetAsync(G_ + L.wte, 0, static_cast<size_t>(V * h) * 4, st));
@@ -922,6 +953,12 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
             const int64_t full = layouts_[static_cast<size_t>(t.stage)].padded;
             if (c_.dp_variant == DpVariant::DP0) {
                 NK(ncclAllReduce(ls.grad, ls.grad, static_cast<size_t>(full), ncclFloat32, ncclSum, I.dp_comm, st));
+            } else if (std::find(ls.seg_done.begin(), ls.seg_done.end(), 1) != ls.seg_done.end()) {
+                // the backward already reduced and updated some segments: finish the others
+                for (size_t si = 0; si + 1 < ls.seg.size(); ++si)
+                    if (!ls.seg_done[si]) reduce_segment(ls, st, si, te.first_unit, te.adam_after, te.adam_tail);
+                std::fill(ls.seg_done.begin(), ls.seg_done.end(), 0);
+                break;
             } else {
                 float* dst = te.first_unit ? ls.gshard : ls.gtmp;
                 reduce_scatter_segments(ls, dst, 0, ls.seg.size() - 1, I.dp_comm, st);

@@ -92,6 +92,12 @@ std::vector<PlanTask> plan_rank(const TaskGraph& g, i64 pp_rank, i64 n_dp) {
             }
             prev_bwd[t.stage] = id;
             if (n_dp < 2 && last_bwd_of_stage[t.stage] == id) te.adam_after = true;
+            auto red = reduce_of_last_bwd.find(id);
+            if (n_dp >= 2 && red != reduce_of_last_bwd.end()) {
+                const auto& rs = reduces_of_stage[t.stage];
+                te.last_unit_bwd = rs.back() == red->second;
+                te.reduce_first_unit = rs.front() == red->second;
+            }
         }
         if (t.kind == TaskKind::Reduce) {
             const auto& rs = reduces_of_stage[t.stage];
