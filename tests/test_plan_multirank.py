@@ -201,3 +201,24 @@ def test_emulator_detects_missing_wait():
     assert err is None
     with pytest.raises(AssertionError):
         check_dependencies(graph, order, n_pp, n_dp)
+
+
+@pytest.mark.parametrize("name", ["bf_pp2x2_dp2_fs", "gpipe_pp2_dp2_fs", "acc_df_dp2_fs"])
+def test_plan_marks_the_backward_completing_each_stage(name):
+    """Flag 64 (last-unit backward: the executor reduces that stage layer by layer inside it) sits on
+    exactly one backward per local stage -- the dependency of the stage's last Reduce; flag 128
+    marks it when that Reduce is also the stage's first (BF: one unit per stage)."""
+    graph, plans, n_pp, n_dp = _local_plans(name)
+    tasks = graph.tasks
+    for r in range(n_pp):
+        plan = plans[r]
+        flagged = {tasks[tid].stage: (tid, fl) for tid, st, fl, sl, w in plan if fl & 64}
+        reduces = {}
+        for tid, st, fl, sl, w in plan:
+            if tasks[tid].kind == ps.TaskKind.Reduce:
+                reduces.setdefault(tasks[tid].stage, []).append((tasks[tid].priority, tid))
+        assert set(flagged) == set(reduces)
+        for stage, (tid, fl) in flagged.items():
+            rs = sorted(reduces[stage])
+            assert tasks[rs[-1][1]].deps[0] == tid
+            assert bool(fl & 128) == (len(rs) == 1)
