@@ -730,7 +730,7 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
         return I.local[static_cast<size_t>(cidx)].w16;
     };
     // Adam over elements [lo, hi) of a stage's (shard of) master weights / moments / gradient
-    auto adam = [&](LocalStage& ls, cudaStream_t st, bool tail, int64_t lo = 0, int64_t hi = -1, size_t s0 = 0,
+    auto adam = [&](LocalStage& ls, cudaStream_t st, int64_t lo = 0, int64_t hi = -1, size_t s0 = 0,
                     size_t s1 = SIZE_MAX) {
         if (o_.skip_optimizer) return;
         if (hi < 0) hi = ls.shard_n;
@@ -740,19 +740,19 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
         bf16* w = sharded ? ls.w16_shard : ls.w16;
         K(K_ADAM, 30.0 * static_cast<double>(hi - lo), 1, st, [&] {
             adam_update(ls.master + lo, ls.m + lo, ls.v + lo, g + lo, w + lo, hi - lo, o_.lr, o_.beta1, o_.beta2,
-                        o_.eps, o_.weight_decay, I.step_no, 0, st, tail ? 8 : 1);
+                        o_.eps, o_.weight_decay, I.step_no, 0, st);
         });
         if (sharded && c_.dp_variant == DpVariant::DP_PS) all_gather_segments(ls, ls.w16, s0, s1, I.dp_comm, st);
     };
     // Reduction of one stage segment (sharded variants): reduce-scatter its gradients into this
     // rank's slice, fold in earlier units, and (last unit) update it — on stream st.
-    auto reduce_segment = [&](LocalStage& ls, cudaStream_t st, size_t si, bool first_unit, bool update, bool tail) {
+    auto reduce_segment = [&](LocalStage& ls, cudaStream_t st, size_t si, bool first_unit, bool update) {
         const int64_t lo = ls.seg[si] / ls.nd, hi = ls.seg[si + 1] / ls.nd;
         reduce_scatter_segments(ls, first_unit ? ls.gshard : ls.gtmp, si, si + 1, I.dp_comm, st);
         if (!first_unit)
             K(K_MISC, 12.0 * static_cast<double>(hi - lo), 1, st,
               [&] { add_f32_kernel<<<296, 256, 0, st>>>(ls.gshard + lo, ls.gtmp + lo, hi - lo); });
-        if (update) adam(ls, st, tail, lo, hi, si, si + 1);
+        if (update) adam(ls, st, lo, hi, si, si + 1);
         ls.seg_done[si] = 1;
     };
     // Under DP_FS / DP_PS the stage's last reduction unit runs segment by segment inside the
@@ -768,7 +768,7 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
             CK(cudaEventRecord(I.ev_opt[1], ws));
             CK(cudaStreamWaitEvent(ds, I.ev_opt[1], 0));
         }
-        reduce_segment(ls, ds, si, first_unit, true, false);
+        reduce_segment(ls, ds, si, first_unit, true);
     };
     // n_dp == 1: a parameter segment's gradient is final as soon as the stage's last backward
     // has produced it, so the optimizer runs segment by segment (a layer at a time) on the DP
@@ -781,7 +781,7 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
             CK(cudaEventRecord(I.ev_opt[1], ws));
             CK(cudaStreamWaitEvent(ds, I.ev_opt[1], 0));
         }
-        adam(ls, ds, false, lo, hi);
+        adam(ls, ds, lo, hi);
     };
 
     for (const TaskExec& te : I.order) {
@@ -956,7 +956,7 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
             } else if (std::find(ls.seg_done.begin(), ls.seg_done.end(), 1) != ls.seg_done.end()) {
                 // the backward already reduced and updated some segments: finish the others
                 for (size_t si = 0; si + 1 < ls.seg.size(); ++si)
-                    if (!ls.seg_done[si]) reduce_segment(ls, st, si, te.first_unit, te.adam_after, te.adam_tail);
+                    if (!ls.seg_done[si]) reduce_segment(ls, st, si, te.first_unit, te.adam_after);
                 std::fill(ls.seg_done.begin(), ls.seg_done.end(), 0);
                 break;
             } else {
@@ -966,7 +966,7 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
                     K(K_MISC, 12.0 * ls.shard_n, 1, st, [&] { add_f32_kernel<<<296, 256, 0, st>>>(ls.gshard, ls.gtmp, ls.shard_n); });
                 // no re-zeroing: the next unit's first backward overwrites the gradient buffer
             }
-            if (te.adam_after) adam(ls, st, te.adam_tail);
+            if (te.adam_after) adam(ls, st);
             break;
         }
         }

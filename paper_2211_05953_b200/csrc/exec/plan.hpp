@@ -22,7 +22,7 @@ struct PlanTask {
     bool first_unit = false, last_unit = false;  // Reduce
     bool adam_after = false;    // Bwd (n_dp == 1) or Reduce (last unit): run the optimizer for this stage
     bool first_in_unit = false; // Bwd: first gradient contribution of its reduction unit (overwrite, no zeroing)
-    bool adam_tail = false;     // the step's last optimizer update (nothing left to overlap: full-chip grid)
+    bool adam_tail = false;     // the step's last optimizer update (nothing left to overlap it; informational)
     // Bwd that completes its stage's last reduction unit (n_dp >= 2): the executor may reduce and
     // update the stage segment by segment inside it; reduce_first_unit = that Reduce is also the
     // stage's first unit (its reduce-scatter overwrites the gradient shard)

@@ -266,7 +266,7 @@ void softmax_xent(void* logits, int64_t ld, const int32_t* labels, float* row_lo
 }
 
 void adam_update(float* p, float* m, float* v, float* g, void* w16, int64_t n, float lr, float b1, float b2,
-                 float eps, float wd, int step, int zero_grad, cudaStream_t st, int blocks_per_sm) {
+                 float eps, float wd, int step, int zero_grad, cudaStream_t st) {
     // the vector kernel multiplies by the reciprocals of the bias corrections
     const float bc1 = 1.f / (1.f - powf(b1, static_cast<float>(step)));
     const float bc2 = 1.f / (1.f - powf(b2, static_cast<float>(step)));
@@ -276,7 +276,6 @@ void adam_update(float* p, float* m, float* v, float* g, void* w16, int64_t n, f
         return true;
     }();
     (void)once;
-    (void)blocks_per_sm;  // kept for the ABI; every call uses short-lived blocks (see adam_kernel)
     const int64_t blocks = (n / 4 + kAdamThreads - 1) / kAdamThreads;
     adam_kernel<<<static_cast<unsigned>(blocks > 0 ? blocks : 1), kAdamThreads, 0, st>>>(
         p, m, v, g, static_cast<__nv_bfloat16*>(w16), n, lr, b1, b2, eps, wd, bc1, bc2, zero_grad);

@@ -32,7 +32,7 @@ void embed_bwd(const int32_t* tok, const void* dx, float* dwte, float* dwpe, int
 void softmax_xent(void* logits, int64_t ld, const int32_t* labels, float* row_loss, int T, int V, float grad_scale,
                   cudaStream_t st);
 void adam_update(float* p, float* m, float* v, float* g, void* w16, int64_t n, float lr, float b1, float b2,
-                 float eps, float wd, int step, int zero_grad, cudaStream_t st, int blocks_per_sm = 1);
+                 float eps, float wd, int step, int zero_grad, cudaStream_t st);
 void init_normal(float* p, void* w16, int64_t n, float mean, float std, uint64_t seed, uint64_t offset,
                  cudaStream_t st);
 void f32_to_bf16(const float* src, void* dst, int64_t n, cudaStream_t st);
