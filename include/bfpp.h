@@ -194,7 +194,8 @@ int bfpp_adam_update(float* p, float* m, float* v, float* g, void* w16, int64_t 
  * bfpp_build_tasks and runs this rank's slice: Compute lane -> compute stream in
  * program order; DpNet lane -> DP stream in priority order (NCCL all-gather for
  * Reconstruct, reduce-scatter / all-reduce + sharded Adam for Reduce); PpNet ->
- * ncclSend/ncclRecv on one 2-rank communicator + stream per directed pipeline edge.
+ * copy-engine peer copies into the receiver's CUDA-IPC-mapped slots, signalled with stream
+ * memory operations (no NCCL on the pipeline path).
  * The model is a pre-LN GPT (bias-free linears, GeLU MLP, untied embeddings; the
  * embedding is folded into stage 0 and final LN + LM head + loss into the last
  * stage). */
@@ -213,9 +214,8 @@ typedef struct bfpp_exec_opts {
 
 /* Fills 128 bytes with a fresh ncclUniqueId (generated on one rank, broadcast by the caller). */
 int bfpp_nccl_unique_id(void* out);
-/* Number of unique ids bfpp_exec_create expects: 1 + n_pp (DP groups) + 2 * n_pp * n_dp
- * (directed pipeline edges); id[1 + d] = DP group of pipeline rank d, id[1 + n_pp + (dp*n_pp + d)*2 + dir]
- * = edge d -> d+1 (dir 0, forward) or d -> d-1 (dir 1, backward) of replica dp. */
+/* Number of unique ids bfpp_exec_create expects: 1 + n_pp; id[0] = the world communicator (IPC
+ * handle exchange, teardown barrier, timeline origin), id[1 + d] = DP group of pipeline rank d. */
 int64_t bfpp_exec_n_comm_ids(const bfpp_parallel_config* c);
 int bfpp_exec_create(const bfpp_model_spec* m, const bfpp_parallel_config* c, const bfpp_exec_opts* o,
                      int32_t rank, int32_t world, const void* uids, bfpp_exec** out);
@@ -267,7 +267,8 @@ int bfpp_plan_rank(const bfpp_graph* g, int64_t pp_rank, int64_t n_dp, int64_t c
 
 /* toggles per-task timeline events and per-kernel profiling for subsequent steps */
 int bfpp_exec_set_flags(bfpp_exec* e, int32_t record_timeline, int32_t profile_kernels);
-/* the executor's compute stream (cudaStream_t); every step starts and ends on it */
+/* the executor's compute stream (cudaStream_t); every step starts on it and ends on it with
+ * all of the step's streams joined (events recorded on it after a step bracket the whole step) */
 void* bfpp_exec_stream(const bfpp_exec* e);
 /* kernel statistics of the last step for category cat (0 GEMM, 1 attention fwd,
  * 2 attention bwd, 3 LayerNorm, 4 misc (embedding, cross-entropy, reductions), 5 Adam):

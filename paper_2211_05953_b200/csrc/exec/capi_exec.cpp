@@ -26,7 +26,7 @@ int bfpp_nccl_unique_id(void* out) {
     });
 }
 
-int64_t bfpp_exec_n_comm_ids(const bfpp_parallel_config* c) { return 1 + c->n_pp + 2 * c->n_pp * c->n_dp; }
+int64_t bfpp_exec_n_comm_ids(const bfpp_parallel_config* c) { return 1 + c->n_pp; }
 
 namespace {
 int create(const bfpp_model_spec* m, const bfpp_parallel_config* c, const bfpp_graph* g, const bfpp_exec_opts* o,

@@ -350,7 +350,7 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
     // teardown barrier) and one DP group per pipeline rank. Pipeline hand-offs do not use NCCL.
     const bool fs = c_.n_dp >= 2 && c_.dp_variant == DpVariant::DP_FS;
     {
-        const size_t need = static_cast<size_t>(1 + p_ + 2 * p_ * c_.n_dp);
+        const size_t need = static_cast<size_t>(1 + p_);
         if (world > 1 && uids.size() < need) throw SpecError("executor: not enough NCCL unique ids");
         NK(ncclGroupStart());
         if (world > 1) NK(ncclCommInitRank(&I.world_comm, world, uids[0], rank));
