@@ -252,6 +252,7 @@ struct Executor::Impl {
     bf16 *gmid_s[2] = {}, *dpre_s[2] = {}, *dqkv_s[2] = {}, *gout_s[2] = {}, *g_head = nullptr;
     cudaEvent_t ev_a[2] = {}, ev_b[2] = {}, ev_wg[2] = {};
     cudaEvent_t ev_opt[2] = {};  // segment-wise optimizer hand-off (compute, wgrad stream)
+    std::vector<cudaEvent_t> rec_ev[2];  // DP_FS: per weight slot, one event per all-gathered segment
     std::vector<cudaEvent_t> done_g;  // per Bwd task: its gradients are complete (compute + wgrad streams)
     float *dq_acc = nullptr, *delta = nullptr;
     int32_t *inputs = nullptr, *labels = nullptr;
@@ -391,8 +392,15 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
         }
         I.local.push_back(ls);
     }
-    if (fs)
+    if (fs) {
         for (auto& s : I.slots) s = I.alloc<bf16>(static_cast<size_t>(max_padded), &total);
+        size_t max_seg = 1;
+        for (const auto& ls : I.local) max_seg = std::max(max_seg, ls.seg.size() - 1);
+        for (auto& evs : I.rec_ev) {
+            evs.resize(max_seg);
+            for (auto& e : evs) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+    }
     // default initialisation: N(0, std), output projections std/sqrt(2L), LayerNorm (1, 0)
     for (auto& ls : I.local) {
         const StageLayout& L = layouts_[static_cast<size_t>(ls.stage)];
@@ -586,6 +594,9 @@ Executor::~Executor() {
     for (auto e : I.t_end)
         if (e) cudaEventDestroy(e);
     for (auto e : I.ev_pool) cudaEventDestroy(e);
+    for (auto& evs : I.rec_ev)
+        for (auto e : evs)
+            if (e) cudaEventDestroy(e);
     for (auto e : I.done_g)
         if (e) cudaEventDestroy(e);
     for (int k = 0; k < 2; ++k)
@@ -787,11 +798,26 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
     for (const TaskExec& te : I.order) {
         const Task& t = graph_.tasks[static_cast<size_t>(te.id)];
         cudaStream_t st = I.st[te.stream];
+        // DP_FS: a compute task waits for its weights segment by segment (right before each layer
+        // uses them), so it starts as soon as the first segment has been all-gathered
+        bool seg_wait = false;
         for (TaskId d : te.waits) {
+            const TaskKind dk = graph_.tasks[static_cast<size_t>(d)].kind;
+            if (fs && dk == TaskKind::Reconstruct && (t.kind == TaskKind::Fwd || t.kind == TaskKind::Bwd)) {
+                seg_wait = true;
+                continue;
+            }
             // gradient consumers (Reduce) need the wgrad stream's half of a backward task too
-            const bool grads = graph_.tasks[static_cast<size_t>(d)].kind == TaskKind::Bwd && t.kind == TaskKind::Reduce;
+            const bool grads = dk == TaskKind::Bwd && t.kind == TaskKind::Reduce;
             CK(cudaStreamWaitEvent(st, grads ? I.done_g[static_cast<size_t>(d)] : I.done[static_cast<size_t>(d)], 0));
         }
+        // wait for the all-gather of the weight segment that holds stage-vector offset `off`
+        auto need_weights = [&](const LocalStage& ls, int64_t off) {
+            if (!seg_wait) return;
+            size_t si = 0;
+            while (si + 2 < ls.seg.size() && ls.seg[si + 1] <= off) ++si;
+            CK(cudaStreamWaitEvent(st, I.rec_ev[te.slot][si], 0));
+        };
         if (o_.record_timeline) CK(cudaEventRecord(I.t_start[static_cast<size_t>(te.id)], st));
         const int cidx = I.task_c[static_cast<size_t>(te.id)];
         switch (t.kind) {
@@ -799,7 +825,9 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
             const StageLayout& L = layouts_[static_cast<size_t>(t.stage)];
             StageActs& a = I.acts[static_cast<size_t>(t.micro_batch)][static_cast<size_t>(cidx)];
             const bf16* W = weights(te, cidx);
+            const LocalStage& lsw = I.local[static_cast<size_t>(cidx)];
             const int32_t* inp = I.inputs + t.micro_batch * T;
+            if (L.first) need_weights(lsw, L.wte);
             if (L.first)
                 K(K_MISC, 3 * Th2, 1, st, [&] {
                     embed_fwd(inp, W + L.wte, W + L.wpe, a.in, static_cast<int>(T), S, static_cast<int>(h), st);
@@ -807,6 +835,7 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
             for (size_t l = 0; l < L.layers.size(); ++l) {
                 const LayerParams& P = L.layers[l];
                 LayerActs& x = a.layers[l];
+                need_weights(lsw, P.ln1_g);
                 LNF(st, x.x_in, W + P.ln1_g, W + P.ln1_b, x.ln1, x.mu1, x.rs1);
                 G(st, T, 3 * h, h, x.ln1, h, 0, W + P.qkv, h, 0, x.qkv, 3 * h, GEMM_EPI_BF16);
                 K(K_ATTN_FWD, attn_flops, 1, st, [&] { attention_fwd(x.qkv, x.o, x.lse, B, S, H, 128, st); });
@@ -816,6 +845,7 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
                 G(st, T, h, mlp, x.act, mlp, 0, W + P.fc2, mlp, 0, x.x_out, h, GEMM_EPI_RESID, x.x_mid, h);
             }
             if (L.last) {
+                need_weights(lsw, L.lnf_g);
                 LNF(st, a.out, W + L.lnf_g, W + L.lnf_b, a.lnf, a.muf, a.rsf);
                 G(st, T, V, h, a.lnf, h, 0, W + L.head, h, 0, a.logits, V, GEMM_EPI_BF16);
                 K(K_MISC, 4.0 * static_cast<double>(T * V), 1, st, [&] {
@@ -852,6 +882,7 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
             };
             const bf16* g;
             if (L.last) {
+                need_weights(ls, L.lnf_g);
                 G(st, T, h, V, a.logits, V, 0, W + L.head, h, 1, I.tmp_h, h, GEMM_EPI_BF16);
                 CK(cudaEventRecord(I.ev_a[0], st));  // logits/lnf are persistent; only ordering matters
                 CK(cudaStreamWaitEvent(ws, I.ev_a[0], 0));
@@ -868,6 +899,7 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
             for (size_t li = L.layers.size(); li-- > 0;) {
                 const LayerParams& P = L.layers[li];
                 LayerActs& x = a.layers[li];
+                need_weights(ls, P.ln1_g);
                 const int lc = I.bwd_layers++;
                 const int k = lc & 1;
                 // set k was last read by the wgrads of layer lc-2
@@ -945,7 +977,10 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
         }
         case TaskKind::Reconstruct: {
             LocalStage& ls = I.local[static_cast<size_t>(t.stage / p_)];
-            all_gather_segments(ls, I.slots[te.slot], 0, ls.seg.size() - 1, I.dp_comm, st);
+            for (size_t si = 0; si + 1 < ls.seg.size(); ++si) {
+                all_gather_segments(ls, I.slots[te.slot], si, si + 1, I.dp_comm, st);
+                CK(cudaEventRecord(I.rec_ev[te.slot][si], st));
+            }
             break;
         }
         case TaskKind::Reduce: {
