@@ -30,6 +30,8 @@ CASES = {
     # four-way data parallelism (the DP group size of bench.py at N = 8)
     "bf_pp1x2_dp4_fs": dict(n_dp=4, n_pp=1, n_loop=2, n_mb=2, dp_variant="DP_FS", schedule="BreadthFirst"),
     "np_dp4_dp0": dict(n_dp=4, n_pp=1, n_loop=1, n_mb=1, dp_variant="DP0", schedule="NoPipeline"),
+    # three ranks: layer segments do not split into 8-element slices -> one segment per stage
+    "bf_pp1x2_dp3_fs": dict(n_dp=3, n_pp=1, n_loop=2, n_mb=2, dp_variant="DP_FS", schedule="BreadthFirst"),
     # gradient-accumulation graphs (build_accumulation_tasks, schedule.cpp:454-500; PAPER App. C):
     # one layer per stage, data parallel; breadth-first reduces per layer, depth-first per micro-batch
     "acc_bf_dp2_fs_mb3": dict(n_dp=2, n_mb=3, dp_variant="DP_FS", accumulation="BreadthFirst"),
