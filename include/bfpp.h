@@ -148,6 +148,10 @@ typedef struct bfpp_gemm_args {
 
 /* D[M,N] = sum_k A[m,k] B[n,k] on tcgen05 (TMA + TMEM), bf16 in, f32 accumulate */
 int bfpp_gemm_bf16(const bfpp_gemm_args* args, void* stream);
+/* Two independent GEMMs in one launch (one persistent tile space: the pair fills the SMs' waves
+ * together and pays one prologue); same operand majors and M, N >= 256 required for the grouped
+ * kernel, otherwise (or with BFPP_GEMM_PAIR=0) two ordinary launches. Results equal bfpp_gemm_bf16. */
+int bfpp_gemm_bf16_pair(const bfpp_gemm_args* a, const bfpp_gemm_args* b, void* stream);
 /* GEMM variant selection for benchmarks and tests (process-wide): mode -1 auto, 1 one-CTA
  * 128-row tiles, 2 two-CTA 256-row tiles; bn2 = pair-tile width (0 default = 256, 128 opt-in);
  * stream_k = 0 off (default), 1 forced, -1 auto (only when the last tile wave leaves pairs idle).

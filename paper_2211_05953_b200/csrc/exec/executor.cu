@@ -723,6 +723,40 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
         K(K_GEMM, 2.0 * M * N * Kd, 1, st,
           [&] { gemm(st, M, N, Kd, A, lda, amn, Bp, ldb, bmn, D, ldd, epi, aux, ldaux, aux_out, ldaux_out, acc); });
     };
+    // two independent f32 weight-gradient GEMMs (store or reduce-add) in one grouped launch
+    struct WG {
+        int64_t M, N, Kd;
+        const void* A;
+        int64_t lda;
+        int amn;
+        const void* B;
+        int64_t ldb;
+        int bmn;
+        void* D;
+        int64_t ldd;
+    };
+    auto G2 = [&](cudaStream_t st, const WG& x, const WG& y, int acc) {
+        auto args = [&](const WG& w) {
+            GemmArgs a;
+            a.M = w.M;
+            a.N = w.N;
+            a.K = w.Kd;
+            a.A = w.A;
+            a.lda = w.lda;
+            a.a_mn_major = w.amn;
+            a.B = w.B;
+            a.ldb = w.ldb;
+            a.b_mn_major = w.bmn;
+            a.D = w.D;
+            a.ldd = w.ldd;
+            a.epilogue = GEMM_EPI_F32;
+            a.accumulate = acc;
+            return a;
+        };
+        const GemmArgs ax = args(x), ay = args(y);
+        K(K_GEMM, 2.0 * (x.M * x.N * x.Kd + y.M * y.N * y.Kd), gemm_pairable(ax, ay) ? 1 : 2, st,
+          [&] { gemm_bf16_pair(ax, ay, st); });
+    };
     const double Th2 = 2.0 * static_cast<double>(T * h);  // bytes of one [T,h] bf16 activation
     const double attn_flops = 2.0 * B * static_cast<double>(S) * (S + 1) * static_cast<double>(h);  // causal, fwd
     auto LNF = [&](cudaStream_t st, const bf16* x, const bf16* g, const bf16* b, bf16* y, float* mu, float* rs) {
@@ -910,8 +944,9 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
                 G(st, T, mlp, h, g, h, 0, W + P.fc2, mlp, 1, dpre, mlp, GEMM_EPI_DGELU, x.pre, mlp);
                 CK(cudaEventRecord(I.ev_a[k], st));
                 CK(cudaStreamWaitEvent(ws, I.ev_a[k], 0));
-                G(ws, h, mlp, T, g, h, 1, x.act, mlp, 1, G_ + P.fc2, mlp, GEMM_EPI_F32, nullptr, 0, nullptr, 0, acc);
-                G(ws, mlp, h, T, dpre, mlp, 1, x.ln2, h, 1, G_ + P.fc1, h, GEMM_EPI_F32, nullptr, 0, nullptr, 0, acc);
+                // weight gradients of fc2 and fc1: independent, one grouped launch
+                G2(ws, {h, mlp, T, g, h, 1, x.act, mlp, 1, G_ + P.fc2, mlp},
+                   {mlp, h, T, dpre, mlp, 1, x.ln2, h, 1, G_ + P.fc1, h}, acc);
                 G(st, T, h, mlp, dpre, mlp, 0, W + P.fc1, h, 1, I.tmp_h, h, GEMM_EPI_BF16);
                 LNB(st, I.tmp_h, x.x_mid, W + P.ln2_g, x.mu2, x.rs2, g, gmid, G_ + P.ln2_g, G_ + P.ln2_b, acc);
                 // attention: x_mid = x_in + attn(ln1 Wqkv^T) Wo^T
@@ -921,9 +956,8 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
                 });
                 CK(cudaEventRecord(I.ev_b[k], st));
                 CK(cudaStreamWaitEvent(ws, I.ev_b[k], 0));
-                G(ws, h, h, T, gmid, h, 1, x.o, h, 1, G_ + P.o, h, GEMM_EPI_F32, nullptr, 0, nullptr, 0, acc);
-                G(ws, 3 * h, h, T, dqkv, 3 * h, 1, x.ln1, h, 1, G_ + P.qkv, h, GEMM_EPI_F32, nullptr, 0, nullptr, 0,
-                  acc);
+                G2(ws, {h, h, T, gmid, h, 1, x.o, h, 1, G_ + P.o, h}, {3 * h, h, T, dqkv, 3 * h, 1, x.ln1, h, 1, G_ + P.qkv, h},
+                   acc);
                 CK(cudaEventRecord(I.ev_wg[k], ws));
                 G(st, T, h, 3 * h, dqkv, 3 * h, 0, W + P.qkv, h, 1, I.tmp_h, h, GEMM_EPI_BF16);
                 // gnext (set k) was last read as g_in by the wgrad of layer lc-1

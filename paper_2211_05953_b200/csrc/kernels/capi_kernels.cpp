@@ -29,27 +29,40 @@ int bfpp_gemm_config(int32_t mode, int32_t bn2, int32_t stream_k) {
     });
 }
 
+namespace {
+GemmArgs to_gemm(const bfpp_gemm_args* a) {
+    GemmArgs g;
+    g.M = a->M;
+    g.N = a->N;
+    g.K = a->K;
+    g.A = a->A;
+    g.lda = a->lda;
+    g.a_mn_major = a->a_mn_major;
+    g.B = a->B;
+    g.ldb = a->ldb;
+    g.b_mn_major = a->b_mn_major;
+    g.D = a->D;
+    g.ldd = a->ldd;
+    g.aux = a->aux;
+    g.ldaux = a->ldaux;
+    g.aux_out = a->aux_out;
+    g.ldaux_out = a->ldaux_out;
+    g.epilogue = a->epilogue;
+    g.accumulate = a->accumulate;
+    return g;
+}
+}  // namespace
+
 int bfpp_gemm_bf16(const bfpp_gemm_args* a, void* stream) {
     return guarded([&] {
-        GemmArgs g;
-        g.M = a->M;
-        g.N = a->N;
-        g.K = a->K;
-        g.A = a->A;
-        g.lda = a->lda;
-        g.a_mn_major = a->a_mn_major;
-        g.B = a->B;
-        g.ldb = a->ldb;
-        g.b_mn_major = a->b_mn_major;
-        g.D = a->D;
-        g.ldd = a->ldd;
-        g.aux = a->aux;
-        g.ldaux = a->ldaux;
-        g.aux_out = a->aux_out;
-        g.ldaux_out = a->ldaux_out;
-        g.epilogue = a->epilogue;
-        g.accumulate = a->accumulate;
-        gemm_bf16(g, static_cast<cudaStream_t>(stream));
+        gemm_bf16(to_gemm(a), static_cast<cudaStream_t>(stream));
+        check_launch();
+    });
+}
+
+int bfpp_gemm_bf16_pair(const bfpp_gemm_args* a, const bfpp_gemm_args* b, void* stream) {
+    return guarded([&] {
+        gemm_bf16_pair(to_gemm(a), to_gemm(b), static_cast<cudaStream_t>(stream));
         check_launch();
     });
 }

@@ -35,7 +35,11 @@ struct GemmArgs {
 
 void gemm_bf16(const GemmArgs& g, cudaStream_t stream);
 extern int gemm_mode;  // -1 auto (2-CTA tiles when M, N >= 256), 1 force 1-CTA, 2 force 2-CTA
-void gemm_bf16_configure(int mode, int bn2, int stream_k);  // overrides the environment defaults
+void gemm_bf16_configure(int mode, int bn2, int stream_k);
+// Two independent GEMMs (same operand majors) in one grouped 2-CTA launch when eligible, else two launches.
+void gemm_bf16_pair(const GemmArgs& a, const GemmArgs& b, cudaStream_t st);
+bool gemm_pairable(const GemmArgs& a, const GemmArgs& b);  // one grouped launch (else two)
+extern int gemm_pair;  // grouped pair launches (default 1; BFPP_GEMM_PAIR=0 disables)  // overrides the environment defaults
 extern int gemm_bn2;   // 2-CTA pair-tile width: 0 default (256), 128 opt-in
 extern int gemm_pdl;   // programmatic dependent launch of the GEMM kernels (default 0, BFPP_GEMM_PDL=1)
 extern int gemm_sk;    // stream-K in the 2-CTA kernel: -1 auto, 0 off, 1 forced (BFPP_GEMM_SK)

@@ -110,6 +110,15 @@ struct Seg {
     int tile, kb0, kb1;
 };
 
+// Second problem of a grouped launch (two independent GEMMs with the same operand majors, e.g.
+// the weight gradients of fc2 and fc1): its tiles follow the first problem's in one persistent
+// tile space, so the pair fills the SM pairs' waves together and pays one prologue.
+struct Second {
+    CUtensorMap A, B, D;
+    int M, N, K;
+    EpiArgs ep;
+};
+
 struct WorkIter {
     bool sk;
     int t, step, num_tiles, nk;  // data-parallel: tiles t, t + step, ...
@@ -464,10 +473,11 @@ struct Smem2 {
     static constexpr int kBytes = kBarOffset + 256 + 1024;
 };
 
-template <int BN, int A_MN, int B_MN, bool SK>
+template <int BN, int A_MN, int B_MN, bool SK, bool GROUP>
 __global__ void __maxnreg__(96)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                 const __grid_constant__ CUtensorMap tmD, int M, int N, int K, EpiArgs ep, SkArgs sk) {
+                 const __grid_constant__ CUtensorMap tmD, int M, int N, int K, EpiArgs ep, SkArgs sk,
+                 const __grid_constant__ Second p2) {
     using S = Smem2<BN>;
     constexpr int kStages2 = S::kStages;
     extern __shared__ uint8_t smem_raw[];
@@ -482,16 +492,34 @@ __global__ void __maxnreg__(96)
     const int lane = threadIdx.x % 32;
     const uint32_t rank = ptx::cluster_ctarank();
     const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
-    const int m_tiles = (M + 255) / 256;
-    const int n_tiles = (N + BN - 1) / BN;
-    const int num_tiles = m_tiles * n_tiles;
-    const int nk = (K + BK - 1) / BK;
-    const bool use_sk = SK && BN == 256 && sk.ws != nullptr;  // stream-K instantiation only
+    const int m_tiles0 = (M + 255) / 256;
+    const int tiles0 = m_tiles0 * ((N + BN - 1) / BN);
+    const int nk0 = (K + BK - 1) / BK;
+    const int m_tiles1 = GROUP ? (p2.M + 255) / 256 : 1;
+    const int nk1 = GROUP ? (p2.K + BK - 1) / BK : 1;
+    const int num_tiles = tiles0 + (GROUP ? m_tiles1 * ((p2.N + BN - 1) / BN) : 0);
+    const int nk = nk0;  // stream-K (never grouped) splits the first problem's k-blocks
+    const bool use_sk = SK && !GROUP && BN == 256 && sk.ws != nullptr;  // stream-K instantiation only
+    // problem of global tile t: tensor maps, shape, epilogue, tile index within the problem
+    struct Prob {
+        const CUtensorMap *A, *B, *D;
+        int M, N, nk, m_tiles, t;
+        const EpiArgs* ep;
+    };
+    auto prob = [&](int t) -> Prob {
+        if (GROUP && t >= tiles0) return {&p2.A, &p2.B, &p2.D, p2.M, p2.N, nk1, m_tiles1, t - tiles0, &p2.ep};
+        return {&tmA, &tmB, &tmD, M, N, nk0, m_tiles0, t, &ep};
+    };
 
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch(&tmA);
         ptx::tma_prefetch(&tmB);
         ptx::tma_prefetch(&tmD);
+        if (GROUP) {
+            ptx::tma_prefetch(&p2.A);
+            ptx::tma_prefetch(&p2.B);
+            ptx::tma_prefetch(&p2.D);
+        }
         for (int s = 0; s < kStages2; ++s) {
             ptx::mbar_init(&full[s], 1);
             ptx::mbar_init(&empty[s], 1);
@@ -519,8 +547,10 @@ __global__ void __maxnreg__(96)
             WorkIter wi(use_sk, pair, n_pairs, num_tiles, nk);
             Seg g;
             while (wi.next(g)) {
-                const int t = g.tile;
-                const int m0 = (t % m_tiles) * 256 + 128 * rank, n0 = (t / m_tiles) * BN + (BN / 2) * rank;
+                const Prob pb = prob(g.tile);
+                if (!use_sk) g.kb1 = pb.nk;
+                const int t = pb.t;
+                const int m0 = (t % pb.m_tiles) * 256 + 128 * rank, n0 = (t / pb.m_tiles) * BN + (BN / 2) * rank;
                 for (int kb = g.kb0; kb < g.kb1; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* sa = smem + stage * S::kStageBytes;
@@ -530,16 +560,16 @@ __global__ void __maxnreg__(96)
                     if (A_MN) {
 #pragma unroll
                         for (int i = 0; i < 2; ++i)
-                            ptx::tma_load_2d_2sm(sa + i * 64 * BK * 2, &tmA, &full[stage], m0 + 64 * i, k0);
+                            ptx::tma_load_2d_2sm(sa + i * 64 * BK * 2, pb.A, &full[stage], m0 + 64 * i, k0);
                     } else {
-                        ptx::tma_load_2d_2sm(sa, &tmA, &full[stage], k0, m0);
+                        ptx::tma_load_2d_2sm(sa, pb.A, &full[stage], k0, m0);
                     }
                     if (B_MN) {
 #pragma unroll
                         for (int i = 0; i < BN / 128; ++i)
-                            ptx::tma_load_2d_2sm(sb + i * 64 * BK * 2, &tmB, &full[stage], n0 + 64 * i, k0);
+                            ptx::tma_load_2d_2sm(sb + i * 64 * BK * 2, pb.B, &full[stage], n0 + 64 * i, k0);
                     } else {
-                        ptx::tma_load_2d_2sm(sb, &tmB, &full[stage], k0, n0);
+                        ptx::tma_load_2d_2sm(sb, pb.B, &full[stage], k0, n0);
                     }
                     if (++stage == kStages2) {
                         stage = 0;
@@ -558,6 +588,7 @@ __global__ void __maxnreg__(96)
             WorkIter wi(use_sk, pair, n_pairs, num_tiles, nk);
             Seg g;
             for (; wi.next(g); ++it) {
+                if (!use_sk) g.kb1 = prob(g.tile).nk;
                 const int acc = it & 1;
                 const uint32_t acc_phase = (it >> 1) & 1;
                 ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -591,20 +622,24 @@ __global__ void __maxnreg__(96)
         const int q = warp & 3;        // TMEM lane quarter (hardware: warp id % 4)
         const int half = ew >> 2;      // which alternate 128-byte column strips this warp owns
         uint8_t* stage_out = smem + S::kOutOffset + ew * kStageBytesOut;
-        const bool f32_out = ep.epi == GEMM_EPI_F32;
-        const int cw = f32_out ? 32 : 64;  // tile columns per 128-byte strip
-        const int n_strips = BN / cw;
         int it = 0;
         const int lr = q * 32 + lane;  // this thread's accumulator row within the CTA's 128 rows
         WorkIter wi(use_sk, pair, n_pairs, num_tiles, nk);
         Seg g;
         for (; wi.next(g); ++it) {
-            const int t = g.tile;
+            const Prob pb = prob(g.tile);
+            if (!use_sk) g.kb1 = pb.nk;
+            const EpiArgs& ep_t = *pb.ep;
+            const CUtensorMap* td = pb.D;
+            const bool f32_out = ep_t.epi == GEMM_EPI_F32;
+            const int cw = f32_out ? 32 : 64;  // tile columns per 128-byte strip
+            const int n_strips = BN / cw;
+            const int t = pb.t;
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
-            const int m0 = (t % m_tiles) * 256 + 128 * rank, n0 = (t / m_tiles) * BN;
+            const int m0 = (t % pb.m_tiles) * 256 + 128 * rank, n0 = (t / pb.m_tiles) * BN;
             const int row = m0 + q * 32 + lane;
-            const bool row_ok = row < M;
+            const bool row_ok = row < pb.M;
             ptx::mbar_wait(&tfull[acc], acc_phase);
             ptx::tc_fence_after();
             auto release = [&] {
@@ -613,7 +648,7 @@ __global__ void __maxnreg__(96)
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tempty[acc]), 0));
             };
-            if (g.kb1 < nk) {
+            if (use_sk && g.kb1 < nk) {
                 // ---- stream-K producer: f32 partial to this pair's workspace slot, then publish ----
                 float* dst = sk.ws + ((static_cast<size_t>(pair) * 2 + rank) * 128 + lr) * 256;
                 for (int sidx = half; sidx < BN / 32; sidx += 2) {
@@ -652,20 +687,20 @@ __global__ void __maxnreg__(96)
             for (int sidx = half; sidx < n_strips; sidx += 2) {
                 const int col0 = n0 + sidx * cw;
                 const uint32_t tcol = tmem_base + ((q * 32) << 16) + acc * BN + sidx * cw;
-                const int valid = row_ok ? min(cw, N - col0) : 0;
+                const int valid = row_ok ? min(cw, pb.N - col0) : 0;
                 // staging buffer reuse: the previous TMA store must have finished reading it
                 if (lane == 0) ptx::bulk_wait_read<0>();
                 __syncwarp();
                 const uint32_t rowa = ptx::smem_u32(stage_out) + lane * 128;
-                epilogue_strip(ep, tcol, row, col0, valid, rowa, lane, sidx + 2 >= n_strips, release,
+                epilogue_strip(ep_t, tcol, row, col0, valid, rowa, lane, sidx + 2 >= n_strips, release,
                                part0 ? part0 + sidx * cw : nullptr, part1 ? part1 + sidx * cw : nullptr);
                 ptx::fence_proxy_async_smem();
                 __syncwarp();
-                if (lane == 0 && col0 < N && m0 + q * 32 < M) {
-                    if (f32_out && ep.accumulate)
-                        ptx::tma_reduce_add_2d(&tmD, stage_out, col0, m0 + q * 32);
+                if (lane == 0 && col0 < pb.N && m0 + q * 32 < pb.M) {
+                    if (f32_out && ep_t.accumulate)
+                        ptx::tma_reduce_add_2d(td, stage_out, col0, m0 + q * 32);
                     else
-                        ptx::tma_store_2d(&tmD, stage_out, col0, m0 + q * 32);
+                        ptx::tma_store_2d(td, stage_out, col0, m0 + q * 32);
                     ptx::bulk_commit();
                 }
             }
@@ -739,23 +774,36 @@ SkWorkspace& sk_workspace(cudaStream_t st, int pairs) {
 }
 
 template <int BN, int A_MN, int B_MN>
-void launch2(const GemmArgs& g, cudaStream_t st) {
-    CUtensorMap ta = A_MN ? make_tma_2d(g.A, g.M, g.K, g.lda, BK, false) : make_tma_2d(g.A, g.K, g.M, g.lda, 128, false);
-    CUtensorMap tb = B_MN ? make_tma_2d(g.B, g.N, g.K, g.ldb, BK, false)
-                          : make_tma_2d(g.B, g.K, g.N, g.ldb, BN / 2, false);
-    const bool f32 = g.epilogue == GEMM_EPI_F32;
-    CUtensorMap td = make_tma_2d(g.D, g.N, g.M, g.ldd, 32, f32);
-    EpiArgs ep{static_cast<const __nv_bfloat16*>(g.aux), g.ldaux, static_cast<__nv_bfloat16*>(g.aux_out),
-               g.ldaux_out, g.epilogue, g.accumulate};
+void launch2(const GemmArgs& g, cudaStream_t st, const GemmArgs* second = nullptr) {
+    auto maps = [](const GemmArgs& a, CUtensorMap& ta, CUtensorMap& tb, CUtensorMap& td) {
+        ta = A_MN ? make_tma_2d(a.A, a.M, a.K, a.lda, BK, false) : make_tma_2d(a.A, a.K, a.M, a.lda, 128, false);
+        tb = B_MN ? make_tma_2d(a.B, a.N, a.K, a.ldb, BK, false) : make_tma_2d(a.B, a.K, a.N, a.ldb, BN / 2, false);
+        td = make_tma_2d(a.D, a.N, a.M, a.ldd, 32, a.epilogue == GEMM_EPI_F32);
+    };
+    auto epi = [](const GemmArgs& a) {
+        return EpiArgs{static_cast<const __nv_bfloat16*>(a.aux), a.ldaux, static_cast<__nv_bfloat16*>(a.aux_out),
+                       a.ldaux_out, a.epilogue, a.accumulate};
+    };
+    CUtensorMap ta, tb, td;
+    maps(g, ta, tb, td);
+    const EpiArgs ep = epi(g);
+    Second p2{};
+    if (second) {
+        maps(*second, p2.A, p2.B, p2.D);
+        p2.M = static_cast<int>(second->M);
+        p2.N = static_cast<int>(second->N);
+        p2.K = static_cast<int>(second->K);
+        p2.ep = epi(*second);
+    }
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(gemm2_kernel<BN, A_MN, B_MN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             Smem2<BN>::kBytes);
-        cudaFuncSetAttribute(gemm2_kernel<BN, A_MN, B_MN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             Smem2<BN>::kBytes);
+        for (auto* k : {gemm2_kernel<BN, A_MN, B_MN, false, false>, gemm2_kernel<BN, A_MN, B_MN, true, false>,
+                        gemm2_kernel<BN, A_MN, B_MN, false, true>})
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem2<BN>::kBytes);
         configured = true;
     }
-    const int tiles = static_cast<int>(((g.M + 255) / 256) * ((g.N + BN - 1) / BN));
+    int tiles = static_cast<int>(((g.M + 255) / 256) * ((g.N + BN - 1) / BN));
+    if (second) tiles += static_cast<int>(((second->M + 255) / 256) * ((second->N + BN - 1) / BN));
     const int nk = static_cast<int>((g.K + BK - 1) / BK);
     int pairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
     SkArgs sk{nullptr, nullptr, 0};
@@ -766,7 +814,7 @@ void launch2(const GemmArgs& g, cudaStream_t st) {
         const long long total = static_cast<long long>(tiles) * nk;
         const int waves = (tiles + all - 1) / all;
         const double eff = static_cast<double>(tiles) / (static_cast<double>(waves) * all);
-        const bool want = gemm_sk == 1 || (gemm_sk < 0 && eff < 0.92);
+        const bool want = !second && (gemm_sk == 1 || (gemm_sk < 0 && eff < 0.92));
         if (want && BN == 256 && total / all >= (nk + 1) / 2 && nk >= 2) {
             SkWorkspace& w = sk_workspace(st, all);
             sk = SkArgs{w.ws, w.flags, ++w.epoch};
@@ -787,12 +835,13 @@ void launch2(const GemmArgs& g, cudaStream_t st) {
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = gemm_pdl ? 2 : 1;
-    if (sk.ws)
-        cudaLaunchKernelEx(&cfg, gemm2_kernel<BN, A_MN, B_MN, true>, ta, tb, td, static_cast<int>(g.M),
-                           static_cast<int>(g.N), static_cast<int>(g.K), ep, sk);
+    const int M = static_cast<int>(g.M), N = static_cast<int>(g.N), K = static_cast<int>(g.K);
+    if (second)
+        cudaLaunchKernelEx(&cfg, gemm2_kernel<BN, A_MN, B_MN, false, true>, ta, tb, td, M, N, K, ep, sk, p2);
+    else if (sk.ws)
+        cudaLaunchKernelEx(&cfg, gemm2_kernel<BN, A_MN, B_MN, true, false>, ta, tb, td, M, N, K, ep, sk, p2);
     else
-        cudaLaunchKernelEx(&cfg, gemm2_kernel<BN, A_MN, B_MN, false>, ta, tb, td, static_cast<int>(g.M),
-                           static_cast<int>(g.N), static_cast<int>(g.K), ep, sk);
+        cudaLaunchKernelEx(&cfg, gemm2_kernel<BN, A_MN, B_MN, false, false>, ta, tb, td, M, N, K, ep, sk, p2);
 }
 
 }  // namespace
@@ -801,6 +850,7 @@ int gemm_sk = 0;     // stream-K for the 2-CTA kernel: 0 off (default), 1 forced
 int gemm_mode = -1;  // -1 auto, 1 force 1-CTA, 2 force 2-CTA (benchmarks / tests)
 int gemm_pdl = 0;    // programmatic dependent launch (BFPP_GEMM_PDL=1): measured no gain in-step (optimizer co-running)
 int gemm_bn2 = 0;    // 2-CTA pair-tile width: 0 / 256 default, 128 opt-in (BFPP_GEMM_BN2; tests)
+int gemm_pair = 1;   // grouped launches of independent GEMM pairs (BFPP_GEMM_PAIR=0: two launches)
 
 static bool env_read = false;
 
@@ -811,14 +861,18 @@ void gemm_bf16_configure(int mode, int bn2, int stream_k) {
     gemm_sk = stream_k;
 }
 
+static void read_env() {
+    if (env_read) return;
+    if (const char* e = getenv("BFPP_GEMM_MODE")) gemm_mode = atoi(e);
+    if (const char* e = getenv("BFPP_GEMM_BN2")) gemm_bn2 = atoi(e);
+    if (const char* e = getenv("BFPP_GEMM_PDL")) gemm_pdl = atoi(e);
+    if (const char* e = getenv("BFPP_GEMM_SK")) gemm_sk = atoi(e);
+    if (const char* e = getenv("BFPP_GEMM_PAIR")) gemm_pair = atoi(e);
+    env_read = true;
+}
+
 void gemm_bf16(const GemmArgs& g, cudaStream_t st) {
-    if (!env_read) {
-        if (const char* e = getenv("BFPP_GEMM_MODE")) gemm_mode = atoi(e);
-        if (const char* e = getenv("BFPP_GEMM_BN2")) gemm_bn2 = atoi(e);
-        if (const char* e = getenv("BFPP_GEMM_PDL")) gemm_pdl = atoi(e);
-        if (const char* e = getenv("BFPP_GEMM_SK")) gemm_sk = atoi(e);
-        env_read = true;
-    }
+    read_env();
     if (g.M <= 0 || g.N <= 0 || g.K <= 0) throw std::runtime_error("gemm: empty problem");
     if (g.K % 8 || g.lda % 8 || g.ldb % 8 || g.ldd % 8) throw std::runtime_error("gemm: K and leading dims must be multiples of 8");
     const bool small_n = g.N <= 128;
@@ -853,6 +907,31 @@ void gemm_bf16(const GemmArgs& g, cudaStream_t st) {
         BFPP_GEMM_CASE(256, 1, 1)
     }
 #undef BFPP_GEMM_CASE
+}
+
+bool gemm_pairable(const GemmArgs& a, const GemmArgs& b) {
+    read_env();
+    const bool same = a.a_mn_major == b.a_mn_major && a.b_mn_major == b.b_mn_major;
+    return gemm_pair && same && gemm_mode != 1 && gemm_bn2 != 128 && a.M >= 256 && a.N >= 256 && b.M >= 256 &&
+           b.N >= 256;
+}
+
+void gemm_bf16_pair(const GemmArgs& a, const GemmArgs& b, cudaStream_t st) {
+    if (!gemm_pairable(a, b)) {
+        gemm_bf16(a, st);
+        gemm_bf16(b, st);
+        return;
+    }
+    for (const GemmArgs* g : {&a, &b}) {
+        if (g->M <= 0 || g->N <= 0 || g->K <= 0) throw std::runtime_error("gemm: empty problem");
+        if (g->K % 8 || g->lda % 8 || g->ldb % 8 || g->ldd % 8)
+            throw std::runtime_error("gemm: K and leading dims must be multiples of 8");
+    }
+    const int am = a.a_mn_major ? 1 : 0, bm = a.b_mn_major ? 1 : 0;
+    if (am == 0 && bm == 0) return launch2<256, 0, 0>(a, st, &b);
+    if (am == 0 && bm == 1) return launch2<256, 0, 1>(a, st, &b);
+    if (am == 1 && bm == 0) return launch2<256, 1, 0>(a, st, &b);
+    return launch2<256, 1, 1>(a, st, &b);
 }
 
 }  // namespace bfpp

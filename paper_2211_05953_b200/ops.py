@@ -51,6 +51,32 @@ def gemm(a: torch.Tensor, b: torch.Tensor, *, a_mn_major=False, b_mn_major=False
     _check(_nat.lib().bfpp_gemm_bf16(C.byref(args), _stream()))
     return out
 
+def _gemm_args(a, b, a_mn_major, b_mn_major, out, epilogue, aux, aux_out, accumulate):
+    assert a.dtype == torch.bfloat16 and b.dtype == torch.bfloat16
+    assert a.stride(1) == 1 and b.stride(1) == 1
+    M, K = (a.shape[1], a.shape[0]) if a_mn_major else a.shape
+    N = b.shape[1] if b_mn_major else b.shape[0]
+    assert (b.shape[0] if b_mn_major else b.shape[1]) == K
+    if out is None:
+        out = torch.empty(M, N, device=a.device,
+                          dtype=torch.float32 if epilogue == EPI_F32 else torch.bfloat16)
+    args = GemmArgsC(M, N, K, a.data_ptr(), a.stride(0), int(a_mn_major), b.data_ptr(), b.stride(0),
+                     int(b_mn_major), out.data_ptr(), out.stride(0),
+                     _ptr(aux), aux.stride(0) if aux is not None else 0,
+                     _ptr(aux_out), aux_out.stride(0) if aux_out is not None else 0, epilogue, int(accumulate))
+    return args, out
+
+
+def gemm_pair(first: dict, second: dict):
+    """Two independent GEMMs in one grouped launch; each dict holds gemm()'s arguments
+    (a, b, and optionally a_mn_major, b_mn_major, out, epilogue, aux, aux_out, accumulate)."""
+    def unpack(d):
+        return _gemm_args(d["a"], d["b"], d.get("a_mn_major", False), d.get("b_mn_major", False), d.get("out"),
+                          d.get("epilogue", EPI_BF16), d.get("aux"), d.get("aux_out"), d.get("accumulate", False))
+    (x, ox), (y, oy) = unpack(first), unpack(second)
+    _check(_nat.lib().bfpp_gemm_bf16_pair(C.byref(x), C.byref(y), _stream()))
+    return ox, oy
+
 
 def gemm_config(mode: int = -1, bn2: int = 0, stream_k: int = -1):
     """Process-wide GEMM variant selection (tests / benchmarks): mode -1 auto, 1 one-CTA, 2 two-CTA;

@@ -20,9 +20,9 @@ def _close(got, ref, rtol):
     assert err <= rtol * scale, (err, scale)
 
 
-# (mode, bn2, stream_k): auto; one-CTA tiles; two-CTA 256x128 and 256x256 pair tiles (forced),
+# (mode, bn2, stream_k): defaults (stream-K off); one-CTA tiles; two-CTA 256x128 and 256x256 pair tiles (forced),
 # data-parallel and stream-K (forced: a k-split wherever every pair gets >= half a tile)
-VARIANTS = [(-1, 0, -1), (1, 0, 0), (2, 128, 0), (2, 256, 0), (2, 256, 1)]
+VARIANTS = [(-1, 0, 0), (-1, 0, -1), (1, 0, 0), (2, 128, 0), (2, 256, 0), (2, 256, 1)]
 
 
 @pytest.fixture(params=VARIANTS, ids=lambda v: f"mode{v[0]}-bn{v[1]}-sk{v[2]}")
@@ -30,7 +30,7 @@ def variant(request, cuda_device):
     ops = _ops()
     ops.gemm_config(*request.param)
     yield request.param
-    ops.gemm_config(-1, 0, -1)
+    ops.gemm_config(-1, 0, 0)  # the library defaults
 
 
 @pytest.mark.parametrize("a_mn", [False, True])
@@ -89,3 +89,33 @@ def test_gemm_strided_views(cuda_device):
     view = X[:, K:2 * K]
     out = ops.gemm(view, W)
     _close(out, view.float() @ W.float().t(), 1e-2)
+
+
+@pytest.mark.parametrize("shapes", [((512, 768, 256), (768, 512, 384)), ((2048, 2048, 512), (6144, 2048, 512)),
+                                    ((256, 8192, 128), (8192, 256, 128))])
+@pytest.mark.parametrize("epi", ["f32_acc", "bf16"])
+def test_gemm_pair_matches_separate_launches(cuda_device, shapes, epi):
+    """Grouped pair launch (one tile space) == two ordinary launches, bit for bit (same per-tile math)."""
+    ops = _ops()
+    g = torch.Generator(device="cuda").manual_seed(11)
+    probs = []
+    for M, N, K in shapes:  # weight-gradient form: A = dY^T, B = X^T (both MN-major)
+        A = torch.randn(K, M, device="cuda", generator=g).bfloat16()
+        B = torch.randn(K, N, device="cuda", generator=g).bfloat16()
+        probs.append((A, B, M, N))
+    kw = dict(a_mn_major=True, b_mn_major=True)
+    if epi == "f32_acc":
+        kw.update(epilogue=ops.EPI_F32, accumulate=True)
+        base = [torch.randn(M, N, device="cuda", generator=g) for _, _, M, N in probs]
+    else:
+        base = [torch.zeros(M, N, device="cuda", dtype=torch.bfloat16) for _, _, M, N in probs]
+    sep = [b.clone() for b in base]
+    grp = [b.clone() for b in base]
+    for (A, B, _, _), o in zip(probs, sep):
+        ops.gemm(A, B, out=o, **kw)
+    ops.gemm_pair(dict(a=probs[0][0], b=probs[0][1], out=grp[0], **kw), dict(a=probs[1][0], b=probs[1][1], out=grp[1], **kw))
+    torch.cuda.synchronize()
+    for s_, g_, (A, B, _, _), b in zip(sep, grp, probs, base):
+        assert torch.equal(s_, g_)
+        ref = A.float().t() @ B.float() + (b.float() if epi == "f32_acc" else 0)
+        _close(g_, ref, 1e-4 if epi == "f32_acc" else 1e-2)
