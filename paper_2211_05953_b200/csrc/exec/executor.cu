@@ -1,6 +1,7 @@
-// Per-rank executor: runs one pipeline rank's slice of a bfpp TaskGraph on a
-// B200 with the sm_100a stage kernels, NCCL point-to-point hand-offs and
-// fully-sharded data-parallel traffic. See executor.hpp and DESIGN.md.
+// Per-rank executor: runs one pipeline rank's slice of a bfpp TaskGraph on a B200 with the
+// sm_100a stage kernels, copy-engine peer copies over NVLink for the pipeline hand-offs (CUDA IPC
+// + stream memory operations) and NCCL for the (fully sharded) data-parallel traffic.
+// See executor.hpp and DESIGN.md §3.
 #include "executor.hpp"
 
 #include <cuda.h>
@@ -9,7 +10,6 @@
 
 #include <algorithm>
 #include <chrono>
-#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -20,6 +20,7 @@
 #include <set>
 #include <stdexcept>
 #include <string>
+#include <thread>
 
 #include "../kernels/gemm.hpp"
 #include "../kernels/kernels.hpp"
