@@ -2,10 +2,11 @@
 // simulate.cpp:41-158, replaced by real execution).
 //
 // One process per GPU. Lanes become CUDA streams: Compute -> compute stream
-// (program order), DpNet -> DP stream (priority order: NCCL all-gather /
-// reduce-scatter / all-reduce + sharded Adam), PpNet -> one stream and one
-// 2-rank NCCL communicator per directed pipeline edge (send in producer order,
-// receive in consumer order). Cross-stream dependencies are CUDA events.
+// (program order), DpNet -> low-priority DP stream (priority order: NCCL all-gather /
+// reduce-scatter / all-reduce + sharded Adam, per layer segment), PpNet -> send / receive
+// streams per direction (copy-engine peer copies into the receiver's CUDA-IPC-mapped slots,
+// flag writes / waits with stream memory operations). Cross-stream dependencies are CUDA
+// events; the per-rank plan (stream, waits, enqueue order) is plan_rank (plan.hpp).
 #pragma once
 
 #include <cuda_runtime.h>
