@@ -88,6 +88,7 @@ struct EpiArgs {
     int64_t ldaux_out;
     int epi;
     int accumulate;
+    int n_fast = 0;  // 2-CTA kernel: tile raster with N fastest (A is reused by the pairs of a wave)
 };
 
 // Stream-K (2-CTA kernel; opt-in, BFPP_GEMM_SK=1 / bfpp_gemm_config): correct and tested, but
@@ -505,10 +506,20 @@ __global__ void __maxnreg__(96)
         const CUtensorMap *A, *B, *D;
         int M, N, nk, m_tiles, t;
         const EpiArgs* ep;
+        int mi, ni;  // tile coordinates (raster: M fastest, or N fastest when A is the big operand)
     };
     auto prob = [&](int t) -> Prob {
-        if (GROUP && t >= tiles0) return {&p2.A, &p2.B, &p2.D, p2.M, p2.N, nk1, m_tiles1, t - tiles0, &p2.ep};
-        return {&tmA, &tmB, &tmD, M, N, nk0, m_tiles0, t, &ep};
+        Prob p = (GROUP && t >= tiles0) ? Prob{&p2.A, &p2.B, &p2.D, p2.M, p2.N, nk1, m_tiles1, t - tiles0, &p2.ep, 0, 0}
+                                        : Prob{&tmA, &tmB, &tmD, M, N, nk0, m_tiles0, t, &ep, 0, 0};
+        if (p.ep->n_fast) {
+            const int nt = (p.N + BN - 1) / BN;
+            p.mi = p.t / nt;
+            p.ni = p.t % nt;
+        } else {
+            p.mi = p.t % p.m_tiles;
+            p.ni = p.t / p.m_tiles;
+        }
+        return p;
     };
 
     if (warp == 0 && lane == 0) {
@@ -550,7 +561,7 @@ __global__ void __maxnreg__(96)
                 const Prob pb = prob(g.tile);
                 if (!use_sk) g.kb1 = pb.nk;
                 const int t = pb.t;
-                const int m0 = (t % pb.m_tiles) * 256 + 128 * rank, n0 = (t / pb.m_tiles) * BN + (BN / 2) * rank;
+                const int m0 = pb.mi * 256 + 128 * rank, n0 = pb.ni * BN + (BN / 2) * rank;
                 for (int kb = g.kb0; kb < g.kb1; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* sa = smem + stage * S::kStageBytes;
@@ -637,7 +648,7 @@ __global__ void __maxnreg__(96)
             const int t = pb.t;
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
-            const int m0 = (t % pb.m_tiles) * 256 + 128 * rank, n0 = (t / pb.m_tiles) * BN;
+            const int m0 = pb.mi * 256 + 128 * rank, n0 = pb.ni * BN;
             const int row = m0 + q * 32 + lane;
             const bool row_ok = row < pb.M;
             ptx::mbar_wait(&tfull[acc], acc_phase);
@@ -781,8 +792,11 @@ void launch2(const GemmArgs& g, cudaStream_t st, const GemmArgs* second = nullpt
         td = make_tma_2d(a.D, a.N, a.M, a.ldd, 32, a.epilogue == GEMM_EPI_F32);
     };
     auto epi = [](const GemmArgs& a) {
+        // N-fastest raster when A does not stay in L2 across the N passes (e.g. the LM-head weight
+        // gradient, A = dlogits^T: 206 MB, read once instead of once per N tile)
+        const bool n_fast = a.M * a.K * 2 > (int64_t(64) << 20) && a.N > BN;
         return EpiArgs{static_cast<const __nv_bfloat16*>(a.aux), a.ldaux, static_cast<__nv_bfloat16*>(a.aux_out),
-                       a.ldaux_out, a.epilogue, a.accumulate};
+                       a.ldaux_out, a.epilogue, a.accumulate, n_fast ? 1 : 0};
     };
     CUtensorMap ta, tb, td;
     maps(g, ta, tb, td);

@@ -37,7 +37,7 @@ def variant(request, cuda_device):
 @pytest.mark.parametrize("b_mn", [False, True])
 @pytest.mark.parametrize("shape", [(256, 512, 128), (128, 256, 64), (384, 768, 320), (64, 1000, 128),
                                    (2048, 2048, 2048), (200, 136, 72), (512, 8192, 256), (2048, 8192, 2048),
-                                   (768, 1280, 4096)])
+                                   (768, 1280, 4096), (8448, 512, 4096)])  # last: N-fastest raster (A > 64 MB)
 def test_gemm_layouts(variant, a_mn, b_mn, shape):
     ops = _ops()
     M, N, K = shape
