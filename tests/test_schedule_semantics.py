@@ -208,3 +208,14 @@ def test_throughput_eq11():
     pp = ps.throughput(m, c, tl, cl)
     assert pp.throughput == pytest.approx(ps.compute_per_gpu(m, c) / tl.makespan)
     assert pp.beta == 2.0
+
+
+def test_param_count_and_compute_per_gpu_closed_forms():
+    """param_count = 12 L h^2 (types.cpp:132-134); compute_per_gpu = Eq. 11 (types.cpp:136-146):
+    s * 96 * n_mb * s_mb * L * h * (h + s/6 + V/(16 L)) / (n_pp * n_tp)."""
+    m = ps.ModelSpec(n_layers=24, s_hidden=2048, n_heads=16, s_seq=2048, s_voc=50304)
+    assert ps.param_count(m) == 12 * 24 * 2048 * 2048
+    c = ps.ParallelConfig(n_dp=1, n_pp=2, n_loop=4, n_mb=2, schedule=S.BreadthFirst)
+    L, h, s, V = 24, 2048.0, 2048.0, 50304.0
+    want = s * 96 * 2 * 1 * L * h * (h + s / 6 + V / (16 * L)) / 2
+    assert ps.compute_per_gpu(m, c) == pytest.approx(want, rel=1e-12)
