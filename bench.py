@@ -340,6 +340,10 @@ def main():
             sp = CB.reference_schedule_path(mspec._c(), config._c(), NN.TimingModelC(1.0, 2.0, 0.0, 0.0, 0.0, 0.0))
             if sp:
                 cpu["reference_schedule_path"] = sp
+            # the reference's own CPU search (rank_configs, simulate scoring) on all host threads
+            ss = CB.reference_search_path(mspec._c(), 8, os.cpu_count() or 1)
+            if ss:
+                cpu["reference_search_path"] = ss
         except Exception as exc:  # the baseline must never break the bench line
             cpu = {"value": None, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
                    "sample": f"failed: {exc}"}

@@ -79,6 +79,24 @@ def tokens_per_sec(cfg, head_tokens: int = 256):
     return cfg.s_seq / per_seq, sample, per_seq
 
 
+def reference_search_path(model_spec_c, n_gpu: int, threads: int):
+    """Wall seconds of the reference's configuration search in simulate mode (enumerate_configs +
+    rank_configs, search.cpp:136-188) on `threads` host threads."""
+    lib = os.path.join(HERE, "_ref", "libpipesim_ref.so")
+    if not os.path.exists(lib):
+        return None
+    L = C.CDLL(lib)
+    if not hasattr(L, "ref_time_rank_configs"):
+        return None
+    L.ref_time_rank_configs.restype = C.c_int
+    sec, ne, nr = C.c_double(), C.c_int64(), C.c_int64()
+    st = L.ref_time_rank_configs(C.byref(model_spec_c), n_gpu, threads, C.byref(sec), C.byref(ne), C.byref(nr))
+    if st != 0:
+        return None
+    return {"seconds": sec.value, "configs_enumerated": ne.value, "configs_ranked": nr.value, "threads": threads,
+            "scoring": "simulate"}
+
+
 def reference_schedule_path(model_spec_c, config_c, timing_c, reps: int = 100):
     """Seconds per (place_stages + build_tasks) and per simulate() of the compiled reference."""
     lib = os.path.join(HERE, "_ref", "libpipesim_ref.so")

@@ -1,7 +1,7 @@
 // TEST INFRASTRUCTURE ONLY — the checker, never the product.
 //
 // extern "C" shim over the UNMODIFIED reference schedule/simulator sources
-// (/root/reference/proj/src/{types,memory,network,perf,schedule,simulate,report}.cpp),
+// (/root/reference/proj/src/{types,memory,network,perf,schedule,simulate,report,search}.cpp),
 // compiled by oracle/Makefile into oracle/_ref/libpipesim_ref.so. It exposes the
 // reference's build_tasks / simulate results (including Task::priority, which
 // the reference's own Python binding omits, bindings/module.cpp:185-193) with
@@ -16,6 +16,7 @@
 #include "../include/bfpp.h"
 #include "pipesim/perf.hpp"
 #include "pipesim/report.hpp"
+#include "pipesim/search.hpp"
 #include "pipesim/schedule.hpp"
 #include "pipesim/simulate.hpp"
 
@@ -219,6 +220,43 @@ int ref_time_schedule_path(const bfpp_model_spec* m, const bfpp_parallel_config*
         }
         *build_s = b / reps;
         *sim_s = s / reps;
+    });
+}
+
+// The reference's configuration search in simulate mode (search.cpp:136-188) over a GPT model on
+// one node of n_gpu B200s: enumerate_configs + rank_configs(Scoring::Simulate) with `threads`
+// workers, timed wall-clock. Returns the number of enumerated / ranked configurations.
+int ref_time_rank_configs(const bfpp_model_spec* m, int64_t n_gpu, int threads, double* seconds,
+                          int64_t* n_enumerated, int64_t* n_ranked) {
+    return guard([&] {
+        ModelSpec ms = model_of(m);
+        ClusterSpec cl;
+        cl.n_node = 1;
+        cl.s_node = n_gpu;
+        cl.peak_flops = 2.25e15;
+        cl.bw_intra = 9.0e11;
+        cl.bw_inter = 5.0e10;
+        cl.pp_latency = 5e-6;
+        cl.mem_capacity = 180e9;
+        SearchSpace sp;
+        sp.schedules = {Schedule::NoPipeline, Schedule::GPipe, Schedule::OneFOneB, Schedule::DepthFirst,
+                        Schedule::BreadthFirst};
+        sp.n_pp_choices = {1, 2, 4, 8};
+        sp.n_tp_choices = {1};
+        sp.s_mb_choices = {1, 2};
+        sp.n_mb_choices = {1, 2, 4, 8, 16, 32};
+        sp.n_loop_choices = {1, 2, 4, 8};
+        sp.dp_variants = {DpVariant::DP0, DpVariant::DP_PS, DpVariant::DP_FS};
+        sp.batch_sizes = {8, 16, 32, 64};
+        sp.scoring = Scoring::Simulate;
+        SearchOptions opts;
+        opts.threads = threads;
+        auto t0 = std::chrono::steady_clock::now();
+        const std::vector<ParallelConfig> all = enumerate_configs(sp, ms, cl);
+        const std::vector<RankedConfig> ranked = rank_configs(all, ms, cl, Scoring::Simulate, opts);
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        *n_enumerated = static_cast<int64_t>(all.size());
+        *n_ranked = static_cast<int64_t>(ranked.size());
     });
 }
 
