@@ -157,6 +157,12 @@ int bfpp_gemm_bf16_pair(const bfpp_gemm_args* a, const bfpp_gemm_args* b, void* 
  * stream_k = 0 off (default), 1 forced, -1 auto (only when the last tile wave leaves pairs idle).
  * Defaults come from BFPP_GEMM_MODE / BFPP_GEMM_BN2 / BFPP_GEMM_SK. */
 int bfpp_gemm_config(int32_t mode, int32_t bn2, int32_t stream_k);
+/* Process-wide launch counters per kernel variant (0 1-CTA GEMM, 1 2-CTA GEMM, 2 grouped 2-CTA
+ * pair, 3 N-fastest raster, 4 stream-K, 5 attention fwd with > 1 head and > 1 query block,
+ * 6 attention bwd with > 1 head and > 1 key block); -1 for an unknown variant. Host-side, no GPU
+ * access: used by the parity tests to show which production kernels a composed step ran. */
+int64_t bfpp_kernel_variant_count(int32_t variant);
+void bfpp_kernel_variant_reset(void);
 
 /* causal multi-head attention, head_dim 128 (flash-style; never materialises T x T).
  * qkv [B*S][3*H*128] bf16 (Q | K | V column blocks), o [B*S][H*128] bf16,
@@ -264,10 +270,12 @@ int bfpp_exec_timeline(const bfpp_exec* e, double* start, double* end);
  * (1 send, 2 first reduce unit, 4 last reduce unit, 8 optimizer after, 16 first gradient
  * contribution of its unit, 32 last optimizer update of the step, 64 backward completing its
  * stage's last reduction unit, 128 ... whose reduction is also the first unit), DP_FS weight slot and the
- * cross-stream waits (CSR). Call with cap = 0 to get *n_tasks and *n_waits. */
-int bfpp_plan_rank(const bfpp_graph* g, int64_t pp_rank, int64_t n_dp, int64_t cap, int32_t* ids, int32_t* streams,
-                   int32_t* flags, int32_t* slots, int32_t* wait_offsets, int32_t* wait_ids, int64_t* n_tasks,
-                   int64_t* n_waits);
+ * cross-stream waits (CSR). Two-phase sizing: call with cap = 0 to get *n_tasks and *n_waits,
+ * then pass cap >= n_tasks (ids, streams, flags, slots: cap entries; wait_offsets: cap + 1) and
+ * wait_cap >= n_waits (wait_ids); smaller capacities fail with status 2 and write nothing. */
+int bfpp_plan_rank(const bfpp_graph* g, int64_t pp_rank, int64_t n_dp, int64_t cap, int64_t wait_cap, int32_t* ids,
+                   int32_t* streams, int32_t* flags, int32_t* slots, int32_t* wait_offsets, int32_t* wait_ids,
+                   int64_t* n_tasks, int64_t* n_waits);
 
 /* toggles per-task timeline events and per-kernel profiling for subsequent steps */
 int bfpp_exec_set_flags(bfpp_exec* e, int32_t record_timeline, int32_t profile_kernels);

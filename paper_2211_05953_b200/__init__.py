@@ -5,9 +5,11 @@
 """
 import os
 
-# The executor runs 7 streams plus NCCL's; with fewer hardware work queues than streams, CUDA
-# maps streams onto shared queues and a NCCL receive waiting for its peer can block an unrelated
-# send queued behind it -> cross-GPU deadlock. Must be set before the CUDA context exists.
+# The executor runs 7 streams; with fewer hardware work queues than streams, CUDA maps streams
+# onto shared queues and a receive stream blocked in cuStreamWaitValue32 (waiting for its peer's
+# copy) can block an unrelated send queued behind it -> cross-GPU deadlock. Must be set before the
+# CUDA context exists: import this package before anything initialises CUDA. The executor refuses
+# pipeline configs (n_pp >= 2) when a smaller value is already set.
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # one hardware queue per executor stream (see executor.py)
 
 from . import pipesim  # noqa: F401

@@ -83,7 +83,7 @@ _PROTOS = {
     "bfpp_chrome_trace_json": (C.c_int, [_P, _P, C.c_char_p, C.c_int64, _I64P]),
     "bfpp_gantt_svg": (C.c_int, [_P, _P, C.c_char_p, C.c_int64, _I64P]),
     "bfpp_measured_timing_model": (C.c_int, [_P, _P, C.POINTER(TimingModelC)]),
-    "bfpp_plan_rank": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64] + [_I32P] * 6 + [_I64P, _I64P]),
+    "bfpp_plan_rank": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64, C.c_int64] + [_I32P] * 6 + [_I64P, _I64P]),
 }
 
 _lib = None

@@ -111,9 +111,9 @@ int bfpp_exec_timeline(const bfpp_exec* e, double* start, double* end) {
     return guarded([&] { e->x->timeline(start, end); });
 }
 
-int bfpp_plan_rank(const bfpp_graph* g, int64_t pp_rank, int64_t n_dp, int64_t cap, int32_t* ids, int32_t* streams,
-                   int32_t* flags, int32_t* slots, int32_t* wait_offsets, int32_t* wait_ids, int64_t* n_tasks,
-                   int64_t* n_waits) {
+int bfpp_plan_rank(const bfpp_graph* g, int64_t pp_rank, int64_t n_dp, int64_t cap, int64_t wait_cap, int32_t* ids,
+                   int32_t* streams, int32_t* flags, int32_t* slots, int32_t* wait_offsets, int32_t* wait_ids,
+                   int64_t* n_tasks, int64_t* n_waits) {
     return guarded([&] {
         if (pp_rank < 0 || pp_rank >= g->g.n_devices) throw SpecError("plan: pipeline rank out of range");
         const std::vector<PlanTask> plan = plan_rank(g->g, pp_rank, n_dp);
@@ -122,7 +122,8 @@ int bfpp_plan_rank(const bfpp_graph* g, int64_t pp_rank, int64_t n_dp, int64_t c
         *n_tasks = static_cast<int64_t>(plan.size());
         *n_waits = nw;
         if (cap == 0) return;
-        if (cap < static_cast<int64_t>(plan.size())) throw SpecError("plan: output buffer too small");
+        if (cap < static_cast<int64_t>(plan.size())) throw SpecError("plan: task arrays smaller than n_tasks");
+        if (wait_cap < nw) throw SpecError("plan: wait_ids smaller than n_waits");
         int32_t k = 0;
         for (size_t i = 0; i < plan.size(); ++i) {
             const PlanTask& p = plan[i];

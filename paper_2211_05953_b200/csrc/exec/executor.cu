@@ -331,6 +331,19 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
     for (i64 s = 0; s < pl_.n_stage; ++s)
         layouts_.push_back(make_stage_layout(m_, s, pl_.n_stage, pl_.layers_per_stage, c_.n_dp));
 
+    // The pipeline receive streams block in cuStreamWaitValue32 until a peer's copy lands; a send
+    // stream that shares their hardware queue would wait behind them and the ring would hang.
+    // CUDA maps streams onto CUDA_DEVICE_MAX_CONNECTIONS queues (default 8); the package sets 32
+    // before CUDA initialises, but a user value (1 is common in Megatron setups) wins.
+    if (p_ >= 2) {
+        const char* e = getenv("CUDA_DEVICE_MAX_CONNECTIONS");
+        const int conns = e ? atoi(e) : 8;
+        if (conns < S_N)
+            throw SpecError("executor: CUDA_DEVICE_MAX_CONNECTIONS=" + std::to_string(conns) +
+                            " gives the executor's " + std::to_string(S_N) +
+                            " streams fewer hardware queues than streams; pipeline hand-offs (n_pp >= 2) can "
+                            "deadlock. Set it to >= 32 before CUDA initialises (import the package first).");
+    }
     Impl& I = *impl_;
     I.dev = o.device;
     if (const char* e = getenv("BFPP_WGRAD_STREAM")) I.wgrad_stream = atoi(e) != 0;

@@ -282,6 +282,7 @@ void attention_fwd_tc(const void* qkv, void* o, float* lse, int batch, int seq, 
     const int64_t T = static_cast<int64_t>(batch) * seq, h3 = 3LL * heads * head_dim;
     const CUtensorMap tm = make_tma_2d(qkv, h3, T, h3, 128, false);
     dim3 grid(heads, (seq + BQ - 1) / BQ, batch);
+    if (heads > 1 && seq > BQ) count_variant(KV_ATTN_FWD_MULTI);
     const float scale_log2 = kLog2e / sqrtf(static_cast<float>(head_dim));
     attn_fwd_tc_kernel<<<grid, 192, FwdSmem::kBytes, st>>>(tm, static_cast<__nv_bfloat16*>(o), lse, seq, heads,
                                                            scale_log2);
@@ -562,6 +563,7 @@ void attention_bwd_tc(const void* qkv, const void* dout, const float* lse, const
     const CUtensorMap tq = make_tma_2d(qkv, 3 * HD, T, 3 * HD, 128, false);
     const CUtensorMap to = make_tma_2d(dout, HD, T, HD, 128, false);
     dim3 grid(heads, (seq + BKV - 1) / BKV, batch);
+    if (heads > 1 && seq > BKV) count_variant(KV_ATTN_BWD_MULTI);
     const float scale = 1.f / sqrtf(static_cast<float>(head_dim));
     attn_bwd_tc_kernel<<<grid, 192, BwdSmem::kBytes, st>>>(tq, to, lse, delta, dq_acc,
                                                            static_cast<__nv_bfloat16*>(dqkv), seq, heads, scale,

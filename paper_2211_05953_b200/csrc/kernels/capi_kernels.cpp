@@ -1,6 +1,7 @@
 // extern "C" entry points of the device kernels (include/bfpp.h, kernel section).
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <stdexcept>
 #include <string>
 
@@ -12,6 +13,13 @@
 using namespace bfpp;
 
 namespace {
+std::atomic<int64_t> g_variant_count[KV_N];
+}  // namespace
+void bfpp::count_variant(int v) {
+    if (v >= 0 && v < KV_N) g_variant_count[v].fetch_add(1, std::memory_order_relaxed);
+}
+
+namespace {
 void check_launch() {
     cudaError_t e = cudaPeekAtLastError();
     if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA launch failed: ") + cudaGetErrorString(e));
@@ -19,6 +27,13 @@ void check_launch() {
 }  // namespace
 
 extern "C" {
+
+int64_t bfpp_kernel_variant_count(int32_t v) {
+    return v >= 0 && v < KV_N ? g_variant_count[v].load(std::memory_order_relaxed) : -1;
+}
+void bfpp_kernel_variant_reset(void) {
+    for (auto& c : g_variant_count) c.store(0, std::memory_order_relaxed);
+}
 
 int bfpp_gemm_config(int32_t mode, int32_t bn2, int32_t stream_k) {
     return guarded([&] {

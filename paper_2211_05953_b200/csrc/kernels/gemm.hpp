@@ -44,6 +44,20 @@ extern int gemm_bn2;   // 2-CTA pair-tile width: 0 default (256), 128 opt-in
 extern int gemm_pdl;   // programmatic dependent launch of the GEMM kernels (default 0, BFPP_GEMM_PDL=1)
 extern int gemm_sk;    // stream-K in the 2-CTA kernel: -1 auto, 0 off, 1 forced (BFPP_GEMM_SK)
 
+// Host-side launch counters per kernel variant (process-wide, reset by bfpp_kernel_variant_reset):
+// lets the composed-step parity tests assert which production paths actually ran.
+enum KernelVariant : int {
+    KV_GEMM_1CTA = 0,     // gemm_kernel (128 x BN tiles)
+    KV_GEMM_2CTA,         // gemm2_kernel, one problem (256 x 256 cta_group::2 tiles)
+    KV_GEMM_2CTA_PAIR,    // gemm2_kernel, two problems in one grouped launch
+    KV_GEMM_2CTA_NFAST,   // gemm2 launch with the N-fastest tile raster
+    KV_GEMM_2CTA_STREAMK, // gemm2 launch with stream-K ranges
+    KV_ATTN_FWD_MULTI,    // attention forward with > 1 head and > 1 query block
+    KV_ATTN_BWD_MULTI,    // attention backward with > 1 head and > 1 key block
+    KV_N
+};
+void count_variant(int v);
+
 // 2-D TMA descriptor over a row-major [rows][ld] matrix (bf16, or f32 if `f32`) with `inner`
 // valid columns; box = {128 bytes of the inner dimension, box_rows}, SWIZZLE_128B, OOB -> 0.
 CUtensorMap make_tma_2d(const void* ptr, int64_t inner, int64_t rows, int64_t ld, int box_rows, bool f32);

@@ -749,6 +749,7 @@ void launch(const GemmArgs& g, cudaStream_t st) {
     }
     const int tiles = static_cast<int>(((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN));
     const int grid = tiles < num_sms() ? tiles : num_sms();
+    count_variant(KV_GEMM_1CTA);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
@@ -850,6 +851,9 @@ void launch2(const GemmArgs& g, cudaStream_t st, const GemmArgs* second = nullpt
     cfg.attrs = attr;
     cfg.numAttrs = gemm_pdl ? 2 : 1;
     const int M = static_cast<int>(g.M), N = static_cast<int>(g.N), K = static_cast<int>(g.K);
+    count_variant(second ? KV_GEMM_2CTA_PAIR : KV_GEMM_2CTA);
+    if (ep.n_fast || (second && p2.ep.n_fast)) count_variant(KV_GEMM_2CTA_NFAST);
+    if (sk.ws) count_variant(KV_GEMM_2CTA_STREAMK);
     if (second)
         cudaLaunchKernelEx(&cfg, gemm2_kernel<BN, A_MN, B_MN, false, true>, ta, tb, td, M, N, K, ep, sk, p2);
     else if (sk.ws)

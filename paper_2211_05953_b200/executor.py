@@ -166,6 +166,20 @@ class Executor:
             pass
 
 
+KERNEL_VARIANTS = ("gemm_1cta", "gemm_2cta", "gemm_2cta_pair", "gemm_2cta_nfast", "gemm_2cta_streamk",
+                   "attn_fwd_multi", "attn_bwd_multi")
+
+
+def kernel_variant_counts(reset: bool = False) -> dict:
+    """Process-wide launch counts per kernel variant (bfpp_kernel_variant_count); reset=True
+    zeroes them after reading."""
+    L = N.lib()
+    out = {name: int(L.bfpp_kernel_variant_count(i)) for i, name in enumerate(KERNEL_VARIANTS)}
+    if reset:
+        L.bfpp_kernel_variant_reset()
+    return out
+
+
 STREAMS = ("compute", "dp", "fwd_send", "fwd_recv", "bwd_send", "bwd_recv", "wgrad")
 
 
@@ -174,11 +188,11 @@ def plan_rank(graph: ps.TaskGraph, pp_rank: int, n_dp: int):
     L = N.lib()
     nt, nw = C.c_int64(), C.c_int64()
     z = C.POINTER(C.c_int32)()
-    _check(L.bfpp_plan_rank(graph.handle, pp_rank, n_dp, 0, z, z, z, z, z, z, C.byref(nt), C.byref(nw)))
+    _check(L.bfpp_plan_rank(graph.handle, pp_rank, n_dp, 0, 0, z, z, z, z, z, z, C.byref(nt), C.byref(nw)))
     n, m = nt.value, nw.value
     arr = lambda k: (C.c_int32 * max(1, k))()  # noqa: E731
     ids, streams, flags, slots, woff, wids = arr(n), arr(n), arr(n), arr(n), arr(n + 1), arr(m)
-    _check(L.bfpp_plan_rank(graph.handle, pp_rank, n_dp, n, ids, streams, flags, slots, woff, wids, C.byref(nt),
+    _check(L.bfpp_plan_rank(graph.handle, pp_rank, n_dp, n, m, ids, streams, flags, slots, woff, wids, C.byref(nt),
                             C.byref(nw)))
     return [(ids[i], streams[i], flags[i], slots[i], list(wids[woff[i]:woff[i + 1]])) for i in range(n)]
 

@@ -18,6 +18,11 @@ from typing import Dict, List, Tuple
 PRESETS = {
     # name: (n_layers, s_hidden, n_heads, s_seq, s_voc)
     "tiny": (4, 128, 1, 64, 1000),        # BASELINE configs[0]; one head of 128 (kernel head_dim)
+    # parity presets at production kernel paths: every GEMM has M, N >= 256 (2-CTA tiles, grouped
+    # weight-gradient pairs), several heads and several 128-row attention blocks per sequence
+    "small": (2, 256, 2, 512, 2048),
+    # + an LM head whose weight-gradient operand (V x tokens) exceeds L2 -> N-fastest tile raster
+    "small-v50k": (1, 384, 3, 512, 50304),
     "gpt-1.3b": (24, 2048, 16, 2048, 50304),
     "gpt-2.7b": (32, 2560, 20, 2048, 50304),
     "gpt-6.7b": (32, 4096, 32, 2048, 50304),

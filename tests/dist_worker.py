@@ -37,7 +37,32 @@ CASES = {
     "acc_bf_dp2_fs_mb3": dict(n_dp=2, n_mb=3, dp_variant="DP_FS", accumulation="BreadthFirst"),
     "acc_df_dp2_fs_mb2": dict(n_dp=2, n_mb=2, dp_variant="DP_FS", accumulation="DepthFirst"),
     "acc_bf_dp2_dp0_mb2": dict(n_dp=2, n_mb=2, dp_variant="DP0", accumulation="BreadthFirst"),
+    # three optimizer steps on one executor per rank (receive-slot / flag reuse across steps, the
+    # run-ahead ring, per-segment early reduce-scatter + Adam moments from step 2 on)
+    "steps3_tiny_bf_pp2x2_dp2_fs": dict(n_dp=2, n_pp=2, n_loop=2, n_mb=4, dp_variant="DP_FS",
+                                        schedule="BreadthFirst", steps=3),
+    "steps3_tiny_df_pp2x2_dp2_fs": dict(n_dp=2, n_pp=2, n_loop=2, n_mb=4, dp_variant="DP_FS",
+                                        schedule="DepthFirst", steps=3),
+    "steps3_tiny_bf_pp2x2_mb4": dict(n_dp=1, n_pp=2, n_loop=2, n_mb=4, dp_variant="DP0", schedule="BreadthFirst",
+                                     steps=3),
+    "steps3_tiny_np_dp2_ps": dict(n_dp=2, n_pp=1, n_loop=1, n_mb=2, dp_variant="DP_PS", schedule="NoPipeline",
+                                  steps=3),
+    # production kernel paths (2-CTA / grouped GEMMs, multi-head multi-block attention) across GPUs
+    "small_bf_pp2x1_dp1_mb2": dict(n_dp=1, n_pp=2, n_loop=1, n_mb=2, s_mb=2, dp_variant="DP0",
+                                   schedule="BreadthFirst", model="small"),
+    "steps3_small_bf_pp1x2_dp2_fs": dict(n_dp=2, n_pp=1, n_loop=2, n_mb=2, dp_variant="DP_FS",
+                                         schedule="BreadthFirst", model="small", steps=3),
+    "steps3_small_bf_pp2x1_dp2_fs": dict(n_dp=2, n_pp=2, n_loop=1, n_mb=2, dp_variant="DP_FS",
+                                         schedule="BreadthFirst", model="small", steps=3),
 }
+
+
+def model_of(name):
+    return H.GPTConfig.preset(CASES[name].get("model", "tiny"))
+
+
+def steps_of(name):
+    return CASES[name].get("steps", 0)
 
 
 def accumulation_graph(name):
@@ -46,15 +71,17 @@ def accumulation_graph(name):
     if "accumulation" not in c:
         return None
     from paper_2211_05953_b200.executor import model_spec
-    return ps.build_accumulation_tasks(model_spec(H.TINY), ps.DpVariant[c["dp_variant"]],
+    return ps.build_accumulation_tasks(model_spec(model_of(name)), ps.DpVariant[c["dp_variant"]],
                                        ps.AccumulationOrder[c["accumulation"]], c["n_mb"])
 
 
 def config_of(name):
     c = dict(CASES[name])
+    c.pop("model", None)
+    c.pop("steps", None)
     if "accumulation" in c:
         from paper_2211_05953_b200.executor import accumulation_config
-        return accumulation_config(H.TINY, ps.DpVariant[c["dp_variant"]], c["n_mb"], c["n_dp"])
+        return accumulation_config(model_of(name), ps.DpVariant[c["dp_variant"]], c["n_mb"], c["n_dp"])
     c["dp_variant"] = ps.DpVariant[c["dp_variant"]]
     c["schedule"] = ps.Schedule[c["schedule"]]
     return ps.ParallelConfig(**c)
@@ -75,8 +102,8 @@ def main():
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(local)
     config = config_of(a.case)
-    cfg = H.TINY
-    params, tokens = H.make_case(cfg, config)
+    cfg = model_of(a.case)
+    n_steps = steps_of(a.case)
 
     def factory(**kw):
         obj = [comm_ids(config) if rank == 0 else None]
@@ -84,7 +111,12 @@ def main():
         return Executor(cfg, config, rank=rank, world=world, device=local, uids=obj[0],
                         graph=accumulation_graph(a.case), **kw)
 
-    res = H.run_rank(factory, cfg, config, params, tokens, rank)
+    if n_steps:
+        params, tokens = H.make_steps_case(cfg, config, n_steps)
+        res = H.run_rank_steps(factory, cfg, config, params, tokens, rank)
+    else:
+        params, tokens = H.make_case(cfg, config)
+        res = H.run_rank(factory, cfg, config, params, tokens, rank)
     with open(os.path.join(a.out, f"rank{rank}.pkl"), "wb") as f:
         pickle.dump(res, f)
     dist.barrier()

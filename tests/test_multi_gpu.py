@@ -1,5 +1,6 @@
-"""Multi-GPU executor parity (PP over NCCL send/recv, DP_FS all-gather/reduce-scatter,
-DP0 all-reduce, DP_PS) vs the CPU oracle. Each case runs under torchrun, one rank per GPU;
+"""Multi-GPU executor parity vs the CPU oracle: pipeline hand-offs as copy-engine peer copies
+into CUDA-IPC-mapped receive slots signalled with cuStreamWriteValue32 / cuStreamWaitValue32,
+DP_FS all-gather / reduce-scatter, DP0 all-reduce and DP_PS over NCCL. Each case runs under torchrun, one rank per GPU;
 skipped when fewer GPUs are visible than the case needs."""
 import os
 import pickle
@@ -9,7 +10,7 @@ import sys
 import pytest
 
 import exec_harness as H
-from dist_worker import CASES, config_of
+from dist_worker import CASES, config_of, model_of, steps_of
 
 pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -36,6 +37,12 @@ def test_multi_gpu_parity(case, tmp_path):
     for rank in range(n):
         with open(tmp_path / f"rank{rank}.pkl", "rb") as f:
             results.append(pickle.load(f))
-    params, tokens = H.make_case(H.TINY, config)
-    rep = H.compare(H.TINY, config, results, params, tokens)
-    print(case, rep.get("losses"), max(rep["grad_rel"].values()))
+    cfg, n_steps = model_of(case), steps_of(case)
+    if n_steps:
+        params, tokens = H.make_steps_case(cfg, config, n_steps)
+        rep = H.compare_steps(cfg, config, results, params, tokens)
+        print(case, rep["losses"], min(rep["weights_frac_close"].values()))
+    else:
+        params, tokens = H.make_case(cfg, config)
+        rep = H.compare(cfg, config, results, params, tokens)
+        print(case, rep.get("losses"), max(rep["grad_rel"].values()))
