@@ -119,8 +119,21 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def config_dict(args, cfg, pp, dp, loops, n_mb, sched):
+    """The workload keys both arms print (identical, so the driver can pair the lines)."""
+    return {"workload": f"BASELINE configs[1]: {args.model} seq {cfg.s_seq}, {sched} PP{pp}x{loops} loops"
+                        f" x DP{dp} {args.dp_variant}, {args.beta} seq/GPU",
+            "model": args.model, "global_batch": n_mb * args.s_mb * dp, "seq_len": cfg.s_seq,
+            "parallelism": f"pp{pp}x{loops}loops-dp{dp}-{args.dp_variant}", "schedule": sched,
+            "n_mb": n_mb, "s_mb": args.s_mb,
+            "l2": "inputs larger than L2 (bf16 weights + activations >> 126 MB)"}
+
+
 def reference_arm(args):
-    """CPU baseline arm: the oracle port (the reference has no model executor) on host cores."""
+    """CPU reference arm: the oracle port (the reference has no model executor) on
+    the host cores. Each step is one bounded sample of the workload (oracle/cpu_baseline.py
+    SampleStep: one layer + an LM-head slice, model-flop weighted into tokens), really executed, so
+    ms_per_step x steps is the wall time the arm spends; value = sample tokens / sample seconds."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import cpu_baseline as CB
     from paper_2211_05953_b200.model import GPTConfig
@@ -130,27 +143,26 @@ def reference_arm(args):
     n = args.gpus
     cfg = GPTConfig.preset(args.model)
     pp, dp, loops, n_mb, sched = layout(args, n)
-    per_step_tokens = n_mb * args.s_mb * dp * cfg.s_seq
+    sample = CB.SampleStep(cfg)
     times = []
+    t_all = time.perf_counter()
     for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        tps, sample, per_seq = CB.tokens_per_sec(cfg)
+        t = sample.run()
         if i >= args.warmup:
-            times.append(time.perf_counter() - t0)
-            last = (tps, sample)
-    tps, sample = last
+            times.append(t)
+    wall = time.perf_counter() - t_all
+    sec = float(np.mean(times))
+    tps = sample.tokens_equiv / sec
     threads = CB.blas_threads()
     line = {"impl": "reference", "metric": "tokens/sec", "value": tps, "unit": "tokens/s", "n_gpus": n,
-            "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": per_step_tokens / tps * 1e3, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"BASELINE configs[1]: {args.model} seq {cfg.s_seq}, {sched} PP{pp}x{loops} loops"
-                                   f" x DP{dp} {args.dp_variant}, {args.beta} seq/GPU",
-                       "model": args.model, "global_batch": n_mb * args.s_mb * dp, "seq_len": cfg.s_seq},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": config_dict(args, cfg, pp, dp, loops, n_mb, sched),
+            "tokens_per_step": sample.tokens_equiv,
             "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": threads, "kind": "port",
-                             "sample": sample + "; the reference (pipesim) has no CPU model executor"},
+                             "sample": sample.desc + "; the reference (pipesim) has no CPU model executor"},
             "e2e": {"value": tps, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "sample_wall_s": float(np.mean(times))}
+            "wall_s": wall}
     print(json.dumps(line), flush=True)
 
 
@@ -332,8 +344,12 @@ def main():
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         try:
             import cpu_baseline as CB
-            tps, sample, _ = CB.tokens_per_sec(cfg)
-            cpu = {"value": tps, "unit": "tokens/s", "cores": CB.blas_threads(), "kind": "port", "sample": sample}
+            smp = CB.SampleStep(cfg)
+            smp.run()
+            sec = min(smp.run() for _ in range(2))
+            tps = smp.tokens_equiv / sec
+            cpu = {"value": tps, "unit": "tokens/s", "cores": CB.blas_threads(), "kind": "port",
+                   "sample": smp.desc + f"; best of 2 after 1 warm-up, {sec:.2f} s per sample"}
             from paper_2211_05953_b200 import _native as NN
             mspec = ps.ModelSpec(n_layers=cfg.n_layers, s_hidden=cfg.s_hidden, n_heads=cfg.n_heads,
                                  s_seq=cfg.s_seq, s_voc=cfg.s_voc)
@@ -353,12 +369,7 @@ def main():
             "metric": "tokens/sec", "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": f"BASELINE configs[1]: {args.model} seq {cfg.s_seq}, {sched} PP{pp}x{loops} loops"
-                                   f" x DP{dp} {args.dp_variant}, {args.beta} seq/GPU",
-                       "model": args.model, "global_batch": n_mb * args.s_mb * dp, "seq_len": cfg.s_seq,
-                       "parallelism": f"pp{pp}x{loops}loops-dp{dp}-{args.dp_variant}", "schedule": sched,
-                       "n_mb": n_mb, "s_mb": args.s_mb,
-                       "l2": "inputs larger than L2 (bf16 weights + activations >> 126 MB)"},
+            "config": config_dict(args, cfg, pp, dp, loops, n_mb, sched),
             "mfu": {"vs_spec_2250TF": mfu, "vs_measured_burst": mfu_meas,
                     "model_flops_per_token": fpt, "eq11_tflops_per_gpu": eq11 / 1e12},
             "bubble_fraction": {"measured": bubble, "eq7": sim_bubble,

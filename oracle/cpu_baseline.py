@@ -3,9 +3,9 @@
 The reference has no CPU executor of the model, so the CPU
 "reference arm" for tokens/sec is this repository's numpy restatement
 (oracle/gpt_oracle.py, kind "port") run in float32 with numpy's BLAS threads.
-Bounded sample: one transformer layer forward+backward on one full-length
-sequence plus the LM head + loss forward+backward on a `head_tokens` slice;
-extrapolated to the whole model as  t_seq = L * t_layer + t_head * S/head_tokens.
+Bounded sample step (SampleStep): one transformer layer forward+backward on one
+full-length sequence plus the LM head + loss forward+backward on a `head_tokens`
+slice, counted as the model-flop-weighted number of tokens it represents.
 Also times the reference's own schedule path (place_stages + build_tasks +
 simulate) from oracle/_ref when it is present.
 """
@@ -44,39 +44,38 @@ def _layer_params(h, rng):
             "l.w_fc2": (rng.standard_normal((h, m)) * 0.02).astype(f)}
 
 
-def time_sample(cfg, head_tokens: int = 256, reps: int = 1, seed: int = 0):
-    """Returns (seconds per sequence for the whole model, t_layer, t_head_slice)."""
-    rng = np.random.default_rng(seed)
-    h, S, V = cfg.s_hidden, cfg.s_seq, cfg.s_voc
-    P = _layer_params(h, rng)
-    G = {k: np.zeros_like(v) for k, v in P.items()}
-    x = rng.standard_normal((S, h)).astype(np.float32)
-    t_layer = 1e30
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        y, cache = O.layer_forward(P, "l.", x, cfg)
-        O.layer_backward(P, G, "l.", np.ones_like(y), cache, cfg)
-        t_layer = min(t_layer, time.perf_counter() - t0)
-    HP = {"lnf_g": np.ones(h, np.float32), "lnf_b": np.zeros(h, np.float32),
-          "w_head": (rng.standard_normal((V, h)) * 0.02).astype(np.float32)}
-    HG = {k: np.zeros_like(v) for k, v in HP.items()}
-    xs = x[:head_tokens]
-    lab = rng.integers(0, V, head_tokens)
-    t_head = 1e30
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        O.head_forward_backward(HP, HG, xs, lab, head_tokens)
-        t_head = min(t_head, time.perf_counter() - t0)
-    per_seq = cfg.n_layers * t_layer + t_head * (S / head_tokens)
-    return per_seq, t_layer, t_head
+class SampleStep:
+    """One bounded CPU step of the workload: one transformer layer forward+backward on a full
+    [S x h] sequence plus the LM head + loss forward+backward on `head_tokens` tokens, float32
+    numpy on the BLAS threads. Inputs and weights are created once, outside the timed step.
+    Its size in tokens is model-flop weighted: the sample's model flops
+    S*(72h^2 + 12Sh) + head_tokens*6hV divided by the model's flops per token
+    (72Lh^2 + 12Lsh + 6hV), so tokens_equiv / seconds is the model's tokens/s on these cores."""
 
+    def __init__(self, cfg, head_tokens: int = 256, seed: int = 0):
+        rng = np.random.default_rng(seed)
+        h, S, V = cfg.s_hidden, cfg.s_seq, cfg.s_voc
+        head_tokens = min(head_tokens, S)
+        self.cfg, self.head_tokens = cfg, head_tokens
+        self.P = _layer_params(h, rng)
+        self.G = {k: np.zeros_like(v) for k, v in self.P.items()}
+        self.x = rng.standard_normal((S, h)).astype(np.float32)
+        self.HP = {"lnf_g": np.ones(h, np.float32), "lnf_b": np.zeros(h, np.float32),
+                   "w_head": (rng.standard_normal((V, h)) * 0.02).astype(np.float32)}
+        self.HG = {k: np.zeros_like(v) for k, v in self.HP.items()}
+        self.lab = rng.integers(0, V, head_tokens)
+        L = cfg.n_layers
+        fpt = 72.0 * L * h * h + 12.0 * L * S * h + 6.0 * h * V
+        self.tokens_equiv = (S * (72.0 * h * h + 12.0 * S * h) + head_tokens * 6.0 * h * V) / fpt
+        self.desc = (f"1 of {L} layers fwd+bwd at [{S} x {h}] + LM head fwd+bwd on {head_tokens} of {S} tokens per "
+                     f"step (float32 numpy); = {self.tokens_equiv:.1f} model-flop-weighted tokens per step")
 
-def tokens_per_sec(cfg, head_tokens: int = 256):
-    per_seq, t_layer, t_head = time_sample(cfg, head_tokens)
-    sample = (f"1 layer fwd+bwd at [{cfg.s_seq} x {cfg.s_hidden}] ({t_layer:.2f} s) + LM head fwd+bwd on "
-              f"{head_tokens} tokens ({t_head:.2f} s), float32 numpy, extrapolated to {cfg.n_layers} layers x "
-              f"{cfg.s_seq} tokens per sequence")
-    return cfg.s_seq / per_seq, sample, per_seq
+    def run(self) -> float:
+        t0 = time.perf_counter()
+        y, cache = O.layer_forward(self.P, "l.", self.x, self.cfg)
+        O.layer_backward(self.P, self.G, "l.", np.ones_like(y), cache, self.cfg)
+        O.head_forward_backward(self.HP, self.HG, self.x[:self.head_tokens], self.lab, self.head_tokens)
+        return time.perf_counter() - t0
 
 
 def reference_search_path(model_spec_c, n_gpu: int, threads: int):
