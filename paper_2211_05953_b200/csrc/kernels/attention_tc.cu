@@ -1,20 +1,25 @@
-// Causal flash attention forward on the 5th-gen tensor cores (sm_100a), head_dim 128.
+// Causal flash attention forward and backward on the 5th-gen tensor cores (sm_100a), head_dim
+// 128. Forward below; the backward's warp roles are described above attn_bwd_tc_kernel.
 //
 // One CTA per (128-query block, head, sample). Warp roles (192 threads):
 //   warp 0      TMA producer: Q once, then K and V tiles of 128 keys (2-stage rings)
 //   warp 1      MMA issuer (one elected thread) + TMEM owner:
 //                 S_j = Q K_j^T  -> TMEM (double-buffered, so S_{j+1} overlaps softmax_j)
-//                 O  += P_j V_j  -> TMEM (A = P from shared memory, B = V MN-major)
+//                 O  += P_j V_j  -> TMEM (A = P_j read from TMEM, where it overwrote S_j;
+//                                   B = V MN-major)
 //   warps 2..5  softmax: thread = query row (TMEM lane); the whole 128-key row of S is in
 //               registers, so max / sum need no shuffles. Online softmax in the log2
 //               domain with a lazily updated running max (O in TMEM is rescaled only when
-//               the max grows by more than 2^8), P written as bf16 into a SWIZZLE_128B
-//               K-major tile for the PV MMA.
+//               the max grows by more than 2^8), P packed as bf16 pairs into the S_j columns
+//               (the A operand of the PV MMA). The exps of tile j run while PV_{j-1} is on the
+//               tensor pipe: only an O rescale waits for it.
 // Layouts as attention.cu: qkv [B*S][3*H*128], o [B*S][H*128], lse [B*H][S] (log2 domain).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <climits>
+#include <cstdlib>
 #include <stdexcept>
 
 #include "gemm.hpp"
@@ -25,6 +30,21 @@ namespace bfpp {
 namespace {
 
 constexpr int D = 128, BQ = 128, BKV = 128;
+
+// Per-iteration clock64 stamps of one CTA's warp roles (scripts/attn_trace.cu builds this file
+// with BFPP_ATTN_TRACE); compiled out of the product library.
+#ifdef BFPP_ATTN_TRACE
+__device__ unsigned long long g_attn_trace[8][64][16];
+#define ATRACE(role, it, ev)                                                                     \
+    do {                                                                                         \
+        if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (it) < 64)                  \
+            g_attn_trace[role][it][ev] = clock64();                                              \
+    } while (0)
+#else
+#define ATRACE(role, it, ev) \
+    do {                     \
+    } while (0)
+#endif
 constexpr int kTile = 128 * 128 * 2;  // one [128 rows][128 dims] bf16 tile = 2 x [128][64] SW128 blocks
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.f;  // log2 units
@@ -33,8 +53,7 @@ struct FwdSmem {
     static constexpr int kQ = 0;
     static constexpr int kK = kQ + kTile;          // 2 stages
     static constexpr int kV = kK + 2 * kTile;      // 2 stages
-    static constexpr int kP = kV + 2 * kTile;
-    static constexpr int kBar = kP + kTile;
+    static constexpr int kBar = kV + 2 * kTile;
     static constexpr int kBytes = kBar + 256 + 1024;
 };
 
@@ -59,9 +78,8 @@ __global__ void __launch_bounds__(192, 1)
     uint64_t* v_full = bar + 5;   // [2]
     uint64_t* v_empty = bar + 7;  // [2]
     uint64_t* s_full = bar + 9;   // [2]
-    uint64_t* s_empty = bar + 11; // [2]
-    uint64_t* p_full = bar + 13;
-    uint64_t* o_done = bar + 14;  // PV_j complete (P buffer free, O stable)
+    uint64_t* p_full = bar + 11;
+    uint64_t* o_done = bar + 12;  // PV_j complete (O stable)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
 
     // grid (H, query blocks, B): x (heads) varies fastest, so the longest query blocks (most
@@ -84,7 +102,6 @@ __global__ void __launch_bounds__(192, 1)
             ptx::mbar_init(&v_full[i], 1);
             ptx::mbar_init(&v_empty[i], 1);
             ptx::mbar_init(&s_full[i], 1);
-            ptx::mbar_init(&s_empty[i], 4);
         }
         ptx::mbar_init(p_full, 4);
         ptx::mbar_init(o_done, 1);
@@ -125,13 +142,13 @@ __global__ void __launch_bounds__(192, 1)
             constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(128, 128, 0, 0);   // Q K^T: both K-major
             constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(128, 128, 0, 1);  // P V: V is MN-major
             const uint32_t sq = ptx::smem_u32(sm + FwdSmem::kQ);
-            const uint32_t sp = ptx::smem_u32(sm + FwdSmem::kP);
             ptx::mbar_wait(q_full, 0);
+            // S_j reuses the columns of P_{j-2}: issued after p_full_{j-1} (so softmax is done with
+            // them) and after PV_{j-2} (the tensor pipe runs this thread's MMAs in issue order)
             auto issue_s = [&](int j) {
                 const int st = j & 1;
                 const uint32_t ph = (j >> 1) & 1;
                 ptx::mbar_wait(&k_full[st], ph);
-                ptx::mbar_wait(&s_empty[st], ph ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t sk = ptx::smem_u32(sm + FwdSmem::kK + st * kTile);
 #pragma unroll
@@ -149,8 +166,8 @@ __global__ void __launch_bounds__(192, 1)
                 ptx::tc_fence_after();
                 const uint32_t sv = ptx::smem_u32(sm + FwdSmem::kV + st * kTile);
 #pragma unroll
-                for (int kk = 0; kk < BKV / 16; ++kk)
-                    ptx::umma_f16(t_o, kmajor_desc(sp, kk), mnmajor_desc(sv, kk), idesc_pv, (j | kk) != 0);
+                for (int kk = 0; kk < BKV / 16; ++kk)  // P: 16 keys = 8 packed columns per K-step
+                    ptx::umma_f16_ts(t_o, t_s + st * 128 + kk * 8, mnmajor_desc(sv, kk), idesc_pv, (j | kk) != 0);
                 ptx::umma_commit(&v_empty[st]);
                 ptx::umma_commit(o_done);
             }
@@ -161,7 +178,6 @@ __global__ void __launch_bounds__(192, 1)
         const int r = q4 * 32 + lane;          // row within the tile (= TMEM lane)
         const int qrow = qb * BQ + r;          // query position within the sequence
         const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
-        const uint32_t prow = ptx::smem_u32(sm + FwdSmem::kP) + r * 128;
         float m_used = -INFINITY, l = 0.f;
         for (int j = 0; j < n_tiles; ++j) {
             const int st = j & 1;
@@ -176,68 +192,70 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
                 for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(rr[i]);
             }
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&s_empty[st]);
             const int k0 = j * BKV;
             const bool diag = k0 + BKV - 1 > qb * BQ || k0 + BKV > S;
+            // keys k0 + i with i < lim are visible to this query row (k <= q, k < S)
+            const int lim = diag ? min(qrow + 1, S) - k0 : BKV;
             float mx = -INFINITY;
 #pragma unroll
             for (int i = 0; i < 128; ++i) {
-                float v = s[i] * scale_log2;
-                if (diag && (k0 + i > qrow || k0 + i >= S)) v = -INFINITY;
+                const float v = i < lim ? s[i] * scale_log2 : -INFINITY;
                 s[i] = v;
                 mx = fmaxf(mx, v);
             }
-            // P buffer and O are free once PV_{j-1} has completed
-            if (j > 0) ptx::mbar_wait(o_done, (j - 1) & 1);
             // The rescale decision is per row, but tcgen05.ld/st are warp-collective
             // (.sync.aligned): if any row of the warp needs it, the whole warp rescales (rows
             // that do not need it use alpha = 1), so the TMEM accesses never diverge.
             const bool mine = mx > m_used + kRescaleThreshold;
-            if (__any_sync(0xffffffffu, mine)) {
-                const float m_new = mine ? mx : m_used;
-                const float alpha = mine ? (m_used == -INFINITY ? 0.f : ptx::ex2_fast(m_used - mx)) : 1.f;
+            const bool rescale = __any_sync(0xffffffffu, mine);
+            float alpha = 1.f;
+            if (rescale) {
+                alpha = mine ? (m_used == -INFINITY ? 0.f : ptx::ex2_fast(m_used - mx)) : 1.f;
+                if (mine) m_used = mx;
                 l *= alpha;
-                if (j > 0) {
-                    ptx::tc_fence_after();
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        uint32_t rr[32];
-                        ptx::tmem_ld_32x32b_x32(t_o + lane_off + c * 32, rr);
-                        ptx::tmem_ld_wait();
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) rr[i] = __float_as_uint(__uint_as_float(rr[i]) * alpha);
-                        ptx::tmem_st_32x32b_x32(t_o + lane_off + c * 32, rr);
-                    }
-                    ptx::tmem_st_wait();
-                }
-                m_used = m_new;
             }
             float sum = 0.f;
+            uint32_t pw[64];
 #pragma unroll
-            for (int c = 0; c < 16; ++c) {  // 16 chunks of 8 keys = 16 B of bf16
-                uint4 pk;
-                uint32_t* w = reinterpret_cast<uint32_t*>(&pk);
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const float p0 = ptx::ex2_fast(s[8 * c + 2 * u] - m_used);
-                    const float p1 = ptx::ex2_fast(s[8 * c + 2 * u + 1] - m_used);
-                    sum += p0 + p1;
-                    __nv_bfloat162 hb = __floats2bfloat162_rn(p0, p1);
-                    w[u] = *reinterpret_cast<uint32_t*>(&hb);
-                }
-                // [2 key-blocks][128 rows][128 B], 16-byte chunk swizzled by row & 7
-                const int blk = c >> 3, ch = c & 7;
-                ptx::st_shared_v4(prow + blk * (kTile / 2) + ((ch ^ (r & 7)) << 4), pk);
+            for (int i = 0; i < 64; ++i) {
+                const float p0 = ptx::ex2_fast(s[2 * i] - m_used);
+                const float p1 = ptx::ex2_fast(s[2 * i + 1] - m_used);
+                sum += p0 + p1;
+                __nv_bfloat162 hb = __floats2bfloat162_rn(p0, p1);
+                pw[i] = *reinterpret_cast<uint32_t*>(&hb);
             }
             l += sum;
-            ptx::fence_proxy_async_smem();
+            if (rescale && j > 0) {
+                // O is stable once PV_{j-1} has completed (PV_j waits for this tile's p_full)
+                ptx::mbar_wait(o_done, (j - 1) & 1);
+                ptx::tc_fence_after();
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t rr[32];
+                    ptx::tmem_ld_32x32b_x32(t_o + lane_off + c * 32, rr);
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) rr[i] = __float_as_uint(__uint_as_float(rr[i]) * alpha);
+                    ptx::tmem_st_32x32b_x32(t_o + lane_off + c * 32, rr);
+                }
+            }
+            // P_j packed into the first 64 columns of S_j's buffer (all of S_j is in registers)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                uint32_t w[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) w[i] = pw[c * 16 + i];
+                ptx::tmem_st_32x32b_x16(t_s + st * 128 + lane_off + c * 16, w);
+            }
+            ptx::tmem_st_wait();
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(p_full);
         }
-        // epilogue: O / l -> bf16 -> global; lse = m + log2(l)
+        // epilogue: O / l -> bf16 -> global; lse = m + log2(l). Passing s_full_{n-1} only proves
+        // PV_{n-3} done, so wait for the phases of PV_{n-2} and PV_{n-1} in turn (a parity wait
+        // must not skip a phase)
+        if (n_tiles >= 2) ptx::mbar_wait(o_done, (n_tiles - 2) & 1);
         ptx::mbar_wait(o_done, (n_tiles - 1) & 1);
         ptx::tc_fence_after();
         const float inv = 1.f / l;
@@ -290,53 +308,90 @@ void attention_fwd_tc(const void* qkv, void* o, float* lse, int batch, int seq, 
 
 
 // =====================================================================================
-// Backward: one CTA per (128-key block, head, sample), looping over the query blocks at or
-// after the diagonal. Warp roles (192 threads):
-//   warp 0      TMA: K, V once; Q_i and dO_i per query block (single buffer, reloaded as soon
-//               as the MMAs that read them have completed)
-//   warp 1      MMA: S^T = K Q_i^T and dP^T = V dO_i^T (TMEM, lanes = keys);
-//               dV += P^T dO_i, dK += dS^T Q_i (TMEM accumulators); dQ_i = dS K (TMEM, lanes = q)
-//   warps 2..5  thread = key row: P^T = exp2(S^T*scale_log2 - lse), dS^T = P^T (dP^T - delta),
-//               both to shared memory as bf16 (K-major over q); then drain dQ_i (thread = q row)
-//               with red.global.add.v4.f32; finally write dK, dV.
-// TMEM columns: [0,128) S^T, [128,256) dP^T / dQ, [256,384) dV, [384,512) dK.
 namespace {
 
-struct BwdSmem {
-    static constexpr int kK = 0, kV = kTile, kQ = 2 * kTile, kO = 3 * kTile, kP = 4 * kTile, kS = 5 * kTile;
-    static constexpr int kLse = 6 * kTile;         // [2][128] f32 (double-buffered by iteration)
-    static constexpr int kDelta = kLse + 1024;     // [2][128] f32
-    static constexpr int kBar = kDelta + 1024;
-    static constexpr int kBytes = kBar + 256 + 1024;
-};
-
-__device__ __forceinline__ void red_add_v4(float* dst, float a, float b, float c, float d) {
-    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(a), "f"(b), "f"(c), "f"(d)
-                 : "memory");
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
-__device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
-__global__ void __launch_bounds__(192, 1)
+// -------------------------------------------------------------------------------------
+// Backward: one CTA per (128-key block, head, sample), 14 warps (448 threads). Every MMA is
+// 128 x 128 x 16 (an N = 64 MMA takes as long as N = 128); the elementwise work of a query block
+// is split into two 64-query halves h = A, B so dV_A / dK_A start while half B is computed:
+//   warp 0      TMA: K, V once; Q_i (2-stage ring) and dO_i per query block (one buffer per
+//               64-row half, refilled as soon as that half's dV MMAs have read it)
+//   warp 1      MMA issuer (one thread), per query block i, in issue order:
+//                 S^T = K Q_i^T -> TMEM[0,128)   dP^T = V dO_i^T -> TMEM[128,256)
+//                 for h: dV += P_h^T dO_h   (A = P_h^T read from TMEM, packed over S_h^T)
+//                        (h = B: dQ^T = K^T dS^T -> TMEM[128,256), lanes = head dims)
+//                        dK += dS_h^T Q_h   (A = dS^T from shared memory)
+//   warps 2..5  dQ drain: thread = head dim d; per 64 queries, each warp stages its 32 dims
+//               as a SWIZZLE_128B f32 box and adds it to the f32 dQ accumulator with one
+//               TMA reduce-add (cp.reduce.async.bulk.tensor)
+//   warps 6..9 (half A), 10..13 (half B): elementwise, thread = key row (TMEM lane):
+//               P^T = exp2(S^T*scale_log2 - lse) packed bf16 into TMEM, dS^T = P^T (dP^T - delta)
+//               bf16 into shared memory (packed f32x2 arithmetic; the causal selects only on
+//               diagonal / partial blocks); finally dK, dV.
+// Shared memory: K, V, Q[2], dO, dS^T, dQ staging (4 x [64][32] f32) = 7 x 32 KB + lse/delta
+// (exactly fits 227 KB; the dynamic shared window is 1024-byte aligned, checked at run time).
+struct BwdSmem {
+    static constexpr int kK = 0, kV = kTile, kQ = 2 * kTile, kO = 4 * kTile, kS = 5 * kTile, kDQ = 6 * kTile;
+    static constexpr int kStat = 7 * kTile;  // [half][iteration parity][-lse 64 | -delta 64] f32
+    static constexpr int kBar = kStat + 2048;
+    static constexpr int kBytes = kBar + 160;  // 17 mbarriers + the TMEM address
+};
+static_assert(BwdSmem::kBytes <= 232448, "attention backward shared memory");
+
+// Elementwise core of the backward for 32 queries of one key row: rs = S^T, rd = dP^T (TMEM
+// words), nl / nd = -lse / -delta of the 32 queries (shared memory, broadcast), [lo, hi) = the
+// visible query range (MASK only) -> P^T and dS^T as packed bf16 pairs.
+template <bool MASK>
+__device__ __forceinline__ void bwd_elementwise32(const uint32_t (&rs)[32], const uint32_t (&rd)[32], const float* nl,
+                                                  const float* nd, float scale_log2, int q_base, int lo, int hi,
+                                                  uint32_t (&pw)[16], uint32_t (&dw)[16]) {
+    const uint64_t sc = ptx::pack2(scale_log2, scale_log2);
+#pragma unroll
+    for (int j = 0; j < 32; j += 2) {
+        const float2 nl2 = *reinterpret_cast<const float2*>(nl + j);
+        const float2 nd2 = *reinterpret_cast<const float2*>(nd + j);
+        const float2 t = ptx::unpack2(ptx::ffma2(ptx::pack2(__uint_as_float(rs[j]), __uint_as_float(rs[j + 1])), sc,
+                                                 ptx::pack2(nl2.x, nl2.y)));
+        float p0 = ptx::ex2_fast(t.x), p1 = ptx::ex2_fast(t.y);
+        if (MASK) {
+            const int q = q_base + j;
+            p0 = ((q >= lo) & (q < hi)) ? p0 : 0.f;
+            p1 = ((q + 1 >= lo) & (q + 1 < hi)) ? p1 : 0.f;
+        }
+        const uint64_t pp = ptx::pack2(p0, p1);
+        const float2 d = ptx::unpack2(
+            ptx::fmul2(pp, ptx::fadd2(ptx::pack2(__uint_as_float(rd[j]), __uint_as_float(rd[j + 1])),
+                                      ptx::pack2(nd2.x, nd2.y))));
+        __nv_bfloat162 hp = __floats2bfloat162_rn(p0, p1), hd = __floats2bfloat162_rn(d.x, d.y);
+        pw[j / 2] = *reinterpret_cast<uint32_t*>(&hp);
+        dw[j / 2] = *reinterpret_cast<uint32_t*>(&hd);
+    }
+}
+
+__global__ void __launch_bounds__(448, 1)
     attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
-                       const float* __restrict__ lse, const float* __restrict__ delta, float* __restrict__ dq_acc,
-                       __nv_bfloat16* __restrict__ dqkv, int S, int H, float scale, float scale_log2) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+                        const __grid_constant__ CUtensorMap tm_dq, const float* __restrict__ lse,
+                        const float* __restrict__ delta, __nv_bfloat16* __restrict__ dqkv, int S, int H, float scale,
+                        float scale_log2) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* sm = smem_raw;
+    if (threadIdx.x == 0 && (ptx::smem_u32(sm) & 1023u)) __trap();
     uint64_t* bar = reinterpret_cast<uint64_t*>(sm + BwdSmem::kBar);
     uint64_t* kv_full = bar + 0;
-    uint64_t* qo_full = bar + 1;
-    uint64_t* qo_empty = bar + 2;
-    uint64_t* s_full = bar + 3;
-    uint64_t* p_full = bar + 4;
-    uint64_t* dq_full = bar + 5;
-    uint64_t* dq_empty = bar + 6;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 8);
-    const uint32_t s_lse = ptx::smem_u32(sm + BwdSmem::kLse);
-    const uint32_t s_del = ptx::smem_u32(sm + BwdSmem::kDelta);
+    uint64_t* q_full = bar + 1;    // [2]
+    uint64_t* q_empty = bar + 3;   // [2]
+    uint64_t* s_full = bar + 5;
+    uint64_t* p_full = bar + 7;    // [half]
+    uint64_t* dq_full = bar + 9;
+    uint64_t* dq_empty = bar + 11;
+    uint64_t* o_full = bar + 13;   // [half]
+    uint64_t* o_empty = bar + 15;  // [half]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 17);
 
-    // grid (H, key blocks, B): the block scheduler walks x fastest, so every head's key block 0
-    // (which sees the most query blocks under the causal mask) starts in the first wave
-    const int n_kb = (S + BKV - 1) / BKV;
     const int kb = blockIdx.y;
     const int head = blockIdx.x, b = blockIdx.z;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -344,18 +399,24 @@ __global__ void __launch_bounds__(192, 1)
     const int row0 = b * S;
     const int i0 = kb;  // first query block that sees this key block (BQ == BKV)
     const int n_qb = (S + BQ - 1) / BQ;
-    (void)n_kb;
+    const int n_it = n_qb - i0;
+    constexpr int kHalf = kTile / 4;  // 64 rows x 128 B: row offset of the second half of a tile
 
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch(&tm_qkv);
         ptx::tma_prefetch(&tm_do);
+        ptx::tma_prefetch(&tm_dq);
         ptx::mbar_init(kv_full, 1);
-        ptx::mbar_init(qo_full, 1);
-        ptx::mbar_init(qo_empty, 1);
         ptx::mbar_init(s_full, 1);
-        ptx::mbar_init(p_full, 4);
         ptx::mbar_init(dq_full, 1);
         ptx::mbar_init(dq_empty, 4);
+        for (int k = 0; k < 2; ++k) {
+            ptx::mbar_init(&q_full[k], 1);
+            ptx::mbar_init(&q_empty[k], 1);
+            ptx::mbar_init(&p_full[k], 4);
+            ptx::mbar_init(&o_full[k], 1);
+            ptx::mbar_init(&o_empty[k], 1);
+        }
         ptx::fence_barrier_init();
     }
     if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
@@ -373,156 +434,214 @@ __global__ void __launch_bounds__(192, 1)
                 ptx::tma_load_2d(sm + BwdSmem::kK + h2 * (kTile / 2), &tm_qkv, kv_full, kcol + 64 * h2, row0 + kb * BKV);
                 ptx::tma_load_2d(sm + BwdSmem::kV + h2 * (kTile / 2), &tm_qkv, kv_full, vcol + 64 * h2, row0 + kb * BKV);
             }
-            for (int i = i0; i < n_qb; ++i) {
-                if (i > i0) ptx::mbar_wait(qo_empty, (i - i0 - 1) & 1);
-                ptx::mbar_expect_tx(qo_full, 2 * kTile);
-                for (int h2 = 0; h2 < 2; ++h2) {
-                    ptx::tma_load_2d(sm + BwdSmem::kQ + h2 * (kTile / 2), &tm_qkv, qo_full, qcol + 64 * h2, row0 + i * BQ);
-                    ptx::tma_load_2d(sm + BwdSmem::kO + h2 * (kTile / 2), &tm_do, qo_full, head * D + 64 * h2, row0 + i * BQ);
+            for (int it = 0; it < n_it; ++it) {
+                const int st = it & 1, i = i0 + it;
+                if (it >= 2) ptx::mbar_wait(&q_empty[st], ((it >> 1) & 1) ^ 1);
+                ATRACE(0, it, 0);
+                ptx::mbar_expect_tx(&q_full[st], kTile);
+                for (int h2 = 0; h2 < 2; ++h2)
+                    ptx::tma_load_2d(sm + BwdSmem::kQ + st * kTile + h2 * (kTile / 2), &tm_qkv, &q_full[st],
+                                     qcol + 64 * h2, row0 + i * BQ);
+                for (int h = 0; h < 2; ++h) {  // dO rows 64h..64h+63: [2 dim blocks][64 rows][128 B]
+                    if (it >= 1) ptx::mbar_wait(&o_empty[h], (it - 1) & 1);
+                    ATRACE(0, it, 1 + h);
+                    ptx::mbar_expect_tx(&o_full[h], kTile / 2);
+                    for (int h2 = 0; h2 < 2; ++h2)
+                        ptx::tma_load_2d(sm + BwdSmem::kO + h2 * (kTile / 2) + h * kHalf, &tm_do, &o_full[h],
+                                         head * D + 64 * h2, row0 + i * BQ + 64 * h);
                 }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            constexpr uint32_t id_kk = ptx::idesc_bf16_f32(128, 128, 0, 0);  // A, B K-major
-            constexpr uint32_t id_kn = ptx::idesc_bf16_f32(128, 128, 0, 1);  // B MN-major
-            constexpr uint32_t id_nn = ptx::idesc_bf16_f32(128, 128, 1, 1);  // A, B MN-major
+            constexpr uint32_t id_kk = ptx::idesc_bf16_f32(128, 128, 0, 0);  // S^T, dP^T: A, B K-major
+            constexpr uint32_t id_kn = ptx::idesc_bf16_f32(128, 128, 0, 1);  // dV, dK: B MN-major
+            constexpr uint32_t id_nn = ptx::idesc_bf16_f32(128, 128, 1, 1);  // dQ^T: A, B MN-major
             const uint32_t sk = ptx::smem_u32(sm + BwdSmem::kK), sv = ptx::smem_u32(sm + BwdSmem::kV);
-            const uint32_t sq = ptx::smem_u32(sm + BwdSmem::kQ), so = ptx::smem_u32(sm + BwdSmem::kO);
-            const uint32_t sp = ptx::smem_u32(sm + BwdSmem::kP), sds = ptx::smem_u32(sm + BwdSmem::kS);
+            const uint32_t so = ptx::smem_u32(sm + BwdSmem::kO), sds = ptx::smem_u32(sm + BwdSmem::kS);
             ptx::mbar_wait(kv_full, 0);
-            for (int i = i0; i < n_qb; ++i) {
-                const int it = i - i0;
-                // S^T_i right away (the tensor pipe runs it while dQ_{i-1} drains); dP^T_i into the
-                // dQ_{i-1} columns once those are drained
-                ptx::mbar_wait(qo_full, it & 1);
+            for (int it = 0; it < n_it; ++it) {
+                const int st = it & 1;
+                const uint32_t sq = ptx::smem_u32(sm + BwdSmem::kQ + st * kTile);
+                ptx::mbar_wait(&q_full[st], (it >> 1) & 1);
+                ATRACE(1, it, 0);
                 ptx::tc_fence_after();
+                // S^T overwrites P^T of the previous block: issued after that block's dV (the
+                // tensor pipe executes one thread's MMAs in issue order). All MMAs are 128 x 128:
+                // N = 64 costs as much tensor time as N = 128.
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk)
                     ptx::umma_f16(t_s, kmajor_desc(sk, kk), kmajor_desc(sq, kk), id_kk, kk != 0);
-                if (it > 0) ptx::mbar_wait(dq_empty, (it - 1) & 1);
+                if (it > 0) ptx::mbar_wait(dq_empty, (it - 1) & 1);  // dQ of block i-1 drained
+                ATRACE(1, it, 1);
+                ptx::mbar_wait(&o_full[0], it & 1);
+                ptx::mbar_wait(&o_full[1], it & 1);
+                ATRACE(1, it, 2);
                 ptx::tc_fence_after();
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk)
                     ptx::umma_f16(t_dp, kmajor_desc(sv, kk), kmajor_desc(so, kk), id_kk, kk != 0);
                 ptx::umma_commit(s_full);
-                ptx::mbar_wait(p_full, it & 1);
-                ptx::tc_fence_after();
+                ATRACE(1, it, 3);
+                for (int h = 0; h < 2; ++h) {
+                    ptx::mbar_wait(&p_full[h], it & 1);
+                    ATRACE(1, it, 7 + 2 * h);
+                    ptx::tc_fence_after();
+                    // dV += P_h^T dO_h: K-step kk = queries 16kk..16kk+15 of the block; P_h^T packed
+                    // in TMEM at columns 64h + 8 (kk % 4)
 #pragma unroll
-                for (int kk = 0; kk < BQ / 16; ++kk) {
-                    ptx::umma_f16(t_dv, kmajor_desc(sp, kk), mnmajor_desc(so, kk), id_kn, (it | kk) != 0);
-                    ptx::umma_f16(t_dk, kmajor_desc(sds, kk), mnmajor_desc(sq, kk), id_kn, (it | kk) != 0);
+                    for (int k4 = 0; k4 < 4; ++k4) {
+                        const int kk = h * 4 + k4;
+                        ptx::umma_f16_ts(t_dv, t_s + h * 64 + k4 * 8, mnmajor_desc(so, kk), id_kn, (it | kk) != 0);
+                    }
+                    ptx::umma_commit(&o_empty[h]);  // dO rows of this half: read by dP^T and dV only
+                    if (h == 1) {
+                        // dQ^T [d][q] = sum_key K[key][d] dS[q][key]: A = K (MN-major over d),
+                        // B = dS^T tile (MN-major over q), K-step = 16 keys; before dK_B so the
+                        // drain runs under it
+#pragma unroll
+                        for (int kk = 0; kk < BKV / 16; ++kk)
+                            ptx::umma_f16(t_dp, mnmajor_desc(sk, kk), mnmajor_desc(sds, kk), id_nn, kk != 0);
+                        ptx::umma_commit(dq_full);
+                        ATRACE(1, it, 10);
+                    }
+#pragma unroll
+                    for (int k4 = 0; k4 < 4; ++k4) {
+                        const int kk = h * 4 + k4;
+                        ptx::umma_f16(t_dk, kmajor_desc(sds, kk), mnmajor_desc(sq, kk), id_kn, (it | kk) != 0);
+                    }
                 }
-                ptx::umma_commit(qo_empty);
-                // dQ_i into the dP^T columns (consumed once p_full fired)
-#pragma unroll
-                for (int kk = 0; kk < BKV / 16; ++kk)
-                    ptx::umma_f16(t_dp, mnmajor_desc(sds, kk), mnmajor_desc(sk, kk), id_nn, kk != 0);
-                ptx::umma_commit(dq_full);
+                ptx::umma_commit(&q_empty[st]);
+                ATRACE(1, it, 11);
             }
         }
-    } else {
+    } else if (warp < 6) {
+        // ===== dQ drain: thread = head dim d (TMEM lane); warp q4 owns dims q4*32..q4*32+31 =====
         const int q4 = warp & 3;
-        const int r = q4 * 32 + lane;  // TMEM lane: key row (S^T, dP^T, dK, dV) or q row (dQ)
+        const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
+        uint8_t* box_ptr = sm + BwdSmem::kDQ + q4 * 8192;  // [64 queries][32 dims] f32, SWIZZLE_128B
+        const uint32_t box = ptx::smem_u32(box_ptr);
+        const uint32_t col = static_cast<uint32_t>(lane & 3) * 4;
+        for (int it = 0; it < n_it; ++it) {
+            const int q0 = (i0 + it) * BQ;
+            if (warp == 2 && lane == 0) ATRACE(2, it, 0);
+            ptx::mbar_wait(dq_full, it & 1);
+            if (warp == 2 && lane == 0) ATRACE(2, it, 1);
+            ptx::tc_fence_after();
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {  // 64 queries per staged box
+                uint32_t v[2][32];
+                ptx::tmem_ld_32x32b_x32(t_dp + lane_off + h * 64, v[0]);
+                ptx::tmem_ld_32x32b_x32(t_dp + lane_off + h * 64 + 32, v[1]);
+                ptx::tmem_ld_wait();
+                if (h == 1) {  // all of dQ^T has left TMEM: the next dP^T may overwrite it
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(dq_empty);
+                }
+                if (lane == 0) ptx::bulk_wait_read<0>();  // the previous reduce has read the box
+                __syncwarp();
+#pragma unroll
+                for (int c2 = 0; c2 < 2; ++c2)
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int ql = c2 * 32 + j;  // row of the box
+                        ptx::st_shared_f32(box + ql * 128 + ((((lane >> 2) ^ ql) & 7) << 4) + col,
+                                           __uint_as_float(v[c2][j]) * scale);
+                    }
+                ptx::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    ptx::tma_reduce_add_2d(&tm_dq, box_ptr, head * D + q4 * 32, row0 + q0 + h * 64);
+                    ptx::bulk_commit();
+                    if (warp == 2) ATRACE(2, it, 2 + h);
+                }
+            }
+        }
+        if (lane == 0) ptx::bulk_wait<0>();
+    } else {
+        // ===== elementwise: thread = key row r, query half h of every 128-query block =====
+        const int q4 = warp & 3, h = (warp - 6) >> 2;
+        const int r = q4 * 32 + lane;
         const int key = kb * BKV + r;
         const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
-        const int tid = threadIdx.x - 64;
-        const uint32_t sp_base = ptx::smem_u32(sm + BwdSmem::kP), sds_base = ptx::smem_u32(sm + BwdSmem::kS);
+        const int e = threadIdx.x - (6 + 4 * h) * 32;  // 0..127 within the half: lse (< 64) or delta
+        const uint32_t sds_base = ptx::smem_u32(sm + BwdSmem::kS);
         const int64_t stat_base = (static_cast<int64_t>(b) * H + head) * S;
-        // LSE / delta of the next query block are loaded one iteration ahead (their global-load
-        // latency was exposed at the top of every iteration)
-        float nxt_l = 0.f, nxt_d = 0.f;
+        const float* stat = e < 64 ? lse : delta;
+        const int eq = e & 63;
+        float nxt = 0.f;
         {
-            const int q = i0 * BQ + tid;
-            if (q < S) {
-                nxt_l = lse[stat_base + q];
-                nxt_d = delta[stat_base + q];
-            }
+            const int q = i0 * BQ + h * 64 + eq;
+            if (q < S) nxt = stat[stat_base + q];
         }
-        for (int i = i0; i < n_qb; ++i) {
-            const int it = i - i0;
-            const int q0 = i * BQ;
-            // double-buffered by iteration: a warp one iteration ahead never overwrites values a
-            // slower warp is still reading (nobody gets two ahead past the barrier below)
-            const uint32_t L = s_lse + (it & 1) * 512;
-            const uint32_t Dl = s_del + (it & 1) * 512;
-            ptx::st_shared_f32(L + 4 * tid, nxt_l);
-            ptx::st_shared_f32(Dl + 4 * tid, nxt_d);
-            if (i + 1 < n_qb) {
-                const int q = q0 + BQ + tid;
-                nxt_l = q < S ? lse[stat_base + q] : 0.f;
-                nxt_d = q < S ? delta[stat_base + q] : 0.f;
+        for (int it = 0; it < n_it; ++it) {
+            const int i = i0 + it;
+            const int qh = i * BQ + h * 64;  // first query of this half
+            // [parity][lse 64 | delta 64]: a warp one iteration ahead never overwrites values a
+            // slower warp of the half still reads (nobody passes the barrier two iterations ahead)
+            reinterpret_cast<float*>(sm + BwdSmem::kStat + h * 1024 + (it & 1) * 512)[e] = -nxt;  // -lse | -delta
+            if (it + 1 < n_it) {
+                const int q = qh + BQ + eq;
+                nxt = q < S ? stat[stat_base + q] : 0.f;
             }
-            named_bar_sync(1, 128);
+            if (lane == 0 && (warp == 6 || warp == 10)) ATRACE(3 + h, it, 0);
+            named_bar_sync(1 + h, 128);
+            if (lane == 0 && (warp == 6 || warp == 10)) ATRACE(3 + h, it, 1);
+            // s_full(i) also orders after every MMA of block i-1 (the readers of dS^T)
             ptx::mbar_wait(s_full, it & 1);
+            if (lane == 0 && (warp == 6 || warp == 10)) ATRACE(3 + h, it, 2);
             ptx::tc_fence_after();
-            const bool mask = (i == i0) || (q0 + BQ > S) || (kb * BKV + BKV > S);
+            const bool mask = (i == i0) || (i * BQ + BQ > S) || (kb * BKV + BKV > S);
+            // valid queries of this thread's key row: key <= q < S, as a [lo, hi) range of the
+            // half's query index (empty when key >= S); a select per element, no branches
+            const int lo = mask ? key - qh : INT_MIN, hi = mask ? S - qh : INT_MAX;
+            const float* Lp = reinterpret_cast<const float*>(sm + BwdSmem::kStat + h * 1024 + (it & 1) * 512);
+            const float* Dp = Lp + 64;
 #pragma unroll 1
-            for (int c = 0; c < 4; ++c) {
+            for (int cc = 0; cc < 2; ++cc) {
                 uint32_t rs[32], rd[32];
-                ptx::tmem_ld_32x32b_x32(t_s + lane_off + c * 32, rs);
-                ptx::tmem_ld_32x32b_x32(t_dp + lane_off + c * 32, rd);
+                ptx::tmem_ld_32x32b_x32(t_s + lane_off + h * 64 + cc * 32, rs);
+                ptx::tmem_ld_32x32b_x32(t_dp + lane_off + h * 64 + cc * 32, rd);
                 ptx::tmem_ld_wait();
                 uint32_t pw[16], dw[16];
-#pragma unroll
-                for (int j = 0; j < 32; j += 2) {
-                    float p[2], d[2];
-#pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        const int ql = c * 32 + j + e;
-                        float pv = ptx::ex2_fast(__uint_as_float(rs[j + e]) * scale_log2 - ptx::ld_shared_f32(L + 4 * ql));
-                        if (mask && (key > q0 + ql || q0 + ql >= S || key >= S)) pv = 0.f;
-                        p[e] = pv;
-                        d[e] = pv * (__uint_as_float(rd[j + e]) - ptx::ld_shared_f32(Dl + 4 * ql));
-                    }
-                    __nv_bfloat162 hp = __floats2bfloat162_rn(p[0], p[1]), hd = __floats2bfloat162_rn(d[0], d[1]);
-                    pw[j / 2] = *reinterpret_cast<uint32_t*>(&hp);
-                    dw[j / 2] = *reinterpret_cast<uint32_t*>(&hd);
-                }
-                // row r of the [2 q-blocks][128 keys][128 B] tiles; chunk c covers q 32c..32c+31
+                if (mask)  // warp-uniform: only diagonal / partial blocks pay for the selects
+                    bwd_elementwise32<true>(rs, rd, Lp + cc * 32, Dp + cc * 32, scale_log2, cc * 32, lo, hi, pw, dw);
+                else
+                    bwd_elementwise32<false>(rs, rd, Lp + cc * 32, Dp + cc * 32, scale_log2, cc * 32, lo, hi, pw, dw);
+                // P^T in place of S^T: the half's 64 queries pack into columns 64h + [0, 32), all of
+                // which this warp has already read
+                ptx::tmem_st_32x32b_x16(t_s + lane_off + h * 64 + cc * 16, pw);
+                // dS^T row r of the [2 q-halves][128 keys][128 B] SW128 tile
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    const int blk = c >> 1, ch = (c & 1) * 4 + u;
-                    const uint32_t off = blk * (kTile / 2) + r * 128 + ((ch ^ (r & 7)) << 4);
-                    ptx::st_shared_v4(sp_base + off, pw[4 * u], pw[4 * u + 1], pw[4 * u + 2], pw[4 * u + 3]);
+                    const int ch = cc * 4 + u;
+                    const uint32_t off = h * (kTile / 2) + r * 128 + ((ch ^ (r & 7)) << 4);
                     ptx::st_shared_v4(sds_base + off, dw[4 * u], dw[4 * u + 1], dw[4 * u + 2], dw[4 * u + 3]);
                 }
             }
+            ptx::tmem_st_wait();
             ptx::fence_proxy_async_smem();
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(p_full);
-            // drain dQ_i (TMEM lane = q row) into the f32 accumulator
-            ptx::mbar_wait(dq_full, it & 1);
-            ptx::tc_fence_after();
-            const int q = q0 + r;
-            float* dst = dq_acc + static_cast<int64_t>(row0 + q) * HD + head * D;
-#pragma unroll 1
-            for (int c = 0; c < 4; ++c) {
-                uint32_t rq[32];
-                ptx::tmem_ld_32x32b_x32(t_dp + lane_off + c * 32, rq);
-                ptx::tmem_ld_wait();
-                if (q < S) {
-#pragma unroll
-                    for (int j = 0; j < 32; j += 4)
-                        red_add_v4(dst + c * 32 + j, __uint_as_float(rq[j]) * scale, __uint_as_float(rq[j + 1]) * scale,
-                                   __uint_as_float(rq[j + 2]) * scale, __uint_as_float(rq[j + 3]) * scale);
-                }
-            }
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(dq_empty);
+            if (lane == 0) ptx::mbar_arrive(&p_full[h]);
+            if (lane == 0 && (warp == 6 || warp == 10)) ATRACE(3 + h, it, 3);
         }
-        // dK (scaled) and dV for this thread's key row. tcgen05.ld is warp-collective
-        // (.sync.aligned): every lane loads, only rows inside the sequence store.
+        // dK (scaled) and dV: every MMA has completed once the last block's q_empty commit fires
+        // (its previous phase, block n-3, completed before s_full of block n-1)
+        {
+            const int last = n_it - 1;
+            ptx::mbar_wait(&q_empty[last & 1], (last >> 1) & 1);
+        }
         ptx::tc_fence_after();
         __nv_bfloat16* dkr = dqkv + static_cast<int64_t>(row0 + key) * 3 * HD + HD + head * D;
         __nv_bfloat16* dvr = dqkv + static_cast<int64_t>(row0 + key) * 3 * HD + 2 * HD + head * D;
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
+        for (int cc = 0; cc < 2; ++cc) {
+            const int c0 = h * 64 + cc * 32;
             uint32_t rk[32], rv[32];
-            ptx::tmem_ld_32x32b_x32(t_dk + lane_off + c * 32, rk);
-            ptx::tmem_ld_32x32b_x32(t_dv + lane_off + c * 32, rv);
+            ptx::tmem_ld_32x32b_x32(t_dk + lane_off + c0, rk);
+            ptx::tmem_ld_32x32b_x32(t_dv + lane_off + c0, rv);
             ptx::tmem_ld_wait();
             if (key >= S) continue;
 #pragma unroll
@@ -539,8 +658,8 @@ __global__ void __launch_bounds__(192, 1)
                     wk[u] = *reinterpret_cast<uint32_t*>(&a);
                     wv[u] = *reinterpret_cast<uint32_t*>(&v);
                 }
-                *reinterpret_cast<uint4*>(dkr + c * 32 + j) = ok;
-                *reinterpret_cast<uint4*>(dvr + c * 32 + j) = ov;
+                *reinterpret_cast<uint4*>(dkr + c0 + j) = ok;
+                *reinterpret_cast<uint4*>(dvr + c0 + j) = ov;
             }
         }
     }
@@ -561,13 +680,14 @@ void attention_bwd_tc(const void* qkv, const void* dout, const float* lse, const
     }
     const int64_t T = static_cast<int64_t>(batch) * seq, HD = static_cast<int64_t>(heads) * head_dim;
     const CUtensorMap tq = make_tma_2d(qkv, 3 * HD, T, 3 * HD, 128, false);
-    const CUtensorMap to = make_tma_2d(dout, HD, T, HD, 128, false);
+    const CUtensorMap to64 = make_tma_2d(dout, HD, T, HD, 64, false);  // dO loaded per 64-row half
     dim3 grid(heads, (seq + BKV - 1) / BKV, batch);
     if (heads > 1 && seq > BKV) count_variant(KV_ATTN_BWD_MULTI);
     const float scale = 1.f / sqrtf(static_cast<float>(head_dim));
-    attn_bwd_tc_kernel<<<grid, 192, BwdSmem::kBytes, st>>>(tq, to, lse, delta, dq_acc,
-                                                           static_cast<__nv_bfloat16*>(dqkv), seq, heads, scale,
-                                                           scale * kLog2e);
+    const CUtensorMap tdq = make_tma_2d(dq_acc, HD, T, HD, 64, true);
+    attn_bwd_tc_kernel<<<grid, 448, BwdSmem::kBytes, st>>>(tq, to64, tdq, lse, delta,
+                                                             static_cast<__nv_bfloat16*>(dqkv), seq, heads, scale,
+                                                             scale * kLog2e);
 }
 
 }  // namespace bfpp
