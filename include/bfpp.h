@@ -70,6 +70,16 @@ const char* bfpp_last_error(void);
 /* replaces ParallelConfig::validate(model[, cluster]) (types.cpp:92-130); cluster may be NULL */
 int bfpp_validate(const bfpp_model_spec* m, const bfpp_parallel_config* c, const bfpp_cluster_spec* cl);
 
+/* replaces total_memory (memory.hpp / memory.cpp:72-80): out[4] = state, activation, checkpoint,
+ * total bytes per device of the reference's analytic model (MemoryOptions::dp0_bytes_per_param) */
+int bfpp_total_memory(const bfpp_model_spec* m, const bfpp_parallel_config* c, double dp0_bytes_per_param,
+                      double* out);
+/* replaces feasible (memory.cpp:82-86): *out = total <= headroom * cl->mem_capacity */
+int bfpp_feasible(const bfpp_model_spec* m, const bfpp_parallel_config* c, const bfpp_cluster_spec* cl,
+                  double dp0_bytes_per_param, double headroom, int32_t* out);
+/* replaces cluster_preset (types.cpp:206-231): "a100", "v100-dgx1", and "b200" (new) */
+int bfpp_cluster_preset(const char* name, bfpp_cluster_spec* out);
+
 /* replaces place_stages (schedule.hpp:20, schedule.cpp:23-33). assignment_out
  * receives n_stage entries (cap must be >= n_pp*n_loop). */
 int bfpp_place_stages(const bfpp_model_spec* m, const bfpp_parallel_config* c, int64_t* assignment_out,
@@ -213,6 +223,9 @@ int bfpp_adam_update(float* p, float* m, float* v, float* g, void* w16, int64_t 
 #define BFPP_NCCL_UID_BYTES 128
 #define BFPP_EXEC_SKIP_OPTIMIZER 1  /* flags: keep gradients, do not run Adam */
 #define BFPP_EXEC_PROFILE_KERNELS 2 /* flags: CUDA events around every kernel -> bfpp_exec_kernel_stats */
+#define BFPP_EXEC_RECOMPUTE 4       /* flags: activation checkpointing -- keep each layer's output only,
+                                       recompute the layer (and LM-head logits) in the backward
+                                       (checkpoint = 2 s h bytes, memory.cpp:64-70) */
 
 typedef struct bfpp_exec_opts {
     int32_t device;          /* CUDA ordinal of this rank */
@@ -235,6 +248,18 @@ int bfpp_exec_create(const bfpp_model_spec* m, const bfpp_parallel_config* c, co
 int bfpp_exec_create_graph(const bfpp_model_spec* m, const bfpp_parallel_config* c, const bfpp_graph* g,
                            const bfpp_exec_opts* o, int32_t rank, int32_t world, const void* uids,
                            bfpp_exec** out);
+/* Device bytes one rank of (m, c, o->flags) allocates, by category (bytes[8]: 0 bf16 compute
+ * weights / DP_FS reconstruction slots, 1 f32 gradient buffers, 2 f32 master + Adam moments,
+ * 3 reduced-gradient shards and reduce-scatter buffers, 4 bf16 all-gather source shards,
+ * 5 activation sets (full, or checkpoints with BFPP_EXEC_RECOMPUTE), 6 pipeline receive arena and
+ * send buffers, 7 scratch) and sets[2] = {pooled activation sets (= peak live (micro-batch, stage)
+ * pairs in program order, simulate.cpp:166-191's peak_inflight in stages), pooled logits sets}.
+ * Sizing only: no GPU is needed (the executor's allocation code run without allocating); the
+ * figure to hold against the reference's total_memory / feasible (memory.cpp:72-86). */
+int bfpp_exec_memory_plan(const bfpp_model_spec* m, const bfpp_parallel_config* c, const bfpp_exec_opts* o,
+                          int32_t rank, int64_t* bytes, int64_t* sets);
+/* the same breakdown of a live executor (its allocations) */
+int bfpp_exec_memory(const bfpp_exec* e, int64_t* bytes, int64_t* sets);
 /* One training step (forward, backward, gradient reduction, Adam) over this replica's
  * tokens [n_mb][s_mb][s_seq+1] int32 (inputs = [..., :-1], labels = [..., 1:]).
  * bfpp_exec_step takes HOST tokens and returns the replica's mean token loss on the
@@ -273,9 +298,9 @@ int bfpp_exec_timeline(const bfpp_exec* e, double* start, double* end);
  * cross-stream waits (CSR). Two-phase sizing: call with cap = 0 to get *n_tasks and *n_waits,
  * then pass cap >= n_tasks (ids, streams, flags, slots: cap entries; wait_offsets: cap + 1) and
  * wait_cap >= n_waits (wait_ids); smaller capacities fail with status 2 and write nothing. */
-int bfpp_plan_rank(const bfpp_graph* g, int64_t pp_rank, int64_t n_dp, int64_t cap, int64_t wait_cap, int32_t* ids,
-                   int32_t* streams, int32_t* flags, int32_t* slots, int32_t* wait_offsets, int32_t* wait_ids,
-                   int64_t* n_tasks, int64_t* n_waits);
+int bfpp_plan_rank(const bfpp_graph* g, int64_t pp_rank, int64_t n_dp, int32_t dp_variant, int64_t cap,
+                   int64_t wait_cap, int32_t* ids, int32_t* streams, int32_t* flags, int32_t* slots,
+                   int32_t* wait_offsets, int32_t* wait_ids, int64_t* n_tasks, int64_t* n_waits);
 
 /* toggles per-task timeline events and per-kernel profiling for subsequent steps */
 int bfpp_exec_set_flags(bfpp_exec* e, int32_t record_timeline, int32_t profile_kernels);

@@ -14,6 +14,7 @@
 #include <string>
 
 #include "../include/bfpp.h"
+#include "pipesim/memory.hpp"
 #include "pipesim/perf.hpp"
 #include "pipesim/report.hpp"
 #include "pipesim/search.hpp"
@@ -197,6 +198,46 @@ int ref_peak_inflight(const bfpp_model_spec* m, const bfpp_parallel_config* c, c
 
 double ref_compute_per_gpu(const bfpp_model_spec* m, const bfpp_parallel_config* c) {
     return compute_per_gpu(model_of(m), config_of(c));
+}
+
+// total_memory / feasible / cluster_preset (memory.cpp:72-86, types.cpp:206-231)
+int ref_total_memory(const bfpp_model_spec* m, const bfpp_parallel_config* c, double dp0_bytes_per_param,
+                     double* out) {
+    return guard([&] {
+        MemoryOptions o;
+        o.dp0_bytes_per_param = dp0_bytes_per_param;
+        const MemoryBreakdown b = total_memory(model_of(m), config_of(c), o);
+        out[0] = b.state_bytes;
+        out[1] = b.activation_bytes;
+        out[2] = b.checkpoint_bytes;
+        out[3] = b.total_bytes;
+    });
+}
+
+int ref_feasible(const bfpp_model_spec* m, const bfpp_parallel_config* c, double mem_capacity,
+                 double dp0_bytes_per_param, double headroom, int32_t* out) {
+    return guard([&] {
+        MemoryOptions o;
+        o.dp0_bytes_per_param = dp0_bytes_per_param;
+        o.headroom = headroom;
+        ClusterSpec k;
+        k.mem_capacity = mem_capacity;
+        *out = feasible(model_of(m), config_of(c), k, o) ? 1 : 0;
+    });
+}
+
+int ref_cluster_preset(const char* name, bfpp_cluster_spec* out) {
+    return guard([&] {
+        const ClusterSpec k = cluster_preset(name);
+        out->n_node = k.n_node;
+        out->s_node = k.s_node;
+        out->peak_flops = k.peak_flops;
+        out->bw_intra = k.bw_intra;
+        out->bw_inter = k.bw_inter;
+        out->pp_latency = k.pp_latency;
+        out->mem_capacity = k.mem_capacity;
+        out->kernel_efficiency = k.kernel_efficiency;
+    });
 }
 
 // CPU baseline: seconds per place_stages+build_tasks and per simulate, median-free

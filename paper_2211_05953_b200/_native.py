@@ -80,10 +80,15 @@ _PROTOS = {
     "bfpp_bubble_fraction": (C.c_double, [_P]),
     "bfpp_peak_inflight": (C.c_int, [_P, _P, C.c_int64, _I64P]),
     "bfpp_compute_per_gpu": (C.c_double, [C.POINTER(ModelSpecC), C.POINTER(ParallelConfigC)]),
+    "bfpp_total_memory": (C.c_int, [C.POINTER(ModelSpecC), C.POINTER(ParallelConfigC), C.c_double, _DP]),
+    "bfpp_feasible": (C.c_int, [C.POINTER(ModelSpecC), C.POINTER(ParallelConfigC), C.POINTER(ClusterSpecC),
+                                C.c_double, C.c_double, _I32P]),
+    "bfpp_cluster_preset": (C.c_int, [C.c_char_p, C.POINTER(ClusterSpecC)]),
     "bfpp_chrome_trace_json": (C.c_int, [_P, _P, C.c_char_p, C.c_int64, _I64P]),
     "bfpp_gantt_svg": (C.c_int, [_P, _P, C.c_char_p, C.c_int64, _I64P]),
     "bfpp_measured_timing_model": (C.c_int, [_P, _P, C.POINTER(TimingModelC)]),
-    "bfpp_plan_rank": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64, C.c_int64] + [_I32P] * 6 + [_I64P, _I64P]),
+    "bfpp_plan_rank": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int32, C.c_int64, C.c_int64] + [_I32P] * 6
+                       + [_I64P, _I64P]),
 }
 
 _lib = None

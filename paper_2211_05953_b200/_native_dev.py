@@ -64,6 +64,9 @@ PROTOS.update({
     "bfpp_exec_local_stage": (_I64, [_P, _I64]),
     "bfpp_exec_stage_numel": (_I64, [_P, _I64]),
     "bfpp_exec_device_bytes": (_I64, [_P]),
+    "bfpp_exec_memory_plan": (C.c_int, [C.POINTER(ModelSpecC), C.POINTER(ParallelConfigC), C.POINTER(ExecOptsC), _I32,
+                                        C.POINTER(_I64), C.POINTER(_I64)]),
+    "bfpp_exec_memory": (C.c_int, [_P, C.POINTER(_I64), C.POINTER(_I64)]),
     "bfpp_exec_set_params": (C.c_int, [_P, _I64, _P, _I64]),
     "bfpp_exec_get_params": (C.c_int, [_P, _I64, _P, _I64, C.POINTER(_I64), C.POINTER(_I64)]),
     "bfpp_exec_get_grads": (C.c_int, [_P, _I64, _P, _I64, C.POINTER(_I64), C.POINTER(_I64)]),

@@ -45,6 +45,7 @@ int create(const bfpp_model_spec* m, const bfpp_parallel_config* c, const bfpp_g
         eo.init_std = o->init_std;
         eo.skip_optimizer = (o->flags & BFPP_EXEC_SKIP_OPTIMIZER) != 0;
         eo.profile_kernels = (o->flags & BFPP_EXEC_PROFILE_KERNELS) != 0;
+        eo.recompute = (o->flags & BFPP_EXEC_RECOMPUTE) != 0;
         std::vector<ncclUniqueId> ids;
         if (uids) {
             const int64_t n = bfpp_exec_n_comm_ids(c);
@@ -66,6 +67,31 @@ int bfpp_exec_create_graph(const bfpp_model_spec* m, const bfpp_parallel_config*
                            const bfpp_exec_opts* o, int32_t rank, int32_t world, const void* uids,
                            bfpp_exec** out) {
     return create(m, c, g, o, rank, world, uids, out);
+}
+
+namespace {
+void copy_plan(const MemoryPlan& mp, int64_t* bytes, int64_t* sets) {
+    for (int k = 0; k < M_NCAT; ++k) bytes[k] = static_cast<int64_t>(mp.bytes[k]);
+    sets[0] = mp.activation_sets;
+    sets[1] = mp.head_sets;
+}
+}  // namespace
+
+int bfpp_exec_memory_plan(const bfpp_model_spec* m, const bfpp_parallel_config* c, const bfpp_exec_opts* o,
+                          int32_t rank, int64_t* bytes, int64_t* sets) {
+    return guarded([&] {
+        ExecOptions eo;
+        eo.skip_optimizer = (o->flags & BFPP_EXEC_SKIP_OPTIMIZER) != 0;
+        eo.recompute = (o->flags & BFPP_EXEC_RECOMPUTE) != 0;
+        eo.dry_run = true;
+        const ParallelConfig pc = to_config(c);
+        Executor x(to_model(m), pc, eo, rank, static_cast<int>(pc.grid_size()), {}, nullptr);
+        copy_plan(x.memory_plan(), bytes, sets);
+    });
+}
+
+int bfpp_exec_memory(const bfpp_exec* e, int64_t* bytes, int64_t* sets) {
+    return guarded([&] { copy_plan(e->x->memory_plan(), bytes, sets); });
 }
 
 int bfpp_exec_step(bfpp_exec* e, const int32_t* tokens_host, float* loss) {
@@ -111,12 +137,15 @@ int bfpp_exec_timeline(const bfpp_exec* e, double* start, double* end) {
     return guarded([&] { e->x->timeline(start, end); });
 }
 
-int bfpp_plan_rank(const bfpp_graph* g, int64_t pp_rank, int64_t n_dp, int64_t cap, int64_t wait_cap, int32_t* ids,
-                   int32_t* streams, int32_t* flags, int32_t* slots, int32_t* wait_offsets, int32_t* wait_ids,
-                   int64_t* n_tasks, int64_t* n_waits) {
+int bfpp_plan_rank(const bfpp_graph* g, int64_t pp_rank, int64_t n_dp, int32_t dp_variant, int64_t cap,
+                   int64_t wait_cap, int32_t* ids, int32_t* streams, int32_t* flags, int32_t* slots,
+                   int32_t* wait_offsets, int32_t* wait_ids, int64_t* n_tasks, int64_t* n_waits) {
     return guarded([&] {
         if (pp_rank < 0 || pp_rank >= g->g.n_devices) throw SpecError("plan: pipeline rank out of range");
-        const std::vector<PlanTask> plan = plan_rank(g->g, pp_rank, n_dp);
+        if (dp_variant < 0 || dp_variant > 2) throw SpecError("plan: dp_variant out of range");
+        // the executor pools the gradient buffers of the sharded variants (see plan.hpp)
+        const bool pooled = n_dp >= 2 && dp_variant != static_cast<int32_t>(DpVariant::DP0);
+        const std::vector<PlanTask> plan = plan_rank(g->g, pp_rank, n_dp, pooled);
         int64_t nw = 0;
         for (const PlanTask& p : plan) nw += static_cast<int64_t>(p.waits.size());
         *n_tasks = static_cast<int64_t>(plan.size());
@@ -131,7 +160,7 @@ int bfpp_plan_rank(const bfpp_graph* g, int64_t pp_rank, int64_t n_dp, int64_t c
             streams[i] = p.stream;
             flags[i] = (p.send ? 1 : 0) | (p.first_unit ? 2 : 0) | (p.last_unit ? 4 : 0) | (p.adam_after ? 8 : 0) |
                        (p.first_in_unit ? 16 : 0) | (p.adam_tail ? 32 : 0) | (p.last_unit_bwd ? 64 : 0) |
-                       (p.reduce_first_unit ? 128 : 0);
+                       (p.reduce_first_unit ? 128 : 0) | (p.unit_end_bwd ? 256 : 0);
             slots[i] = p.slot;
             wait_offsets[i] = k;
             for (TaskId w : p.waits) wait_ids[k++] = w;

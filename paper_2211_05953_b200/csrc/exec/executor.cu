@@ -176,12 +176,13 @@ struct LocalStage {
     // segment s of rank r = [seg[s] + r * len_s / n_dp, + len_s / n_dp) -> shard offset seg[s] / n_dp.
     std::vector<int64_t> seg;
     std::vector<char> seg_done;  // segments already reduced (and updated) in the current step
+    std::vector<cudaEvent_t> seg_ev;  // per segment: its latest reduce-scatter has read the gradient
     int64_t nd = 1, r = 0;       // shard degree and this rank's slice (1, 0 when not sharded)
+    int n_units = 0;             // reduction units of this stage per step (Reduce tasks)
     bf16* w16 = nullptr;      // resident compute weights (not DP_FS with n_dp >= 2)
-    float* grad = nullptr;    // full f32 gradient (accumulated across micro-batches)
+    float* grad = nullptr;    // full f32 gradient (accumulated across micro-batches; pooled: inside gbuf)
     float *master = nullptr, *m = nullptr, *v = nullptr;  // f32 optimizer shard
-    float* gshard = nullptr;  // reduced gradient shard (n_dp >= 2, sharded variants)
-    float* gtmp = nullptr;    // reduce-scatter landing buffer when a stage reduces several times
+    float* gshard = nullptr;  // reduced gradient shard (sharded variants; null = transient per segment)
     bf16* w16_shard = nullptr;
 };
 
@@ -217,15 +218,19 @@ void all_gather_segments(const LocalStage& ls, bf16* dst, size_t s0, size_t s1, 
     NK(ncclGroupEnd());
 }
 
-// f32 gradients of segments [s0, s1): summed over the ranks, this rank's slices -> dst (shard layout)
+// f32 gradients of segments [s0, s1): summed over the ranks, this rank's slices -> dst (shard
+// layout, shifted down by `shift` elements); each segment's event is recorded once they are read
 void reduce_scatter_segments(const LocalStage& ls, float* dst, size_t s0, size_t s1, ncclComm_t comm,
-                             cudaStream_t st) {
+                             cudaStream_t st, int64_t shift = 0) {
     NK(ncclGroupStart());
     for (size_t s = s0; s < s1; ++s) {
         const size_t n = static_cast<size_t>((ls.seg[s + 1] - ls.seg[s]) / ls.nd);
-        NK(ncclReduceScatter(ls.grad + ls.seg[s], dst + ls.seg[s] / ls.nd, n, ncclFloat32, ncclSum, comm, st));
+        NK(ncclReduceScatter(ls.grad + ls.seg[s], dst + ls.seg[s] / ls.nd - shift, n, ncclFloat32, ncclSum, comm,
+                             st));
     }
     NK(ncclGroupEnd());
+    for (size_t s = s0; s < s1; ++s)
+        if (s < ls.seg_ev.size()) CK(cudaEventRecord(ls.seg_ev[s], st));
 }
 
 using TaskExec = PlanTask;
@@ -278,13 +283,29 @@ struct Executor::Impl {
     std::vector<cudaEvent_t> ev_pool;
     std::vector<Mark> marks;
 
+    // pooled f32 gradient buffer of the sharded variants + transient shard buffers (DP stream)
+    float* gbuf = nullptr;
+    int64_t gbuf_n = 0;
+    float* gtmp = nullptr;  // reduce-scatter landing buffer of stages that reduce several times
+    float* gseg = nullptr;  // per-segment reduced gradient of single-unit stages (then Adam)
+
+    bool dry = false;  // sizing only (ExecOptions::dry_run): no device memory is touched
+    uintptr_t fake = 0x10000;
+    MemoryPlan* mem = nullptr;
+    size_t* total = nullptr;
     template <class T>
-    T* alloc(size_t n, size_t* total) {
-        void* p = nullptr;
+    T* alloc(size_t n, int cat) {
         const size_t bytes = std::max<size_t>(n * sizeof(T), 256);
+        mem->bytes[cat] += bytes;
+        *total += bytes;
+        if (dry) {
+            void* p = reinterpret_cast<void*>(fake);
+            fake += (bytes + 255) / 256 * 256;
+            return static_cast<T*>(p);
+        }
+        void* p = nullptr;
         CK(cudaMalloc(&p, bytes));
         allocs.push_back(p);
-        *total += bytes;
         return static_cast<T*>(p);
     }
 };
@@ -331,6 +352,231 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
     for (i64 s = 0; s < pl_.n_stage; ++s)
         layouts_.push_back(make_stage_layout(m_, s, pl_.n_stage, pl_.layers_per_stage, c_.n_dp));
 
+    Impl& I = *impl_;
+    I.dev = o.device;
+    I.dry = o.dry_run;
+    I.mem = &mem_;
+    I.total = &dev_bytes_;
+    if (const char* e = getenv("BFPP_WGRAD_STREAM")) I.wgrad_stream = atoi(e) != 0;
+    if (const char* e = getenv("BFPP_EXEC_DEBUG")) I.debug = atoi(e) != 0;
+    // recompute: one working set per rank, so weight gradients stay on the compute stream
+    if (o_.recompute) I.wgrad_stream = false;
+    const bool fs = c_.n_dp >= 2 && c_.dp_variant == DpVariant::DP_FS;
+    // sharded variants: gradients are consumed by reduce-scatters, so the rank's stages share one
+    // f32 gradient buffer (reused per segment as the previous unit's reduce-scatters drain it)
+    const bool pooled = c_.n_dp >= 2 && c_.dp_variant != DpVariant::DP0;
+
+    // ---- per-task execution plan (host only) ----
+    I.order = plan_rank(graph_, pp_rank_, c_.n_dp, pooled);
+
+    // ---- parameters, gradients, optimizer shards ----
+    int64_t max_padded = 0;
+    std::vector<int> n_units(static_cast<size_t>(v_), 0);  // reduction units per local stage
+    for (const Task& t : graph_.tasks)
+        if (t.kind == TaskKind::Reduce && t.device == pp_rank_) ++n_units[static_cast<size_t>(t.stage / p_)];
+    for (i64 cc = 0; cc < v_; ++cc) max_padded = std::max(max_padded, layouts_[static_cast<size_t>(local_stage(cc))].padded);
+    int64_t gtmp_n = 0, gseg_n = 0;
+    for (i64 cc = 0; cc < v_; ++cc) {
+        LocalStage ls;
+        ls.stage = local_stage(cc);
+        const StageLayout& L = layouts_[static_cast<size_t>(ls.stage)];
+        ls.shard_n = pooled ? L.padded / c_.n_dp : L.padded;
+        ls.seg = pooled ? shard_segments(L, c_.n_dp) : std::vector<int64_t>{0, L.padded};
+        ls.seg_done.assign(ls.seg.size() - 1, 0);
+        ls.nd = pooled ? c_.n_dp : 1;
+        ls.r = pooled ? dp_rank_ : 0;
+        ls.n_units = n_units[static_cast<size_t>(cc)];
+        if (!fs) ls.w16 = I.alloc<bf16>(static_cast<size_t>(L.padded), M_WEIGHTS);
+        if (!pooled) ls.grad = I.alloc<float>(static_cast<size_t>(L.padded), M_GRADS);
+        ls.master = I.alloc<float>(static_cast<size_t>(ls.shard_n), M_OPTIMIZER);
+        ls.m = I.alloc<float>(static_cast<size_t>(ls.shard_n), M_OPTIMIZER);
+        ls.v = I.alloc<float>(static_cast<size_t>(ls.shard_n), M_OPTIMIZER);
+        if (pooled) {
+            // the reduced gradient persists across units only when the stage reduces more than
+            // once (DF / GPipe / 1F1B units); a single unit is reduced and updated segment by
+            // segment through a transient buffer (kept whole when the optimizer is skipped, so
+            // the gradients can be read back)
+            if (ls.n_units > 1 || o_.skip_optimizer) {
+                ls.gshard = I.alloc<float>(static_cast<size_t>(ls.shard_n), M_GRAD_SHARDS);
+            } else {
+                for (size_t si = 0; si + 1 < ls.seg.size(); ++si)
+                    gseg_n = std::max(gseg_n, (ls.seg[si + 1] - ls.seg[si]) / ls.nd);
+            }
+            if (ls.n_units > 1) gtmp_n = std::max(gtmp_n, ls.shard_n);
+            ls.w16_shard = I.alloc<bf16>(static_cast<size_t>(ls.shard_n), M_WEIGHT_SHARDS);
+        }
+        I.local.push_back(ls);
+    }
+    if (pooled) {
+        I.gbuf = I.alloc<float>(static_cast<size_t>(max_padded), M_GRADS);
+        I.gbuf_n = max_padded;
+        for (auto& ls : I.local)  // right-aligned: every stage's gradient ends at the buffer end
+            ls.grad = I.gbuf + (max_padded - layouts_[static_cast<size_t>(ls.stage)].padded);
+        if (gtmp_n) I.gtmp = I.alloc<float>(static_cast<size_t>(gtmp_n), M_GRAD_SHARDS);
+        if (gseg_n) I.gseg = I.alloc<float>(static_cast<size_t>(gseg_n), M_GRAD_SHARDS);
+    }
+    if (fs)
+        for (auto& sl : I.slots) sl = I.alloc<bf16>(static_cast<size_t>(max_padded), M_WEIGHTS);
+
+    // ---- activations: pooled sets of the live (micro-batch, local stage) pairs ----
+    // A forward takes a set, the backward of the same (micro-batch, stage) returns it; set ids are
+    // assigned once by walking this device's compute program (the same every step), so the pool
+    // holds peak_inflight sets (simulate.cpp:166-191) and reuse is ordered by the compute stream.
+    const int64_t T = c_.s_mb * m_.s_seq, h = m_.s_hidden, mlp = m_.s_mlp, V = m_.s_voc, H = m_.n_heads;
+    const size_t Th = static_cast<size_t>(T * h);
+    const i64 last_stage = pl_.n_stage - 1;
+    const bool has_last = pl_.device_of(last_stage) == pp_rank_;
+    std::vector<int> set_of(static_cast<size_t>(c_.n_mb * v_), -1), head_of(static_cast<size_t>(c_.n_mb), -1);
+    {
+        std::vector<int> used, hused;
+        auto take = [](std::vector<int>& u) {
+            for (size_t k = 0; k < u.size(); ++k)
+                if (!u[k]) {
+                    u[k] = 1;
+                    return static_cast<int>(k);
+                }
+            u.push_back(1);
+            return static_cast<int>(u.size() - 1);
+        };
+        for (TaskId id : graph_.compute_program[static_cast<size_t>(pp_rank_)]) {
+            const Task& t = graph_.tasks[static_cast<size_t>(id)];
+            const size_t key = static_cast<size_t>(t.micro_batch * v_ + t.stage / p_);
+            const bool head = t.stage == last_stage && !o_.recompute;
+            if (t.kind == TaskKind::Fwd) {
+                set_of[key] = take(used);
+                if (head) head_of[static_cast<size_t>(t.micro_batch)] = take(hused);
+            } else {
+                used[static_cast<size_t>(set_of[key])] = 0;
+                if (head) hused[static_cast<size_t>(head_of[static_cast<size_t>(t.micro_batch)])] = 0;
+            }
+        }
+        mem_.activation_sets = static_cast<int64_t>(used.size());
+        mem_.head_sets = static_cast<int64_t>(hused.size());
+    }
+    const i64 lps = pl_.layers_per_stage;
+    // one activation set: per layer either everything the backward reads (no recompute) or only
+    // the layer output (the checkpoint; the next layer's input)
+    struct LayerSet {
+        std::vector<LayerActs> layers;
+    };
+    auto make_layer_acts = [&](int cat) {
+        LayerActs la{};
+        la.ln1 = I.alloc<bf16>(Th, cat);
+        la.qkv = I.alloc<bf16>(3 * Th, cat);
+        la.o = I.alloc<bf16>(Th, cat);
+        la.x_mid = I.alloc<bf16>(Th, cat);
+        la.ln2 = I.alloc<bf16>(Th, cat);
+        la.pre = I.alloc<bf16>(static_cast<size_t>(T * mlp), cat);
+        la.act = I.alloc<bf16>(static_cast<size_t>(T * mlp), cat);
+        la.mu1 = I.alloc<float>(static_cast<size_t>(T), cat);
+        la.rs1 = I.alloc<float>(static_cast<size_t>(T), cat);
+        la.mu2 = I.alloc<float>(static_cast<size_t>(T), cat);
+        la.rs2 = I.alloc<float>(static_cast<size_t>(T), cat);
+        la.lse = I.alloc<float>(static_cast<size_t>(T * H), cat);
+        return la;
+    };
+    LayerActs work{};  // recompute: the one working set
+    if (o_.recompute) work = make_layer_acts(M_SCRATCH);
+    std::vector<LayerSet> sets(static_cast<size_t>(mem_.activation_sets));
+    for (auto& st : sets)
+        for (i64 l = 0; l < lps; ++l) {
+            LayerActs la = o_.recompute ? work : make_layer_acts(M_ACTIVATIONS);
+            la.x_out = I.alloc<bf16>(Th, M_ACTIVATIONS);
+            st.layers.push_back(la);
+        }
+    struct HeadSet {
+        bf16 *lnf, *logits;
+        float *muf, *rsf;
+    };
+    auto make_head = [&](int cat) {
+        HeadSet hs{};
+        hs.lnf = I.alloc<bf16>(Th, cat);
+        hs.muf = I.alloc<float>(static_cast<size_t>(T), cat);
+        hs.rsf = I.alloc<float>(static_cast<size_t>(T), cat);
+        hs.logits = I.alloc<bf16>(static_cast<size_t>(T * V), cat);
+        return hs;
+    };
+    std::vector<HeadSet> heads;
+    if (has_last) {
+        if (o_.recompute)
+            heads.push_back(make_head(M_SCRATCH));
+        else
+            for (int64_t k = 0; k < mem_.head_sets; ++k) heads.push_back(make_head(M_ACTIVATIONS));
+    }
+
+    I.acts.assign(static_cast<size_t>(c_.n_mb), std::vector<StageActs>(static_cast<size_t>(v_)));
+    // receive slot (dir 0 = forward activation, 1 = backward gradient) of (mb, local stage c)
+    auto slot = [&](int dir, i64 mb, i64 cc) { return static_cast<size_t>((mb * v_ + cc) * 2 + dir); };
+    const size_t n_slots = static_cast<size_t>(c_.n_mb * v_ * 2);
+    if (p_ >= 2) {
+        const size_t arena = n_slots * Th * sizeof(bf16), flags = n_slots * sizeof(uint32_t) + 256;
+        if (!I.dry) {
+            CK(cudaSetDevice(I.dev));
+            CK(cudaMalloc(&I.recv_arena, arena));
+            CK(cudaMalloc(&I.recv_flags, flags));
+            CK(cudaMemset(I.recv_flags, 0, n_slots * sizeof(uint32_t)));
+        }
+        mem_.bytes[M_PP_BUFFERS] += arena + flags;
+        dev_bytes_ += arena + flags;
+    }
+    for (i64 mb = 0; mb < c_.n_mb; ++mb) {
+        for (i64 cc = 0; cc < v_; ++cc) {
+            StageActs& a = I.acts[static_cast<size_t>(mb)][static_cast<size_t>(cc)];
+            const i64 s = local_stage(cc);
+            const StageLayout& L = layouts_[static_cast<size_t>(s)];
+            const LayerSet& set = sets[static_cast<size_t>(set_of[static_cast<size_t>(mb * v_ + cc)])];
+            // input: aliases the previous stage's output when both live on this device
+            if (s > 0 && pl_.device_of(s - 1) == pp_rank_)
+                a.in = I.acts[static_cast<size_t>(mb)][static_cast<size_t>(cc - 1)].out;
+            else if (s > 0)
+                a.in = I.recv_arena + slot(0, mb, cc) * Th;  // written by the previous rank's copy engine
+            else
+                a.in = I.alloc<bf16>(Th, M_ACTIVATIONS);     // embedding output
+            bf16* x = a.in;
+            for (size_t l = 0; l < L.layers.size(); ++l) {
+                LayerActs la = set.layers[l];
+                la.x_in = x;
+                x = la.x_out;
+                a.layers.push_back(la);
+            }
+            a.out = x;
+            if (L.last) {
+                const HeadSet& hs = heads[o_.recompute ? 0 : static_cast<size_t>(head_of[static_cast<size_t>(mb)])];
+                a.lnf = hs.lnf;
+                a.muf = hs.muf;
+                a.rsf = hs.rsf;
+                a.logits = hs.logits;
+            }
+            if (!L.first) a.gout = I.alloc<bf16>(Th, M_PP_BUFFERS);
+        }
+        // gin: the next stage's gout when it lives on this device, else a receive buffer
+        for (i64 cc = 0; cc < v_; ++cc) {
+            StageActs& a = I.acts[static_cast<size_t>(mb)][static_cast<size_t>(cc)];
+            const i64 s = local_stage(cc);
+            if (s == pl_.n_stage - 1) continue;
+            if (pl_.device_of(s + 1) == pp_rank_)
+                a.gin = I.acts[static_cast<size_t>(mb)][static_cast<size_t>(cc + 1)].gout;
+            else
+                a.gin = I.recv_arena + slot(1, mb, cc) * Th;
+        }
+    }
+    I.tmp_h = I.alloc<bf16>(Th, M_SCRATCH);
+    I.g_head = I.alloc<bf16>(Th, M_SCRATCH);
+    for (int k = 0; k < 2; ++k) {
+        I.gmid_s[k] = I.alloc<bf16>(Th, M_SCRATCH);
+        I.gout_s[k] = I.alloc<bf16>(Th, M_SCRATCH);
+        I.dpre_s[k] = I.alloc<bf16>(static_cast<size_t>(T * mlp), M_SCRATCH);
+        I.dqkv_s[k] = I.alloc<bf16>(3 * Th, M_SCRATCH);
+    }
+    I.dq_acc = I.alloc<float>(Th, M_SCRATCH);
+    I.delta = I.alloc<float>(static_cast<size_t>(T * H), M_SCRATCH);
+    I.inputs = I.alloc<int32_t>(static_cast<size_t>(c_.n_mb * T), M_SCRATCH);
+    I.labels = I.alloc<int32_t>(static_cast<size_t>(c_.n_mb * T), M_SCRATCH);
+    I.row_loss = I.alloc<float>(static_cast<size_t>(c_.n_mb * T), M_SCRATCH);
+    I.loss_dev = I.alloc<float>(4, M_SCRATCH);
+    if (I.dry) return;  // sizing only: no streams, communicators, initialisation or events
+
+    CK(cudaSetDevice(I.dev));
     // The pipeline receive streams block in cuStreamWaitValue32 until a peer's copy lands; a send
     // stream that shares their hardware queue would wait behind them and the ring would hang.
     // CUDA maps streams onto CUDA_DEVICE_MAX_CONNECTIONS queues (default 8); the package sets 32
@@ -344,11 +590,6 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
                             " streams fewer hardware queues than streams; pipeline hand-offs (n_pp >= 2) can "
                             "deadlock. Set it to >= 32 before CUDA initialises (import the package first).");
     }
-    Impl& I = *impl_;
-    I.dev = o.device;
-    if (const char* e = getenv("BFPP_WGRAD_STREAM")) I.wgrad_stream = atoi(e) != 0;
-    if (const char* e = getenv("BFPP_EXEC_DEBUG")) I.debug = atoi(e) != 0;
-    CK(cudaSetDevice(I.dev));
     // Stream priorities: compute and pipeline hand-offs high, the DP lane (all-gather,
     // reduce-scatter, Adam) low, so bandwidth-bound optimizer blocks fill gaps instead of
     // delaying the compute stream's CTAs.
@@ -363,7 +604,6 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
 
     // ---- NCCL communicators (uid layout: see bfpp_exec_n_comm_ids): world (IPC handle exchange,
     // teardown barrier) and one DP group per pipeline rank. Pipeline hand-offs do not use NCCL.
-    const bool fs = c_.n_dp >= 2 && c_.dp_variant == DpVariant::DP_FS;
     {
         const size_t need = static_cast<size_t>(1 + p_);
         if (world > 1 && uids.size() < need) throw SpecError("executor: not enough NCCL unique ids");
@@ -376,38 +616,15 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
         if (I.world_comm) I.comm_ids.push_back({0, I.world_comm});
         if (I.dp_comm) I.comm_ids.push_back({static_cast<size_t>(1 + pp_rank_), I.dp_comm});
     }
-
-    // ---- parameters, gradients, optimizer shards ----
-    size_t& total = dev_bytes_;
-    int64_t max_padded = 0;
-    for (i64 cc = 0; cc < v_; ++cc) {
-        LocalStage ls;
-        ls.stage = local_stage(cc);
-        const StageLayout& L = layouts_[static_cast<size_t>(ls.stage)];
-        max_padded = std::max(max_padded, L.padded);
-        const bool sharded = c_.n_dp >= 2 && c_.dp_variant != DpVariant::DP0;
-        ls.shard_n = sharded ? L.padded / c_.n_dp : L.padded;
-        ls.seg = sharded ? shard_segments(L, c_.n_dp) : std::vector<int64_t>{0, L.padded};
-        ls.seg_done.assign(ls.seg.size() - 1, 0);
-        ls.nd = sharded ? c_.n_dp : 1;
-        ls.r = sharded ? dp_rank_ : 0;
-        if (!fs) ls.w16 = I.alloc<bf16>(static_cast<size_t>(L.padded), &total);
-        ls.grad = I.alloc<float>(static_cast<size_t>(L.padded), &total);
-        CK(cudaMemset(ls.grad, 0, static_cast<size_t>(L.padded) * 4));
-        ls.master = I.alloc<float>(static_cast<size_t>(ls.shard_n), &total);
-        ls.m = I.alloc<float>(static_cast<size_t>(ls.shard_n), &total);
-        ls.v = I.alloc<float>(static_cast<size_t>(ls.shard_n), &total);
+    if (I.gbuf) CK(cudaMemset(I.gbuf, 0, static_cast<size_t>(max_padded) * 4));
+    for (auto& ls : I.local) {
+        if (!pooled) CK(cudaMemset(ls.grad, 0, static_cast<size_t>(layouts_[static_cast<size_t>(ls.stage)].padded) * 4));
         CK(cudaMemset(ls.m, 0, static_cast<size_t>(ls.shard_n) * 4));
         CK(cudaMemset(ls.v, 0, static_cast<size_t>(ls.shard_n) * 4));
-        if (sharded) {
-            ls.gshard = I.alloc<float>(static_cast<size_t>(ls.shard_n), &total);
-            ls.gtmp = I.alloc<float>(static_cast<size_t>(ls.shard_n), &total);
-            ls.w16_shard = I.alloc<bf16>(static_cast<size_t>(ls.shard_n), &total);
-        }
-        I.local.push_back(ls);
+        ls.seg_ev.resize(ls.seg.size() - 1);
+        for (auto& e : ls.seg_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     if (fs) {
-        for (auto& s : I.slots) s = I.alloc<bf16>(static_cast<size_t>(max_padded), &total);
         size_t max_seg = 1;
         for (const auto& ls : I.local) max_seg = std::max(max_seg, ls.seg.size() - 1);
         for (auto& evs : I.rec_ev) {
@@ -436,90 +653,12 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
                 f32_to_bf16(ls.master, ls.w16, ls.shard_n, I.st[S_COMPUTE]);
         }
     }
-
-    // ---- activations and scratch ----
-    const int64_t T = c_.s_mb * m_.s_seq, h = m_.s_hidden, mlp = m_.s_mlp, V = m_.s_voc, H = m_.n_heads;
-    const size_t Th = static_cast<size_t>(T * h);
-    I.acts.assign(static_cast<size_t>(c_.n_mb), std::vector<StageActs>(static_cast<size_t>(v_)));
-    // receive slot (dir 0 = forward activation, 1 = backward gradient) of (mb, local stage c)
-    auto slot = [&](int dir, i64 mb, i64 cc) { return static_cast<size_t>((mb * v_ + cc) * 2 + dir); };
-    const size_t n_slots = static_cast<size_t>(c_.n_mb * v_ * 2);
-    if (p_ >= 2) {
-        CK(cudaMalloc(&I.recv_arena, n_slots * Th * sizeof(bf16)));
-        CK(cudaMalloc(&I.recv_flags, n_slots * sizeof(uint32_t) + 256));
-        CK(cudaMemset(I.recv_flags, 0, n_slots * sizeof(uint32_t)));
-        total += n_slots * Th * sizeof(bf16);
-    }
-    for (i64 mb = 0; mb < c_.n_mb; ++mb) {
-        for (i64 cc = 0; cc < v_; ++cc) {
-            StageActs& a = I.acts[static_cast<size_t>(mb)][static_cast<size_t>(cc)];
-            const i64 s = local_stage(cc);
-            const StageLayout& L = layouts_[static_cast<size_t>(s)];
-            // input: aliases the previous stage's output when both live on this device
-            if (s > 0 && pl_.device_of(s - 1) == pp_rank_)
-                a.in = I.acts[static_cast<size_t>(mb)][static_cast<size_t>(cc - 1)].out;
-            else if (s > 0)
-                a.in = I.recv_arena + slot(0, mb, cc) * Th;  // written by the previous rank's copy engine
-            else
-                a.in = I.alloc<bf16>(Th, &total);              // embedding output
-            bf16* x = a.in;
-            for (size_t l = 0; l < L.layers.size(); ++l) {
-                LayerActs la;
-                la.x_in = x;
-                la.ln1 = I.alloc<bf16>(Th, &total);
-                la.qkv = I.alloc<bf16>(3 * Th, &total);
-                la.o = I.alloc<bf16>(Th, &total);
-                la.x_mid = I.alloc<bf16>(Th, &total);
-                la.ln2 = I.alloc<bf16>(Th, &total);
-                la.pre = I.alloc<bf16>(static_cast<size_t>(T * mlp), &total);
-                la.act = I.alloc<bf16>(static_cast<size_t>(T * mlp), &total);
-                la.x_out = I.alloc<bf16>(Th, &total);
-                la.mu1 = I.alloc<float>(static_cast<size_t>(T), &total);
-                la.rs1 = I.alloc<float>(static_cast<size_t>(T), &total);
-                la.mu2 = I.alloc<float>(static_cast<size_t>(T), &total);
-                la.rs2 = I.alloc<float>(static_cast<size_t>(T), &total);
-                la.lse = I.alloc<float>(static_cast<size_t>(T * H), &total);
-                x = la.x_out;
-                a.layers.push_back(la);
-            }
-            a.out = x;
-            if (L.last) {
-                a.lnf = I.alloc<bf16>(Th, &total);
-                a.muf = I.alloc<float>(static_cast<size_t>(T), &total);
-                a.rsf = I.alloc<float>(static_cast<size_t>(T), &total);
-                a.logits = I.alloc<bf16>(static_cast<size_t>(T * V), &total);
-            }
-            if (!L.first) a.gout = I.alloc<bf16>(Th, &total);
-        }
-        // gin: the next stage's gout when it lives on this device, else a receive buffer
-        for (i64 cc = 0; cc < v_; ++cc) {
-            StageActs& a = I.acts[static_cast<size_t>(mb)][static_cast<size_t>(cc)];
-            const i64 s = local_stage(cc);
-            if (s == pl_.n_stage - 1) continue;
-            if (pl_.device_of(s + 1) == pp_rank_)
-                a.gin = I.acts[static_cast<size_t>(mb)][static_cast<size_t>(cc + 1)].gout;
-            else
-                a.gin = I.recv_arena + slot(1, mb, cc) * Th;
-        }
-    }
-    I.tmp_h = I.alloc<bf16>(Th, &total);
-    I.g_head = I.alloc<bf16>(Th, &total);
     for (int k = 0; k < 2; ++k) {
-        I.gmid_s[k] = I.alloc<bf16>(Th, &total);
-        I.gout_s[k] = I.alloc<bf16>(Th, &total);
-        I.dpre_s[k] = I.alloc<bf16>(static_cast<size_t>(T * mlp), &total);
-        I.dqkv_s[k] = I.alloc<bf16>(3 * Th, &total);
         CK(cudaEventCreateWithFlags(&I.ev_a[k], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&I.ev_b[k], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&I.ev_wg[k], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&I.ev_opt[k], cudaEventDisableTiming));
     }
-    I.dq_acc = I.alloc<float>(Th, &total);
-    I.delta = I.alloc<float>(static_cast<size_t>(T * H), &total);
-    I.inputs = I.alloc<int32_t>(static_cast<size_t>(c_.n_mb * T), &total);
-    I.labels = I.alloc<int32_t>(static_cast<size_t>(c_.n_mb * T), &total);
-    I.row_loss = I.alloc<float>(static_cast<size_t>(c_.n_mb * T), &total);
-    I.loss_dev = I.alloc<float>(4, &total);
     CK(cudaMallocHost(&I.loss_pinned, sizeof(float)));
 
     // ---- CUDA IPC: map the ring neighbours' receive arenas and flags ----
@@ -554,7 +693,7 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
         }
     }
 
-    // ---- per-task execution plan ----
+    // ---- per-task events ----
     const size_t n = graph_.tasks.size();
     I.done.assign(n, nullptr);
     I.done_g.assign(n, nullptr);
@@ -563,7 +702,6 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
     I.task_c.assign(n, -1);
     I.tl_start.assign(n, NAN);
     I.tl_end.assign(n, NAN);
-    I.order = plan_rank(graph_, pp_rank_, c_.n_dp);
     for (const TaskExec& te : I.order) {
         const Task& t = graph_.tasks[static_cast<size_t>(te.id)];
         if (t.lane == Lane::Compute) I.task_c[static_cast<size_t>(te.id)] = static_cast<int>(t.stage / p_);
@@ -580,8 +718,10 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
     CK(cudaStreamSynchronize(I.st[S_COMPUTE]));
 }
 
+
 Executor::~Executor() {
     Impl& I = *impl_;
+    if (I.dry) return;
     cudaSetDevice(I.dev);
     cudaDeviceSynchronize();
     // Tear communicators down in ascending global id order so that the two members of
@@ -613,6 +753,9 @@ Executor::~Executor() {
             if (e) cudaEventDestroy(e);
     for (auto e : I.done_g)
         if (e) cudaEventDestroy(e);
+    for (auto& ls : I.local)
+        for (auto e : ls.seg_ev)
+            if (e) cudaEventDestroy(e);
     for (int k = 0; k < 2; ++k)
         for (cudaEvent_t e : {I.ev_a[k], I.ev_b[k], I.ev_wg[k], I.ev_opt[k]})
             if (e) cudaEventDestroy(e);
@@ -788,36 +931,45 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
         if (fs) return I.slots[te.slot];
         return I.local[static_cast<size_t>(cidx)].w16;
     };
-    // Adam over elements [lo, hi) of a stage's (shard of) master weights / moments / gradient
+    // Adam over elements [lo, hi) of a stage's (shard of) master weights / moments; gradient = g
+    // (elements lo..hi) or, by default, the stage's gradient shard / full gradient at lo
     auto adam = [&](LocalStage& ls, cudaStream_t st, int64_t lo = 0, int64_t hi = -1, size_t s0 = 0,
-                    size_t s1 = SIZE_MAX) {
+                    size_t s1 = SIZE_MAX, const float* g = nullptr) {
         if (o_.skip_optimizer) return;
         if (hi < 0) hi = ls.shard_n;
         if (s1 == SIZE_MAX) s1 = ls.seg.size() - 1;
-        const bool sharded = ls.gshard != nullptr;
-        float* g = sharded ? ls.gshard : ls.grad;
+        const bool sharded = ls.w16_shard != nullptr;
+        if (!g) g = (sharded ? ls.gshard : ls.grad) + lo;
         bf16* w = sharded ? ls.w16_shard : ls.w16;
         K(K_ADAM, 30.0 * static_cast<double>(hi - lo), 1, st, [&] {
-            adam_update(ls.master + lo, ls.m + lo, ls.v + lo, g + lo, w + lo, hi - lo, o_.lr, o_.beta1, o_.beta2,
-                        o_.eps, o_.weight_decay, I.step_no, 0, st);
+            adam_update(ls.master + lo, ls.m + lo, ls.v + lo, const_cast<float*>(g), w + lo, hi - lo, o_.lr, o_.beta1,
+                        o_.beta2, o_.eps, o_.weight_decay, I.step_no, 0, st);
         });
         if (sharded && c_.dp_variant == DpVariant::DP_PS) all_gather_segments(ls, ls.w16, s0, s1, I.dp_comm, st);
     };
     // Reduction of one stage segment (sharded variants): reduce-scatter its gradients into this
-    // rank's slice, fold in earlier units, and (last unit) update it — on stream st.
+    // rank's slice, fold in earlier units, and (last unit) update it — on stream st. A stage with
+    // a single unit and no persistent shard goes through the transient per-segment buffer.
     auto reduce_segment = [&](LocalStage& ls, cudaStream_t st, size_t si, bool first_unit, bool update) {
         const int64_t lo = ls.seg[si] / ls.nd, hi = ls.seg[si + 1] / ls.nd;
-        reduce_scatter_segments(ls, first_unit ? ls.gshard : ls.gtmp, si, si + 1, I.dp_comm, st);
-        if (!first_unit)
-            K(K_MISC, 12.0 * static_cast<double>(hi - lo), 1, st,
-              [&] { add_f32_kernel<<<296, 256, 0, st>>>(ls.gshard + lo, ls.gtmp + lo, hi - lo); });
-        if (update) adam(ls, st, lo, hi, si, si + 1);
+        if (!ls.gshard) {
+            reduce_scatter_segments(ls, I.gseg, si, si + 1, I.dp_comm, st, lo);
+            if (update) adam(ls, st, lo, hi, si, si + 1, I.gseg);
+        } else {
+            reduce_scatter_segments(ls, first_unit ? ls.gshard : I.gtmp, si, si + 1, I.dp_comm, st);
+            if (!first_unit)
+                K(K_MISC, 12.0 * static_cast<double>(hi - lo), 1, st,
+                  [&] { add_f32_kernel<<<296, 256, 0, st>>>(ls.gshard + lo, I.gtmp + lo, hi - lo); });
+            if (update) adam(ls, st, lo, hi, si, si + 1);
+        }
         ls.seg_done[si] = 1;
     };
-    // Under DP_FS / DP_PS the stage's last reduction unit runs segment by segment inside the
-    // backward that completes it: each layer is reduce-scattered and updated on the DP stream as
-    // soon as its gradients are final, leaving only the last segments for the Reduce task.
-    auto early_segment = [&](LocalStage& ls, cudaStream_t st, cudaStream_t ws, int64_t seg_start, bool first_unit) {
+    // Under DP_FS / DP_PS every reduction unit runs segment by segment inside the backward that
+    // completes it: each layer is reduce-scattered (and, in the stage's last unit, updated) on the
+    // DP stream as soon as its gradients are final, leaving only the last segments for the Reduce
+    // task, and the pooled gradient buffer drains in the order the next unit refills it.
+    auto early_segment = [&](LocalStage& ls, cudaStream_t st, cudaStream_t ws, int64_t seg_start, bool first_unit,
+                             bool update) {
         size_t si = 0;
         while (si + 1 < ls.seg.size() && ls.seg[si] != seg_start) ++si;
         if (si + 1 >= ls.seg.size()) return;  // single-segment layout: the Reduce task does it all
@@ -827,7 +979,22 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
             CK(cudaEventRecord(I.ev_opt[1], ws));
             CK(cudaStreamWaitEvent(ds, I.ev_opt[1], 0));
         }
-        reduce_segment(ls, ds, si, first_unit, true);
+        reduce_segment(ls, ds, si, first_unit, update);
+    };
+    // Pooled gradients: before a unit's first backward overwrites stage-vector range [lo, hi) of
+    // its stage, wait until every reduce-scatter still reading that part of the shared buffer
+    // (any local stage's segment overlapping it) has finished.
+    auto guard_grads = [&](const LocalStage& ls, cudaStream_t st, cudaStream_t ws, int64_t lo, int64_t hi) {
+        if (!I.gbuf) return;
+        const int64_t blo = (ls.grad - I.gbuf) + lo, bhi = (ls.grad - I.gbuf) + hi;
+        for (const LocalStage& o2 : I.local) {
+            const int64_t base = o2.grad - I.gbuf;
+            for (size_t si = 0; si + 1 < o2.seg.size(); ++si)
+                if (base + o2.seg[si] < bhi && base + o2.seg[si + 1] > blo) {
+                    CK(cudaStreamWaitEvent(st, o2.seg_ev[si], 0));
+                    if (ws != st) CK(cudaStreamWaitEvent(ws, o2.seg_ev[si], 0));
+                }
+        }
     };
     // n_dp == 1: a parameter segment's gradient is final as soon as the stage's last backward
     // has produced it, so the optimizer runs segment by segment (a layer at a time) on the DP
@@ -915,7 +1082,10 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
             cudaStream_t ws = I.wgrad_stream ? I.st[S_WGRAD] : st;
             const int acc = te.first_in_unit ? 0 : 1;  // the unit's first contribution overwrites
             const bool seg_opt = te.adam_after;  // only set on a backward task when n_dp == 1
-            const bool early = te.last_unit_bwd && ls.gshard != nullptr && ls.seg.size() > 2;
+            // sharded variants: the backward that completes a reduction unit reduce-scatters it
+            // segment by segment (and updates it in the stage's last unit)
+            const bool early = te.unit_end_bwd && ls.w16_shard != nullptr && ls.seg.size() > 2;
+            const bool guard = te.first_in_unit && I.gbuf != nullptr;
             const size_t nl = L.layers.size();
             auto layer_end = [&](size_t li) -> int64_t {
                 return li + 1 < nl ? L.layers[li + 1].ln1_g : (L.last ? L.lnf_g : ls.shard_n);
@@ -931,6 +1101,15 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
             const bf16* g;
             if (L.last) {
                 need_weights(ls, L.lnf_g);
+                if (o_.recompute) {  // the LM head's logits and dlogits were not kept: recompute them
+                    LNF(st, a.out, W + L.lnf_g, W + L.lnf_b, a.lnf, a.muf, a.rsf);
+                    G(st, T, V, h, a.lnf, h, 0, W + L.head, h, 0, a.logits, V, GEMM_EPI_BF16);
+                    K(K_MISC, 4.0 * static_cast<double>(T * V), 1, st, [&] {
+                        softmax_xent(a.logits, V, I.labels + t.micro_batch * T, I.row_loss + t.micro_batch * T,
+                                     static_cast<int>(T), static_cast<int>(V), grad_scale, st);
+                    });
+                }
+                if (guard) guard_grads(ls, st, ws, L.lnf_g, L.padded);
                 G(st, T, h, V, a.logits, V, 0, W + L.head, h, 1, I.tmp_h, h, GEMM_EPI_BF16);
                 CK(cudaEventRecord(I.ev_a[0], st));  // logits/lnf are persistent; only ordering matters
                 CK(cudaStreamWaitEvent(ws, I.ev_a[0], 0));
@@ -940,7 +1119,7 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
                     acc);
                 g = I.g_head;
                 if (seg_opt) adam_segment(ls, st, ws, L.lnf_g, ls.shard_n);
-                if (early) early_segment(ls, st, ws, L.lnf_g, te.reduce_first_unit);
+                if (early) early_segment(ls, st, ws, L.lnf_g, te.reduce_first_unit, te.last_unit_bwd);
             } else {
                 g = a.gin;
             }
@@ -952,6 +1131,17 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
                 const int k = lc & 1;
                 // set k was last read by the wgrads of layer lc-2
                 if (lc >= 2) CK(cudaStreamWaitEvent(st, I.ev_wg[k], 0));
+                if (o_.recompute) {
+                    // the layer's forward from its checkpointed input into the working set (its
+                    // output x_out is the checkpoint itself and is not recomputed)
+                    LNF(st, x.x_in, W + P.ln1_g, W + P.ln1_b, x.ln1, x.mu1, x.rs1);
+                    G(st, T, 3 * h, h, x.ln1, h, 0, W + P.qkv, h, 0, x.qkv, 3 * h, GEMM_EPI_BF16);
+                    K(K_ATTN_FWD, attn_flops, 1, st, [&] { attention_fwd(x.qkv, x.o, x.lse, B, S, H, 128, st); });
+                    G(st, T, h, h, x.o, h, 0, W + P.o, h, 0, x.x_mid, h, GEMM_EPI_RESID, x.x_in, h);
+                    LNF(st, x.x_mid, W + P.ln2_g, W + P.ln2_b, x.ln2, x.mu2, x.rs2);
+                    G(st, T, mlp, h, x.ln2, h, 0, W + P.fc1, h, 0, x.act, mlp, GEMM_EPI_GELU, nullptr, 0, x.pre, mlp);
+                }
+                if (guard) guard_grads(ls, st, ws, P.ln1_g, layer_end(li));
                 bf16 *gmid = I.gmid_s[k], *dpre = I.dpre_s[k], *dqkv = I.dqkv_s[k];
                 bf16* gnext = (li == 0 && !L.first) ? a.gout : I.gout_s[k];
                 // MLP: x_out = x_mid + gelu(ln2 W1^T) W2^T
@@ -979,8 +1169,9 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
                 LNB(st, I.tmp_h, x.x_in, W + P.ln1_g, x.mu1, x.rs1, gmid, gnext, G_ + P.ln1_g, G_ + P.ln1_b, acc);
                 g = gnext;
                 if (seg_opt) adam_segment(ls, st, ws, P.ln1_g, layer_end(li));
-                if (early) early_segment(ls, st, ws, P.ln1_g, te.reduce_first_unit);
+                if (early) early_segment(ls, st, ws, P.ln1_g, te.reduce_first_unit, te.last_unit_bwd);
             }
+            if (L.first && guard) guard_grads(ls, st, ws, 0, L.layers[0].ln1_g);
             if (L.first && acc == 0) {  // scatter-added gradients need a zeroed start
                 CK(cudaMemsetAsync(G_ + L.wte, 0, static_cast<size_t>(V * h) * 4, st));
                 CK(cudaMemsetAsync(G_ + L.wpe, 0, static_cast<size_t>(m_.s_seq * h) * 4, st));
@@ -1042,11 +1233,16 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
                     if (!ls.seg_done[si]) reduce_segment(ls, st, si, te.first_unit, te.adam_after);
                 std::fill(ls.seg_done.begin(), ls.seg_done.end(), 0);
                 break;
+            } else if (!ls.gshard) {  // single unit, transient shard buffer (segments, or the whole stage)
+                for (size_t si = 0; si + 1 < ls.seg.size(); ++si)
+                    reduce_segment(ls, st, si, true, te.adam_after);
+                std::fill(ls.seg_done.begin(), ls.seg_done.end(), 0);
+                break;
             } else {
-                float* dst = te.first_unit ? ls.gshard : ls.gtmp;
+                float* dst = te.first_unit ? ls.gshard : I.gtmp;
                 reduce_scatter_segments(ls, dst, 0, ls.seg.size() - 1, I.dp_comm, st);
                 if (!te.first_unit)
-                    K(K_MISC, 12.0 * ls.shard_n, 1, st, [&] { add_f32_kernel<<<296, 256, 0, st>>>(ls.gshard, ls.gtmp, ls.shard_n); });
+                    K(K_MISC, 12.0 * ls.shard_n, 1, st, [&] { add_f32_kernel<<<296, 256, 0, st>>>(ls.gshard, I.gtmp, ls.shard_n); });
                 // no re-zeroing: the next unit's first backward overwrites the gradient buffer
             }
             if (te.adam_after) adam(ls, st);
@@ -1210,6 +1406,9 @@ void Executor::get_grads(i64 stage, float* host, int64_t n, int64_t* lo, int64_t
     LocalStage& ls = find_local(I.local, stage);
     const StageLayout& L = layouts_[static_cast<size_t>(stage)];
     if (n < L.numel) throw SpecError("get_grads: buffer too small");
+    if (ls.w16_shard && !ls.gshard)
+        throw SpecError("get_grads: this stage's reduced gradients are transient (one reduction unit); "
+                        "create the executor with skip_optimizer to keep them");
     if (ls.gshard) {
         scatter_shard(ls, L, ls.gshard, host, lo, hi);
     } else {
@@ -1246,8 +1445,9 @@ void Executor::get_weights16(i64 stage, uint16_t* host, int64_t n, int64_t* lo, 
 void Executor::zero_grads() {
     Impl& I = *impl_;
     sync();
+    if (I.gbuf) CK(cudaMemset(I.gbuf, 0, static_cast<size_t>(I.gbuf_n) * 4));
     for (auto& ls : I.local) {
-        CK(cudaMemset(ls.grad, 0, static_cast<size_t>(layouts_[static_cast<size_t>(ls.stage)].padded) * 4));
+        if (!I.gbuf) CK(cudaMemset(ls.grad, 0, static_cast<size_t>(layouts_[static_cast<size_t>(ls.stage)].padded) * 4));
         if (ls.gshard) CK(cudaMemset(ls.gshard, 0, static_cast<size_t>(ls.shard_n) * 4));
     }
     CK(cudaDeviceSynchronize());

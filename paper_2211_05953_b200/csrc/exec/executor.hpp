@@ -28,6 +28,35 @@ struct ExecOptions {
     float lr = 1e-4f, beta1 = 0.9f, beta2 = 0.95f, eps = 1e-8f, weight_decay = 0.f, init_std = 0.02f;
     bool skip_optimizer = false;
     bool profile_kernels = false;  // CUDA events around every kernel of the step (per-category stats)
+    // activation checkpointing: a forward keeps only each layer's output
+    // (2 T h bytes, the reference's checkpoint, memory.cpp:64-70); the backward recomputes the
+    // layer's forward into one working set (and the LM head's logits) before differentiating it
+    bool recompute = false;
+    // size the rank's buffers without touching the GPU (memory_plan)
+    bool dry_run = false;
+};
+
+// Device bytes of one rank by category (allocation sizes as the executor requests them).
+enum MemCat : int {
+    M_WEIGHTS = 0,     // bf16 compute weights: resident stages, or the two DP_FS reconstruction slots
+    M_GRADS,           // f32 gradient accumulation: per stage, or one pooled buffer (sharded variants)
+    M_OPTIMIZER,       // f32 master weights + Adam m, v (this rank's shards)
+    M_GRAD_SHARDS,     // reduced-gradient shards, reduce-scatter landing / per-segment buffers
+    M_WEIGHT_SHARDS,   // bf16 all-gather source shards (sharded variants)
+    M_ACTIVATIONS,     // activation sets of the live (micro-batch, stage) pairs: full or checkpoints
+    M_PP_BUFFERS,      // pipeline receive arena + per-(micro-batch, stage) backward send buffers
+    M_SCRATCH,         // per-layer working sets, attention temporaries, logits (recompute), tokens
+    M_NCAT
+};
+struct MemoryPlan {
+    size_t bytes[M_NCAT] = {};
+    int64_t activation_sets = 0;  // pooled (micro-batch, local stage) activation sets = peak live in program order
+    int64_t head_sets = 0;        // pooled logits sets of the last stage (0 with recompute)
+    size_t total() const {
+        size_t t = 0;
+        for (size_t b : bytes) t += b;
+        return t;
+    }
 };
 
 // Kernel categories for per-step statistics (launch counts always; times when profiling).
@@ -79,6 +108,7 @@ public:
     // per-task [start,end] seconds of the last step (tasks of other devices: NaN)
     void timeline(double* start, double* end) const;
     size_t device_bytes() const { return dev_bytes_; }
+    const MemoryPlan& memory_plan() const { return mem_; }
     const KernelStats& kernel_stats() const;  // of the last step
     cudaStream_t compute_stream() const;
     void set_flags(bool record_timeline, bool profile_kernels);
@@ -95,6 +125,7 @@ private:
     int rank_, world_;
     i64 p_, v_, pp_rank_, dp_rank_;
     size_t dev_bytes_ = 0;
+    MemoryPlan mem_;
 };
 
 }  // namespace bfpp

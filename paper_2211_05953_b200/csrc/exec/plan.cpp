@@ -9,7 +9,7 @@
 
 namespace bfpp {
 
-std::vector<PlanTask> plan_rank(const TaskGraph& g, i64 pp_rank, i64 n_dp) {
+std::vector<PlanTask> plan_rank(const TaskGraph& g, i64 pp_rank, i64 n_dp, bool pooled_grads) {
     std::vector<PlanTask> order;
     // enqueue order = start order of a simulation with positive durations (a topological order
     // consistent with every lane's program/priority order on this device)
@@ -64,6 +64,7 @@ std::vector<PlanTask> plan_rank(const TaskGraph& g, i64 pp_rank, i64 n_dp) {
         bool send = false;
         stream_of_task[static_cast<size_t>(id)] = stream_of(g.tasks[static_cast<size_t>(id)], &send);
     }
+    TaskId last_reduce = -1;  // Reduce of the latest unit-ending backward seen (program order)
     for (TaskId id : mine) {
         const Task& t = g.tasks[static_cast<size_t>(id)];
         PlanTask te;
@@ -80,23 +81,27 @@ std::vector<PlanTask> plan_rank(const TaskGraph& g, i64 pp_rank, i64 n_dp) {
         if (t.kind == TaskKind::Reconstruct) te.slot = rec_slot[id];
         if (t.kind == TaskKind::Bwd) {
             // a new reduction unit of this stage may only start once the previous unit's
-            // reduce-scatter has drained (and re-zeroed) the stage's gradient buffer
+            // reduce-scatter has drained the stage's gradient buffer (pooled: per segment, by the
+            // executor; the host enqueues this task after the rank's latest Reduce)
             auto pb = prev_bwd.find(t.stage);
             if (pb == prev_bwd.end()) te.first_in_unit = true;
             if (pb != prev_bwd.end()) {
                 auto r = reduce_of_last_bwd.find(pb->second);
                 if (r != reduce_of_last_bwd.end()) {
-                    te.waits.push_back(r->second);
+                    if (!pooled_grads) te.waits.push_back(r->second);
                     te.first_in_unit = true;
                 }
             }
+            if (pooled_grads && te.first_in_unit && last_reduce >= 0) te.after.push_back(last_reduce);
             prev_bwd[t.stage] = id;
             if (n_dp < 2 && last_bwd_of_stage[t.stage] == id) te.adam_after = true;
             auto red = reduce_of_last_bwd.find(id);
             if (n_dp >= 2 && red != reduce_of_last_bwd.end()) {
                 const auto& rs = reduces_of_stage[t.stage];
+                te.unit_end_bwd = true;
                 te.last_unit_bwd = rs.back() == red->second;
                 te.reduce_first_unit = rs.front() == red->second;
+                last_reduce = red->second;
             }
         }
         if (t.kind == TaskKind::Reduce) {
@@ -126,6 +131,10 @@ std::vector<PlanTask> plan_rank(const TaskGraph& g, i64 pp_rank, i64 n_dp) {
             }
             last[te.stream] = static_cast<long>(i);
             for (TaskId w : te.waits) {
+                succ[pos.at(w)].push_back(i);
+                ++indeg[i];
+            }
+            for (TaskId w : te.after) {
                 succ[pos.at(w)].push_back(i);
                 ++indeg[i];
             }

@@ -27,11 +27,19 @@ struct PlanTask {
     // update the stage segment by segment inside it; reduce_first_unit = that Reduce is also the
     // stage's first unit (its reduce-scatter overwrites the gradient shard)
     bool last_unit_bwd = false, reduce_first_unit = false;
+    // Bwd that completes a reduction unit (any unit, n_dp >= 2): under pooled gradients its
+    // segments are reduce-scattered as the backward produces them
+    bool unit_end_bwd = false;
     std::vector<TaskId> waits;  // events to wait on (deps on other streams + resource deps)
+    std::vector<TaskId> after;  // host enqueue order only (no GPU wait)
 };
 
 // Tasks of pipeline rank `pp_rank` (compute, DP and both ends of its transfers) in host
 // enqueue order: a topological order over cross-stream waits and per-stream FIFO order.
-std::vector<PlanTask> plan_rank(const TaskGraph& g, i64 pp_rank, i64 n_dp);
+// pooled_grads (sharded variants): the rank's stages share one f32 gradient buffer whose reuse the
+// executor guards per segment; a unit's first backward is then only ordered on the host after the
+// previous unit's Reduce (whose reduce-scatters record those segment events) instead of waiting
+// for that Reduce on the GPU.
+std::vector<PlanTask> plan_rank(const TaskGraph& g, i64 pp_rank, i64 n_dp, bool pooled_grads = false);
 
 }  // namespace bfpp

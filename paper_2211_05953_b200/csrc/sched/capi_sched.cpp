@@ -262,6 +262,45 @@ int bfpp_peak_inflight(const bfpp_timeline* tl, const bfpp_graph* g, int64_t lay
     });
 }
 
+int bfpp_total_memory(const bfpp_model_spec* m, const bfpp_parallel_config* c, double dp0_bytes_per_param,
+                      double* out) {
+    return guarded([&] {
+        MemoryOptions o;
+        o.dp0_bytes_per_param = dp0_bytes_per_param;
+        const MemoryBreakdown b = total_memory(to_model(m), to_config(c), o);
+        out[0] = b.state_bytes;
+        out[1] = b.activation_bytes;
+        out[2] = b.checkpoint_bytes;
+        out[3] = b.total_bytes;
+    });
+}
+
+int bfpp_feasible(const bfpp_model_spec* m, const bfpp_parallel_config* c, const bfpp_cluster_spec* cl,
+                  double dp0_bytes_per_param, double headroom, int32_t* out) {
+    return guarded([&] {
+        MemoryOptions o;
+        o.dp0_bytes_per_param = dp0_bytes_per_param;
+        o.headroom = headroom;
+        ClusterSpec k;
+        k.mem_capacity = cl->mem_capacity;
+        *out = feasible(to_model(m), to_config(c), k, o) ? 1 : 0;
+    });
+}
+
+int bfpp_cluster_preset(const char* name, bfpp_cluster_spec* out) {
+    return guarded([&] {
+        const ClusterSpec k = cluster_preset(name ? name : "");
+        out->n_node = k.n_node;
+        out->s_node = k.s_node;
+        out->peak_flops = k.peak_flops;
+        out->bw_intra = k.bw_intra;
+        out->bw_inter = k.bw_inter;
+        out->pp_latency = k.pp_latency;
+        out->mem_capacity = k.mem_capacity;
+        out->kernel_efficiency = k.kernel_efficiency;
+    });
+}
+
 double bfpp_compute_per_gpu(const bfpp_model_spec* m, const bfpp_parallel_config* c) {
     try {
         return compute_per_gpu(to_model(m), to_config(c));

@@ -119,4 +119,21 @@ Timeline timeline_from_intervals(const TaskGraph& g, const double* start, const 
 double compute_per_gpu(const ModelSpec& m, const ParallelConfig& c);
 i64 param_count(const ModelSpec& m);
 
+// Analytic memory model (reference memory.hpp / memory.cpp, restated in memory.cpp).
+struct MemoryOptions {
+    double dp0_bytes_per_param = 20.0;
+    double headroom = 0.85;
+};
+struct MemoryBreakdown {
+    double state_bytes = 0.0, activation_bytes = 0.0, checkpoint_bytes = 0.0, total_bytes = 0.0;
+};
+double state_memory(const ModelSpec& m, const ParallelConfig& c, const MemoryOptions& o = {});
+double activation_memory(const ModelSpec& m, const ParallelConfig& c);
+double checkpoint_count(const ModelSpec& m, const ParallelConfig& c);
+double checkpoint_memory(const ModelSpec& m, const ParallelConfig& c);
+MemoryBreakdown total_memory(const ModelSpec& m, const ParallelConfig& c, const MemoryOptions& o = {});
+bool feasible(const ModelSpec& m, const ParallelConfig& c, const ClusterSpec& k, const MemoryOptions& o = {});
+// "a100", "v100-dgx1" (the reference's, types.cpp:206-231) and "b200"
+ClusterSpec cluster_preset(const std::string& name);
+
 }  // namespace bfpp

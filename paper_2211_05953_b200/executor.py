@@ -23,6 +23,9 @@ from .model import GPTConfig
 
 SKIP_OPTIMIZER = 1
 PROFILE_KERNELS = 2
+RECOMPUTE = 4
+MEMORY_CATEGORIES = ("weights", "grads", "optimizer", "grad_shards", "weight_shards", "activations", "pp_buffers",
+                     "scratch")
 KERNEL_CATEGORIES = ("gemm", "attention_fwd", "attention_bwd", "layernorm", "misc", "adam")
 
 
@@ -52,7 +55,7 @@ class Executor:
                  device: Optional[int] = None, uids: Optional[bytes] = None, record_timeline: bool = False,
                  seed: int = 1234, lr: float = 1e-4, beta1: float = 0.9, beta2: float = 0.95,
                  eps: float = 1e-8, weight_decay: float = 0.0, init_std: float = 0.02,
-                 skip_optimizer: bool = False, profile_kernels: bool = False,
+                 skip_optimizer: bool = False, profile_kernels: bool = False, recompute: bool = False,
                  graph: Optional[ps.TaskGraph] = None):
         """graph: run this task graph (e.g. ``ps.build_accumulation_tasks``) instead of
         ``build_tasks(model, config)``; ``config`` then describes its placement (see
@@ -63,7 +66,8 @@ class Executor:
         if device is None:
             device = int(os.environ.get("LOCAL_RANK", rank))
         opts = N.ExecOptsC(device, int(record_timeline), seed, lr, beta1, beta2, eps, weight_decay, init_std,
-                           (SKIP_OPTIMIZER if skip_optimizer else 0) | (PROFILE_KERNELS if profile_kernels else 0))
+                           (SKIP_OPTIMIZER if skip_optimizer else 0) | (PROFILE_KERNELS if profile_kernels else 0)
+                           | (RECOMPUTE if recompute else 0))
         h = C.c_void_p()
         ubuf = C.create_string_buffer(uids, len(uids)) if uids else None
         if graph is None:
@@ -81,6 +85,10 @@ class Executor:
         L = N.lib()
         self.local_stages = [L.bfpp_exec_local_stage(self._h, c) for c in range(L.bfpp_exec_n_local_stages(self._h))]
         self.device_bytes = L.bfpp_exec_device_bytes(self._h)
+
+    def memory(self) -> dict:
+        """This rank's device bytes by category (+ pooled activation / logits set counts)."""
+        return _memory_dict(lambda b, n: N.lib().bfpp_exec_memory(self._h, b, n))
 
     # ---- training step -------------------------------------------------------------------
     def step(self, tokens) -> float:
@@ -166,6 +174,28 @@ class Executor:
             pass
 
 
+def _memory_dict(fill) -> dict:
+    b = (C.c_int64 * len(MEMORY_CATEGORIES))()
+    n = (C.c_int64 * 2)()
+    _check(fill(b, n))
+    out = {k: int(b[i]) for i, k in enumerate(MEMORY_CATEGORIES)}
+    out["total"] = sum(out.values())
+    out["activation_sets"], out["head_sets"] = int(n[0]), int(n[1])
+    return out
+
+
+def memory_plan(model, config: ps.ParallelConfig, rank: int = 0, *, recompute: bool = False,
+                skip_optimizer: bool = False) -> dict:
+    """Device bytes rank `rank` of an executor for (model, config) would allocate, by category,
+    computed on the host (the executor's own allocation code in sizing mode; no GPU needed)."""
+    if isinstance(model, GPTConfig):
+        model = model_spec(model)
+    opts = N.ExecOptsC(0, 0, 0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0,
+                       (RECOMPUTE if recompute else 0) | (SKIP_OPTIMIZER if skip_optimizer else 0))
+    return _memory_dict(lambda b, n: N.lib().bfpp_exec_memory_plan(C.byref(model._c()), C.byref(config._c()),
+                                                                   C.byref(opts), rank, b, n))
+
+
 KERNEL_VARIANTS = ("gemm_1cta", "gemm_2cta", "gemm_2cta_pair", "gemm_2cta_nfast", "gemm_2cta_streamk",
                    "attn_fwd_multi", "attn_bwd_multi")
 
@@ -183,17 +213,19 @@ def kernel_variant_counts(reset: bool = False) -> dict:
 STREAMS = ("compute", "dp", "fwd_send", "fwd_recv", "bwd_send", "bwd_recv", "wgrad")
 
 
-def plan_rank(graph: ps.TaskGraph, pp_rank: int, n_dp: int):
-    """The executor's per-rank plan (host only): [(task id, stream, flags, slot, waits)] in enqueue order."""
+def plan_rank(graph: ps.TaskGraph, pp_rank: int, n_dp: int, dp_variant: ps.DpVariant = ps.DpVariant.DP0):
+    """The executor's per-rank plan (host only): [(task id, stream, flags, slot, waits)] in enqueue
+    order. dp_variant selects the gradient-buffer discipline (sharded variants pool the buffers)."""
     L = N.lib()
     nt, nw = C.c_int64(), C.c_int64()
     z = C.POINTER(C.c_int32)()
-    _check(L.bfpp_plan_rank(graph.handle, pp_rank, n_dp, 0, 0, z, z, z, z, z, z, C.byref(nt), C.byref(nw)))
+    v = int(dp_variant)
+    _check(L.bfpp_plan_rank(graph.handle, pp_rank, n_dp, v, 0, 0, z, z, z, z, z, z, C.byref(nt), C.byref(nw)))
     n, m = nt.value, nw.value
     arr = lambda k: (C.c_int32 * max(1, k))()  # noqa: E731
     ids, streams, flags, slots, woff, wids = arr(n), arr(n), arr(n), arr(n), arr(n + 1), arr(m)
-    _check(L.bfpp_plan_rank(graph.handle, pp_rank, n_dp, n, m, ids, streams, flags, slots, woff, wids, C.byref(nt),
-                            C.byref(nw)))
+    _check(L.bfpp_plan_rank(graph.handle, pp_rank, n_dp, v, n, m, ids, streams, flags, slots, woff, wids,
+                            C.byref(nt), C.byref(nw)))
     return [(ids[i], streams[i], flags[i], slots[i], list(wids[woff[i]:woff[i + 1]])) for i in range(n)]
 
 

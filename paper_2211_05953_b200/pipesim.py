@@ -386,6 +386,44 @@ def compute_per_gpu(model: ModelSpec, config: ParallelConfig) -> float:
     return float(N.lib().bfpp_compute_per_gpu(C.byref(model._c()), C.byref(config._c())))
 
 
+@dataclass(frozen=True)
+class MemoryBreakdown:
+    state_bytes: float
+    activation_bytes: float
+    checkpoint_bytes: float
+    total_bytes: float
+
+
+@dataclass(frozen=True)
+class MemoryOptions:
+    dp0_bytes_per_param: float = 20.0
+    headroom: float = 0.85
+
+
+def total_memory(model: ModelSpec, config: ParallelConfig, opts: MemoryOptions = MemoryOptions()) -> MemoryBreakdown:
+    """Analytic bytes per device (memory.cpp:72-80)."""
+    out = (C.c_double * 4)()
+    _check(N.lib().bfpp_total_memory(C.byref(model._c()), C.byref(config._c()), opts.dp0_bytes_per_param, out))
+    return MemoryBreakdown(*out)
+
+
+def feasible(model: ModelSpec, config: ParallelConfig, cluster: ClusterSpec,
+             opts: MemoryOptions = MemoryOptions()) -> bool:
+    """total_memory <= headroom * mem_capacity (memory.cpp:82-86)."""
+    r = C.c_int32()
+    _check(N.lib().bfpp_feasible(C.byref(model._c()), C.byref(config._c()), C.byref(cluster._c()),
+                                 opts.dp0_bytes_per_param, opts.headroom, C.byref(r)))
+    return bool(r.value)
+
+
+def cluster_preset(name: str) -> ClusterSpec:
+    """The reference's presets (types.cpp:206-231: "a100", "v100-dgx1") plus "b200"."""
+    k = N.ClusterSpecC()
+    _check(N.lib().bfpp_cluster_preset(name.encode(), C.byref(k)))
+    return ClusterSpec(k.n_node, k.s_node, k.peak_flops, k.bw_intra, k.bw_inter, k.pp_latency, k.mem_capacity,
+                       k.kernel_efficiency)
+
+
 def param_count(model: ModelSpec) -> int:
     return 12 * model.n_layers * model.s_hidden * model.s_hidden
 

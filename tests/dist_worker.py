@@ -54,6 +54,14 @@ CASES = {
                                          schedule="BreadthFirst", model="small", steps=3),
     "steps3_small_bf_pp2x1_dp2_fs": dict(n_dp=2, n_pp=2, n_loop=1, n_mb=2, dp_variant="DP_FS",
                                          schedule="BreadthFirst", model="small", steps=3),
+    # activation checkpointing (recompute in the backward) with the pooled sharded gradients,
+    # pipeline hand-offs and several optimizer steps; and a multi-unit (depth-first) DP_FS stage
+    "steps3_tiny_bf_pp2x2_dp2_fs_rc": dict(n_dp=2, n_pp=2, n_loop=2, n_mb=4, dp_variant="DP_FS",
+                                           schedule="BreadthFirst", steps=3, recompute=True),
+    "tiny_df_pp2x2_dp2_fs_rc": dict(n_dp=2, n_pp=2, n_loop=2, n_mb=4, dp_variant="DP_FS", schedule="DepthFirst",
+                                    recompute=True),
+    "steps3_small_1f1b_pp2_dp2_fs_rc": dict(n_dp=2, n_pp=2, n_loop=1, n_mb=4, dp_variant="DP_FS",
+                                            schedule="OneFOneB", model="small", steps=3, recompute=True),
 }
 
 
@@ -63,6 +71,10 @@ def model_of(name):
 
 def steps_of(name):
     return CASES[name].get("steps", 0)
+
+
+def recompute_of(name):
+    return CASES[name].get("recompute", False)
 
 
 def accumulation_graph(name):
@@ -79,6 +91,7 @@ def config_of(name):
     c = dict(CASES[name])
     c.pop("model", None)
     c.pop("steps", None)
+    c.pop("recompute", None)
     if "accumulation" in c:
         from paper_2211_05953_b200.executor import accumulation_config
         return accumulation_config(model_of(name), ps.DpVariant[c["dp_variant"]], c["n_mb"], c["n_dp"])
@@ -109,7 +122,7 @@ def main():
         obj = [comm_ids(config) if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         return Executor(cfg, config, rank=rank, world=world, device=local, uids=obj[0],
-                        graph=accumulation_graph(a.case), **kw)
+                        graph=accumulation_graph(a.case), recompute=recompute_of(a.case), **kw)
 
     if n_steps:
         params, tokens = H.make_steps_case(cfg, config, n_steps)

@@ -45,6 +45,9 @@ def ref():
             "ref_simulate": (C.c_int, [P, T] + [C.POINTER(C.c_double)] * 5),
             "ref_peak_inflight": (C.c_int, [M, Cf, T, C.POINTER(C.c_int64)]),
             "ref_compute_per_gpu": (C.c_double, [M, Cf]),
+            "ref_total_memory": (C.c_int, [M, Cf, C.c_double, C.POINTER(C.c_double)]),
+            "ref_feasible": (C.c_int, [M, Cf, C.c_double, C.c_double, C.c_double, C.POINTER(C.c_int32)]),
+            "ref_cluster_preset": (C.c_int, [C.c_char_p, C.POINTER(N.ClusterSpecC)]),
             "ref_timeline_text": (C.c_int, [P, T, C.c_int32, C.c_char_p, C.c_int64, C.POINTER(C.c_int64)]),
             "ref_time_schedule_path": (C.c_int, [M, Cf, T, C.c_int, C.POINTER(C.c_double),
                                                  C.POINTER(C.c_double), C.POINTER(C.c_int64)]),

@@ -152,3 +152,39 @@ def test_cli_execute_writes_measured_trace(tmp_path, capsys, cuda_device):
     doc = json.loads(trace.read_text())
     assert sum(e["ph"] == "X" for e in doc["traceEvents"]) == 2 * 2 * 2  # (fwd + bwd) x 2 stages x 2 mb
     assert svg.read_text().startswith("<svg")
+
+
+RC_CONFIGS = {
+    "tiny_bf_loop2_mb3_rc": (H.TINY, ps.ParallelConfig(n_mb=3, n_loop=2, schedule=S.BreadthFirst)),
+    "tiny_df_loop2_mb2_rc": (H.TINY, ps.ParallelConfig(n_mb=2, n_loop=2, schedule=S.DepthFirst)),
+    "small_bf_loop2_mb2_smb2_rc": (SMALL, ps.ParallelConfig(n_mb=2, s_mb=2, n_loop=2, schedule=S.BreadthFirst)),
+}
+
+
+@pytest.mark.parametrize("name", list(RC_CONFIGS))
+def test_executor_recompute_matches_oracle(cuda_device, name):
+    """Activation checkpointing: each layer's forward recomputed from its checkpoint inside the
+    backward (and the LM head's logits), gradients and a 3-step trajectory vs the oracle."""
+    from paper_2211_05953_b200.executor import Executor
+    cfg, config = RC_CONFIGS[name]
+    params, tokens = H.make_case(cfg, config)
+    res = H.run_rank(lambda **kw: Executor(cfg, config, recompute=True, **kw), cfg, config, params, tokens, 0)
+    rep = H.compare(cfg, config, [res], params, tokens)
+    params, tokens = H.make_steps_case(cfg, config, n_steps=3)
+    res = H.run_rank_steps(lambda **kw: Executor(cfg, config, recompute=True, **kw), cfg, config, params, tokens, 0)
+    rep2 = H.compare_steps(cfg, config, [res], params, tokens)
+    print(name, rep["losses"], max(rep["grad_rel"].values()), rep2["losses"])
+
+
+@pytest.mark.parametrize("recompute", [False, True])
+def test_executor_memory_matches_plan(cuda_device, recompute):
+    """The live executor allocates exactly what the host-side plan (bfpp_exec_memory_plan, no GPU)
+    says, category by category."""
+    from paper_2211_05953_b200.executor import Executor, memory_plan
+    for cfg, config in ((SMALL, ps.ParallelConfig(n_mb=2, n_loop=2, schedule=S.BreadthFirst)),
+                        (H.TINY, ps.ParallelConfig(n_mb=4, n_loop=2, schedule=S.DepthFirst))):
+        ex = Executor(cfg, config, recompute=recompute)
+        live = ex.memory()
+        assert live == memory_plan(cfg, config, 0, recompute=recompute)
+        assert live["total"] == ex.device_bytes
+        ex.close()

@@ -136,7 +136,7 @@ def _worker(rank, world, port, name, q):
                                 schedule=ps.Schedule.BreadthFirst if loops is None else sched)
         ids = [comm_ids(cfg) if rank == 0 else None]      # NCCL unique ids, as execute_distributed
         dist.broadcast_object_list(ids, src=0)
-        plan = plan_rank(graph, rank % n_pp, n_dp)
+        plan = plan_rank(graph, rank % n_pp, n_dp, variant)
         # per-task "measured" times of this rank's tasks (simulated durations stand in for CUDA events)
         sim = ps.simulate(graph, ps.TimingModel(t_fwd_stage=1.0, bwd_ratio=2.0, t_pp_transfer=0.1,
                                                 t_dp_reduce_stage=0.3, t_dp_reconstruct_stage=0.2))
@@ -180,7 +180,8 @@ def test_multirank_plan_emulation(name):
 def _local_plans(name):
     n_pp, n_dp = CASES[name][:2]
     graph = _case_graph(name)
-    return graph, {r: plan_rank(graph, r % n_pp, n_dp) for r in range(n_pp * n_dp)}, n_pp, n_dp
+    variant = CASES[name][4]
+    return graph, {r: plan_rank(graph, r % n_pp, n_dp, variant) for r in range(n_pp * n_dp)}, n_pp, n_dp
 
 
 def test_emulator_detects_mismatched_collective_order():
