@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-timeline", action="store_true")
+    ap.add_argument("--recompute", action="store_true", help="activation checkpointing (recompute in the backward)")
     return ap.parse_args()
 
 
@@ -166,6 +167,58 @@ def reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+NVLINK_GBS_PER_DIR = 770.0  # measured NVLink 5 peer-copy bandwidth per direction
+
+
+def comm_rates(ex, cfg, config, tl, s_mb):
+    """Achieved bandwidth of the measured timeline's communication tasks (NCCL / peer
+    copies are NVLink-bound): each Transfer moves one [s_mb*seq, h] bf16 activation (or gradient)
+    to the ring neighbour; each Reconstruct all-gathers a stage's bf16 weights, (n_dp-1)/n_dp of
+    which arrive over NVLink per rank. Under the per-segment early reduce the Reduce tasks only hold
+    the tail segments, so they are not rated."""
+    from paper_2211_05953_b200 import pipesim as ps
+    out = {}
+    ev = tl.events
+    tasks = ex.graph.tasks
+    xfer = [ev[t.id].end - ev[t.id].start for t in tasks if t.kind == ps.TaskKind.Transfer]
+    if xfer:
+        b = 2.0 * s_mb * cfg.s_seq * cfg.s_hidden
+        med = float(np.median(xfer))
+        out["transfer"] = {"count": len(xfer), "bytes": b, "median_us": med * 1e6,
+                           "gbs_median": b / med / 1e9 if med > 0 else None,
+                           "frac_of_nvlink_dir": b / med / 1e9 / NVLINK_GBS_PER_DIR if med > 0 else None}
+    if config.n_dp >= 2:
+        rec = [(t, ev[t.id].end - ev[t.id].start) for t in tasks if t.kind == ps.TaskKind.Reconstruct
+               and t.stage in ex.local_stages]
+        if rec:
+            rates = [2.0 * ex.stage_numel(t.stage) * (config.n_dp - 1) / config.n_dp / d / 1e9 for t, d in rec if d > 0]
+            out["reconstruct"] = {"count": len(rec), "gbs_median": float(np.median(rates)),
+                                  "frac_of_nvlink_dir": float(np.median(rates)) / NVLINK_GBS_PER_DIR,
+                                  "median_us": float(np.median([d for _, d in rec])) * 1e6}
+    return out or None
+
+
+def memory_report(ex, cfg, config, recompute, used):
+    """Allocated device bytes by category (== the host-side plan), the device's used bytes (incl.
+    CUDA context and NCCL buffers), and the reference's analytic total_memory / feasible for the
+    same config on the B200 preset (memory.cpp:72-86)."""
+    from paper_2211_05953_b200 import pipesim as ps
+    from paper_2211_05953_b200.executor import memory_plan
+    m = ps.ModelSpec(n_layers=cfg.n_layers, s_hidden=cfg.s_hidden, n_heads=cfg.n_heads, s_seq=cfg.s_seq,
+                     s_voc=cfg.s_voc)
+    live = ex.memory()
+    plan = memory_plan(cfg, config, ex.rank, recompute=recompute)
+    ref = ps.total_memory(m, config)
+    b200 = ps.cluster_preset("b200")
+    return {"allocated": live, "plan_total": plan["total"], "plan_matches": plan == live, "device_used": used,
+            "recompute": recompute,
+            "reference_total_memory": {"state": ref.state_bytes, "activation": ref.activation_bytes,
+                                       "checkpoint": ref.checkpoint_bytes, "total": ref.total_bytes},
+            "reference_feasible_b200": ps.feasible(m, config, b200),
+            "allocated_over_reference": live["total"] / ref.total_bytes if ref.total_bytes else None,
+            "allocated_frac_of_hbm": live["total"] / b200.mem_capacity}
+
+
 def _progress(msg):
     if os.environ.get("BFPP_BENCH_VERBOSE"):
         print(f"[rank {os.environ.get('RANK', '0')}] {msg}", file=sys.stderr, flush=True)
@@ -204,7 +257,7 @@ def main():
         obj = [comm_ids(config) if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uids = obj[0]
-    ex = Executor(cfg, config, rank=rank, world=world, device=local, uids=uids, lr=1e-4)
+    ex = Executor(cfg, config, rank=rank, world=world, device=local, uids=uids, lr=1e-4, recompute=args.recompute)
     stream = torch.cuda.ExternalStream(ex.stream_handle)
     T = args.s_mb * cfg.s_seq
     g = torch.Generator(device="cuda").manual_seed(1234 + rank // pp)
@@ -237,6 +290,8 @@ def main():
         e1.record(stream)
         barrier()
     _progress('timed done')
+    free_b, total_b = torch.cuda.mem_get_info(local)
+    mem_used = total_b - free_b
     ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
     launches_step = sum(v[0] for v in ex.kernel_stats().values())
     tokens_per_step = n_mb * args.s_mb * dp * cfg.s_seq
@@ -280,6 +335,7 @@ def main():
     ex.sync()
     kst = ex.kernel_stats()
     bubble = None
+    comm = None
     sim_bubble = None
     replay_bubble = None
     peak_layers = None
@@ -301,6 +357,7 @@ def main():
         # the same graph simulated with the measured per-kind task durations
         replay_bubble = ps.bubble_fraction(ps.simulate(ex.graph, ps.measured_timing_model(ex.graph, tl)))
         peak_layers = max(ps.peak_inflight(tl, ex.graph, ps.place_stages(ex.model, config)))
+        comm = comm_rates(ex, cfg, config, tl, args.s_mb)
     ex.set_flags(False, False)
 
     pk, pk_kind = peaks()
@@ -379,6 +436,8 @@ def main():
             "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clocks, "roofline": roofline,
             "cpu_baseline": cpu,
             "device_bytes_per_rank": ex.device_bytes,
+            "memory": memory_report(ex, cfg, config, args.recompute, mem_used),
+            "comm": comm,
         }
         print(json.dumps(line), flush=True)
     ex.close()

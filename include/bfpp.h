@@ -80,6 +80,38 @@ int bfpp_feasible(const bfpp_model_spec* m, const bfpp_parallel_config* c, const
 /* replaces cluster_preset (types.cpp:206-231): "a100", "v100-dgx1", and "b200" (new) */
 int bfpp_cluster_preset(const char* name, bfpp_cluster_spec* out);
 
+/* Configuration search (replaces enumerate_configs + rank_configs, search.cpp:62-188; n_tp = 1).
+ * Measured per-kind task costs in units that carry across configurations (see rates_from_timing). */
+typedef struct bfpp_measured_rates {
+    double fwd_layer_seq;           /* forward seconds per layer per sequence (s_mb = 1) */
+    double bwd_ratio;               /* backward / forward */
+    double pp_s_per_byte, pp_latency;
+    double reduce_s_per_param;      /* DP reduction seconds per stage parameter */
+    double reconstruct_s_per_param; /* DP_FS reconstruction seconds per stage parameter */
+} bfpp_measured_rates;
+typedef struct bfpp_ranked_config {
+    bfpp_parallel_config config;
+    double score;        /* flop/s per GPU: Eq. 11 over the simulated makespan (perf.cpp:8-20) */
+    double memory_bytes; /* total_memory (memory.cpp:72-80) */
+    double bubble;       /* bubble_fraction of the simulated timeline */
+    bfpp_timing_model timing;
+} bfpp_ranked_config;
+/* rates of a (measured) timing model at configuration c: divides out c's stage size, micro-batch
+ * size and message sizes */
+int bfpp_rates_from_timing(const bfpp_model_spec* m, const bfpp_parallel_config* c, const bfpp_timing_model* t,
+                           bfpp_measured_rates* out);
+/* Enumerates the space (choice arrays; the reference's sharding policy and grid rules), keeps the
+ * feasible configs (total_memory <= headroom * mem_capacity), simulates each with
+ * TimingModel::derive (scoring 0, the reference's "simulate" mode) or with the measured rates
+ * (scoring 1), and returns them best first (ties: lower memory, less model parallelism).
+ * Two-phase sizing: cap = 0 returns the count in *n_out. */
+int bfpp_rank_configs(const bfpp_model_spec* m, const bfpp_cluster_spec* k, const int32_t* schedules, int64_t n_sched,
+                      const int32_t* dp_variants, int64_t n_var, const int64_t* n_pp, int64_t n_n_pp,
+                      const int64_t* s_mb, int64_t n_s_mb, const int64_t* n_mb, int64_t n_n_mb,
+                      const int64_t* n_loop, int64_t n_n_loop, const int64_t* batch_sizes, int64_t n_batch,
+                      int32_t scoring, const bfpp_measured_rates* rates, double dp0_bytes_per_param, double headroom,
+                      int32_t threads, int64_t cap, bfpp_ranked_config* out, int64_t* n_out);
+
 /* replaces place_stages (schedule.hpp:20, schedule.cpp:23-33). assignment_out
  * receives n_stage entries (cap must be >= n_pp*n_loop). */
 int bfpp_place_stages(const bfpp_model_spec* m, const bfpp_parallel_config* c, int64_t* assignment_out,

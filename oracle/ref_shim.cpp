@@ -226,6 +226,46 @@ int ref_feasible(const bfpp_model_spec* m, const bfpp_parallel_config* c, double
     });
 }
 
+// enumerate_configs + rank_configs(Scoring::Simulate) of the reference (search.cpp:62-188), n_tp = 1
+int ref_rank_configs(const bfpp_model_spec* m, const bfpp_cluster_spec* k, const int32_t* schedules, int64_t n_sched,
+                     const int32_t* dp_variants, int64_t n_var, const int64_t* n_pp, int64_t n_n_pp,
+                     const int64_t* s_mb, int64_t n_s_mb, const int64_t* n_mb, int64_t n_n_mb, const int64_t* n_loop,
+                     int64_t n_n_loop, const int64_t* batch_sizes, int64_t n_batch, int32_t threads, int64_t cap,
+                     bfpp_parallel_config* configs, double* scores, int64_t* n_out) {
+    return guard([&] {
+        SearchSpace sp;
+        for (int64_t i = 0; i < n_sched; ++i) sp.schedules.insert(static_cast<Schedule>(schedules[i]));
+        for (int64_t i = 0; i < n_var; ++i) sp.dp_variants.insert(static_cast<DpVariant>(dp_variants[i]));
+        sp.n_pp_choices.insert(n_pp, n_pp + n_n_pp);
+        sp.n_tp_choices = {1};
+        sp.s_mb_choices.insert(s_mb, s_mb + n_s_mb);
+        sp.n_mb_choices.insert(n_mb, n_mb + n_n_mb);
+        sp.n_loop_choices.insert(n_loop, n_loop + n_n_loop);
+        sp.batch_sizes.insert(batch_sizes, batch_sizes + n_batch);
+        ClusterSpec c;
+        c.n_node = k->n_node;
+        c.s_node = k->s_node;
+        c.peak_flops = k->peak_flops;
+        c.bw_intra = k->bw_intra;
+        c.bw_inter = k->bw_inter;
+        c.pp_latency = k->pp_latency;
+        c.mem_capacity = k->mem_capacity;
+        c.kernel_efficiency = k->kernel_efficiency;
+        const ModelSpec mm = model_of(m);
+        SearchOptions so;
+        so.threads = threads;
+        const std::vector<RankedConfig> r = rank_configs(enumerate_configs(sp, mm, c), mm, c, Scoring::Simulate, so);
+        *n_out = static_cast<int64_t>(r.size());
+        if (cap < *n_out) return;
+        for (size_t i = 0; i < r.size(); ++i) {
+            const ParallelConfig& p = r[i].config;
+            configs[i] = {p.n_dp, p.n_tp, p.n_pp, p.n_mb, p.s_mb, p.n_loop, static_cast<int32_t>(p.dp_variant),
+                          static_cast<int32_t>(p.schedule)};
+            scores[i] = r[i].score;
+        }
+    });
+}
+
 int ref_cluster_preset(const char* name, bfpp_cluster_spec* out) {
     return guard([&] {
         const ClusterSpec k = cluster_preset(name);

@@ -40,6 +40,17 @@ class TaskC(C.Structure):
                 ("stage", C.c_int64)]
 
 
+class MeasuredRatesC(C.Structure):
+    _fields_ = [("fwd_layer_seq", C.c_double), ("bwd_ratio", C.c_double), ("pp_s_per_byte", C.c_double),
+                ("pp_latency", C.c_double), ("reduce_s_per_param", C.c_double),
+                ("reconstruct_s_per_param", C.c_double)]
+
+
+class RankedConfigC(C.Structure):
+    _fields_ = [("config", ParallelConfigC), ("score", C.c_double), ("memory_bytes", C.c_double),
+                ("bubble", C.c_double), ("timing", TimingModelC)]
+
+
 class ExecOptsC(C.Structure):
     _fields_ = [("device", C.c_int32), ("record_timeline", C.c_int32), ("seed", C.c_uint64),
                 ("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
@@ -84,6 +95,12 @@ _PROTOS = {
     "bfpp_feasible": (C.c_int, [C.POINTER(ModelSpecC), C.POINTER(ParallelConfigC), C.POINTER(ClusterSpecC),
                                 C.c_double, C.c_double, _I32P]),
     "bfpp_cluster_preset": (C.c_int, [C.c_char_p, C.POINTER(ClusterSpecC)]),
+    "bfpp_rates_from_timing": (C.c_int, [C.POINTER(ModelSpecC), C.POINTER(ParallelConfigC),
+                                         C.POINTER(TimingModelC), C.POINTER(MeasuredRatesC)]),
+    "bfpp_rank_configs": (C.c_int, [C.POINTER(ModelSpecC), C.POINTER(ClusterSpecC), _I32P, C.c_int64, _I32P,
+                                    C.c_int64] + [_I64P, C.c_int64] * 5
+                          + [C.c_int32, C.POINTER(MeasuredRatesC), C.c_double, C.c_double, C.c_int32, C.c_int64,
+                             C.POINTER(RankedConfigC), _I64P]),
     "bfpp_chrome_trace_json": (C.c_int, [_P, _P, C.c_char_p, C.c_int64, _I64P]),
     "bfpp_gantt_svg": (C.c_int, [_P, _P, C.c_char_p, C.c_int64, _I64P]),
     "bfpp_measured_timing_model": (C.c_int, [_P, _P, C.POINTER(TimingModelC)]),

@@ -1087,8 +1087,10 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
             const bool early = te.unit_end_bwd && ls.w16_shard != nullptr && ls.seg.size() > 2;
             const bool guard = te.first_in_unit && I.gbuf != nullptr;
             const size_t nl = L.layers.size();
+            // end of layer li's parameters in the stage vector (the last layer of a non-last stage
+            // runs to the padded end; n_dp == 1 here for the optimizer segments, so shard = stage)
             auto layer_end = [&](size_t li) -> int64_t {
-                return li + 1 < nl ? L.layers[li + 1].ln1_g : (L.last ? L.lnf_g : ls.shard_n);
+                return li + 1 < nl ? L.layers[li + 1].ln1_g : (L.last ? L.lnf_g : L.padded);
             };
             // the wgrad stream also writes this stage's gradient buffer: honour the same
             // resource waits (previous unit's reduce-scatter) as the compute stream

@@ -301,6 +301,80 @@ int bfpp_cluster_preset(const char* name, bfpp_cluster_spec* out) {
     });
 }
 
+int bfpp_rates_from_timing(const bfpp_model_spec* m, const bfpp_parallel_config* c, const bfpp_timing_model* t,
+                           bfpp_measured_rates* out) {
+    return guarded([&] {
+        TimingModel tm;
+        tm.t_fwd_stage = t->t_fwd_stage;
+        tm.bwd_ratio = t->bwd_ratio;
+        tm.t_pp_transfer = t->t_pp_transfer;
+        tm.pp_latency = t->pp_latency;
+        tm.t_dp_reduce_stage = t->t_dp_reduce_stage;
+        tm.t_dp_reconstruct_stage = t->t_dp_reconstruct_stage;
+        const MeasuredRates r = rates_from_timing(to_model(m), to_config(c), tm);
+        *out = {r.fwd_layer_seq, r.bwd_ratio, r.pp_s_per_byte, r.pp_latency, r.reduce_s_per_param,
+                r.reconstruct_s_per_param};
+    });
+}
+
+int bfpp_rank_configs(const bfpp_model_spec* m, const bfpp_cluster_spec* k, const int32_t* schedules, int64_t n_sched,
+                      const int32_t* dp_variants, int64_t n_var, const int64_t* n_pp, int64_t n_n_pp,
+                      const int64_t* s_mb, int64_t n_s_mb, const int64_t* n_mb, int64_t n_n_mb,
+                      const int64_t* n_loop, int64_t n_n_loop, const int64_t* batch_sizes, int64_t n_batch,
+                      int32_t scoring, const bfpp_measured_rates* rates, double dp0_bytes_per_param, double headroom,
+                      int32_t threads, int64_t cap, bfpp_ranked_config* out, int64_t* n_out) {
+    return guarded([&] {
+        SearchSpace sp;
+        sp.schedules.assign(schedules, schedules + n_sched);
+        sp.dp_variants.assign(dp_variants, dp_variants + n_var);
+        sp.n_pp.assign(n_pp, n_pp + n_n_pp);
+        sp.n_tp = {1};
+        sp.s_mb.assign(s_mb, s_mb + n_s_mb);
+        sp.n_mb.assign(n_mb, n_mb + n_n_mb);
+        sp.n_loop.assign(n_loop, n_loop + n_n_loop);
+        sp.batch_sizes.assign(batch_sizes, batch_sizes + n_batch);
+        for (int32_t s : sp.schedules)
+            if (s < 0 || s > 4) throw SpecError("search: unknown schedule");
+        for (int32_t v : sp.dp_variants)
+            if (v < 0 || v > 2) throw SpecError("search: unknown data-parallel variant");
+        if (scoring == 1 && !rates) throw SpecError("search: measured scoring needs rates");
+        ClusterSpec kc;
+        kc.n_node = k->n_node;
+        kc.s_node = k->s_node;
+        kc.peak_flops = k->peak_flops;
+        kc.bw_intra = k->bw_intra;
+        kc.bw_inter = k->bw_inter;
+        kc.pp_latency = k->pp_latency;
+        kc.mem_capacity = k->mem_capacity;
+        kc.kernel_efficiency = k->kernel_efficiency;
+        MeasuredRates r;
+        if (rates)
+            r = {rates->fwd_layer_seq, rates->bwd_ratio, rates->pp_s_per_byte, rates->pp_latency,
+                 rates->reduce_s_per_param, rates->reconstruct_s_per_param};
+        MemoryOptions mo;
+        mo.dp0_bytes_per_param = dp0_bytes_per_param;
+        mo.headroom = headroom;
+        const ModelSpec mm = to_model(m);
+        const std::vector<RankedConfig> ranked =
+            rank_configs(enumerate_configs(sp, mm, kc), mm, kc, scoring == 1, r, mo, threads);
+        *n_out = static_cast<int64_t>(ranked.size());
+        if (cap == 0) return;
+        if (cap < *n_out) throw SpecError("search: output array smaller than the ranked list");
+        for (size_t i = 0; i < ranked.size(); ++i) {
+            const RankedConfig& rc = ranked[i];
+            bfpp_ranked_config& o = out[i];
+            o.config = {rc.config.n_dp, rc.config.n_tp, rc.config.n_pp, rc.config.n_mb, rc.config.s_mb,
+                        rc.config.n_loop, static_cast<int32_t>(rc.config.dp_variant),
+                        static_cast<int32_t>(rc.config.schedule)};
+            o.score = rc.score;
+            o.memory_bytes = rc.memory_bytes;
+            o.bubble = rc.bubble;
+            o.timing = {rc.timing.t_fwd_stage, rc.timing.bwd_ratio, rc.timing.t_pp_transfer, rc.timing.pp_latency,
+                        rc.timing.t_dp_reduce_stage, rc.timing.t_dp_reconstruct_stage};
+        }
+    });
+}
+
 double bfpp_compute_per_gpu(const bfpp_model_spec* m, const bfpp_parallel_config* c) {
     try {
         return compute_per_gpu(to_model(m), to_config(c));

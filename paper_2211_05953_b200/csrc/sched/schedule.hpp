@@ -136,4 +136,31 @@ bool feasible(const ModelSpec& m, const ParallelConfig& c, const ClusterSpec& k,
 // "a100", "v100-dgx1" (the reference's, types.cpp:206-231) and "b200"
 ClusterSpec cluster_preset(const std::string& name);
 
+// Configuration search (search.cpp, restated in search.cpp) + measured scoring.
+TimingModel derive_timing(const ModelSpec& m, const ParallelConfig& c, const ClusterSpec& k, bool recompute = false);
+// Per-kind task costs measured at one configuration, in units that carry to another:
+// forward seconds per layer per sequence, the backward/forward ratio, seconds per hand-off byte,
+// DP seconds per stage parameter (reduce-scatter of the f32 gradient / all-gather of bf16 weights).
+struct MeasuredRates {
+    double fwd_layer_seq = 0, bwd_ratio = 2, pp_s_per_byte = 0, pp_latency = 0, reduce_s_per_param = 0,
+           reconstruct_s_per_param = 0;
+};
+MeasuredRates rates_from_timing(const ModelSpec& m, const ParallelConfig& c, const TimingModel& t);
+TimingModel timing_from_rates(const ModelSpec& m, const ParallelConfig& c, const MeasuredRates& r);
+struct SearchSpace {
+    std::vector<int> schedules, dp_variants;
+    std::vector<i64> n_pp, n_tp, s_mb, n_mb, n_loop, batch_sizes;
+};
+struct RankedConfig {
+    ParallelConfig config;
+    double score = 0.0;  // flop/s per GPU (Eq. 11 over the simulated makespan)
+    double memory_bytes = 0.0, bubble = 0.0;
+    TimingModel timing;
+};
+std::vector<ParallelConfig> enumerate_configs(const SearchSpace& sp, const ModelSpec& m, const ClusterSpec& k);
+// measured = false: the reference's simulate scoring (TimingModel::derive); true: timing_from_rates
+std::vector<RankedConfig> rank_configs(const std::vector<ParallelConfig>& configs, const ModelSpec& m,
+                                       const ClusterSpec& k, bool measured, const MeasuredRates& rates,
+                                       const MemoryOptions& mo, int threads);
+
 }  // namespace bfpp
