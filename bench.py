@@ -12,6 +12,7 @@ Inputs are synthetic token ids; weights are random-initialised on device.
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import subprocess
@@ -336,6 +337,7 @@ def main():
     kst = ex.kernel_stats()
     bubble = None
     comm = None
+    measured_timing = None
     sim_bubble = None
     replay_bubble = None
     peak_layers = None
@@ -355,7 +357,12 @@ def main():
         bubble = ps.bubble_fraction(tl)
         sim_bubble = (pp - 1) / (n_mb * loops)
         # the same graph simulated with the measured per-kind task durations
-        replay_bubble = ps.bubble_fraction(ps.simulate(ex.graph, ps.measured_timing_model(ex.graph, tl)))
+        mtm = ps.measured_timing_model(ex.graph, tl)
+        replay_bubble = ps.bubble_fraction(ps.simulate(ex.graph, mtm))
+        mspec = ps.ModelSpec(n_layers=cfg.n_layers, s_hidden=cfg.s_hidden, n_heads=cfg.n_heads, s_seq=cfg.s_seq,
+                             s_voc=cfg.s_voc)
+        measured_timing = {"timing_model": dataclasses.asdict(mtm),
+                           "rates": dataclasses.asdict(ps.rates_from_timing(mspec, config, mtm))}
         peak_layers = max(ps.peak_inflight(tl, ex.graph, ps.place_stages(ex.model, config)))
         comm = comm_rates(ex, cfg, config, tl, args.s_mb)
     ex.set_flags(False, False)
@@ -438,6 +445,7 @@ def main():
             "device_bytes_per_rank": ex.device_bytes,
             "memory": memory_report(ex, cfg, config, args.recompute, mem_used),
             "comm": comm,
+            "measured_timing": measured_timing,
         }
         print(json.dumps(line), flush=True)
     ex.close()

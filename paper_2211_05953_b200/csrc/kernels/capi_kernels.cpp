@@ -44,6 +44,13 @@ int bfpp_gemm_config(int32_t mode, int32_t bn2, int32_t stream_k) {
     });
 }
 
+int bfpp_gemm_sm_limit(int32_t n) {
+    return guarded([&] {
+        if (n < 0) throw SpecError("gemm_sm_limit: must be >= 0 (0 = all SMs)");
+        bfpp::gemm_sm_limit = n;
+    });
+}
+
 namespace {
 GemmArgs to_gemm(const bfpp_gemm_args* a) {
     GemmArgs g;

@@ -34,7 +34,8 @@ struct GemmArgs {
 };
 
 void gemm_bf16(const GemmArgs& g, cudaStream_t stream);
-extern int gemm_mode;  // -1 auto (2-CTA tiles when M, N >= 256), 1 force 1-CTA, 2 force 2-CTA
+extern int gemm_mode;
+extern int gemm_sm_limit;  // > 0: persistent grids sized to this many SMs (SM partition of the launching stream)  // -1 auto (2-CTA tiles when M, N >= 256), 1 force 1-CTA, 2 force 2-CTA
 void gemm_bf16_configure(int mode, int bn2, int stream_k);
 // Two independent GEMMs (same operand majors) in one grouped 2-CTA launch when eligible, else two launches.
 void gemm_bf16_pair(const GemmArgs& a, const GemmArgs& b, cudaStream_t st);

@@ -730,7 +730,8 @@ int num_sms() {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     }
-    return n;
+    // persistent grids launched into an SM partition (green context) size to the partition
+    return gemm_sm_limit > 0 && gemm_sm_limit < n ? gemm_sm_limit : n;
 }
 
 template <int BN, int A_MN, int B_MN>
@@ -866,6 +867,7 @@ void launch2(const GemmArgs& g, cudaStream_t st, const GemmArgs* second = nullpt
 
 int gemm_sk = 0;     // stream-K for the 2-CTA kernel: 0 off (default), 1 forced, -1 auto (BFPP_GEMM_SK)
 int gemm_mode = -1;  // -1 auto, 1 force 1-CTA, 2 force 2-CTA (benchmarks / tests)
+int gemm_sm_limit = 0;  // > 0: persistent grids sized to this many SMs (a green-context partition)
 int gemm_pdl = 0;    // programmatic dependent launch (BFPP_GEMM_PDL=1): measured no gain in-step (optimizer co-running)
 int gemm_bn2 = 0;    // 2-CTA pair-tile width: 0 / 256 default, 128 opt-in (BFPP_GEMM_BN2; tests)
 int gemm_pair = 1;   // grouped launches of independent GEMM pairs (BFPP_GEMM_PAIR=0: two launches)

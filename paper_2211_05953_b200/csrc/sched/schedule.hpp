@@ -137,7 +137,7 @@ bool feasible(const ModelSpec& m, const ParallelConfig& c, const ClusterSpec& k,
 ClusterSpec cluster_preset(const std::string& name);
 
 // Configuration search (search.cpp, restated in search.cpp) + measured scoring.
-TimingModel derive_timing(const ModelSpec& m, const ParallelConfig& c, const ClusterSpec& k, bool recompute = false);
+TimingModel derive_timing(const ModelSpec& m, const ParallelConfig& c, const ClusterSpec& k, bool recompute = true);
 // Per-kind task costs measured at one configuration, in units that carry to another:
 // forward seconds per layer per sequence, the backward/forward ratio, seconds per hand-off byte,
 // DP seconds per stage parameter (reduce-scatter of the f32 gradient / all-gather of bf16 weights).

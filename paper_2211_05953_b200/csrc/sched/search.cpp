@@ -44,7 +44,8 @@ double message_bytes(const ModelSpec& m, const ParallelConfig& c) {  // one [s_m
 
 }  // namespace
 
-// schedule.cpp:43-86 (n_tp = 1: no tensor-parallel blocking term)
+// schedule.cpp:43-86 (n_tp = 1: no tensor-parallel blocking term); recompute defaults to true as in
+// the reference (schedule.hpp:37-38)
 TimingModel derive_timing(const ModelSpec& m, const ParallelConfig& c, const ClusterSpec& k, bool recompute) {
     c.validate(m, k);
     if (c.n_tp != 1) throw SpecError("derive_timing: tensor parallelism is not modelled (n_tp must be 1)");
@@ -156,7 +157,8 @@ std::vector<RankedConfig> rank_configs(const std::vector<ParallelConfig>& config
         rc.memory_bytes = total_memory(m, rc.config, mo).total_bytes;
         const StagePlacement pl = place_stages(m, rc.config);
         const TaskGraph g = build_tasks(m, rc.config, pl);
-        rc.timing = measured ? timing_from_rates(m, rc.config, rates) : derive_timing(m, rc.config, k, false);
+        // simulate_score derives with the default recompute = true (schedule.hpp:37-38: bwd_ratio 3)
+        rc.timing = measured ? timing_from_rates(m, rc.config, rates) : derive_timing(m, rc.config, k);
         const Timeline tl = simulate(g, rc.timing);
         rc.config.validate(m, k);
         if (tl.makespan <= 0) throw SpecError("throughput: timeline has no extent");

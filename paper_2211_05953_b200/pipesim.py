@@ -424,6 +424,75 @@ def cluster_preset(name: str) -> ClusterSpec:
                        k.kernel_efficiency)
 
 
+@dataclass(frozen=True)
+class MeasuredRates:
+    """Per-kind task costs measured at one configuration, in units that carry to another
+    (forward s per layer per sequence, backward/forward, s per hand-off byte, DP s per stage param)."""
+    fwd_layer_seq: float
+    bwd_ratio: float
+    pp_s_per_byte: float
+    pp_latency: float
+    reduce_s_per_param: float
+    reconstruct_s_per_param: float
+
+    def _c(self):
+        return N.MeasuredRatesC(self.fwd_layer_seq, self.bwd_ratio, self.pp_s_per_byte, self.pp_latency,
+                                self.reduce_s_per_param, self.reconstruct_s_per_param)
+
+
+def rates_from_timing(model: ModelSpec, config: ParallelConfig, timing: TimingModel) -> MeasuredRates:
+    """Rates of a (measured) TimingModel at `config` (divides out stage size, s_mb, message sizes)."""
+    r = N.MeasuredRatesC()
+    _check(N.lib().bfpp_rates_from_timing(C.byref(model._c()), C.byref(config._c()), C.byref(timing._c()),
+                                          C.byref(r)))
+    return MeasuredRates(r.fwd_layer_seq, r.bwd_ratio, r.pp_s_per_byte, r.pp_latency, r.reduce_s_per_param,
+                         r.reconstruct_s_per_param)
+
+
+@dataclass(frozen=True)
+class RankedConfig:
+    config: ParallelConfig
+    score: float          # flop/s per GPU (Eq. 11 over the simulated makespan)
+    memory_bytes: float   # total_memory
+    bubble: float
+    timing: TimingModel
+
+
+def rank_configs(model: ModelSpec, cluster: ClusterSpec, *, schedules, dp_variants, n_pp, s_mb, n_mb, n_loop,
+                 batch_sizes, scoring: str = "simulate", rates: MeasuredRates | None = None,
+                 memory: MemoryOptions = MemoryOptions(), threads: int = 0) -> List[RankedConfig]:
+    """enumerate_configs + rank_configs (search.cpp:62-188, n_tp = 1): the feasible configurations of
+    the space, best first. scoring "simulate" = the reference's (TimingModel::derive); "measured" =
+    simulated with timing_from_rates(rates) (per-kind durations measured on B200s)."""
+    if scoring not in ("simulate", "measured"):
+        raise SpecError(f"unknown scoring mode '{scoring}' (expected simulate or measured)")
+    if scoring == "measured" and rates is None:
+        raise SpecError("measured scoring needs rates")
+    i32 = lambda xs: (C.c_int32 * len(xs))(*[int(x) for x in xs])  # noqa: E731
+    i64 = lambda xs: (C.c_int64 * len(xs))(*[int(x) for x in xs])  # noqa: E731
+    arrays = [i32(schedules), len(schedules), i32(dp_variants), len(dp_variants), i64(n_pp), len(n_pp), i64(s_mb),
+              len(s_mb), i64(n_mb), len(n_mb), i64(n_loop), len(n_loop), i64(batch_sizes), len(batch_sizes)]
+    rc = C.byref(rates._c()) if rates is not None else None
+    n = C.c_int64()
+    L = N.lib()
+    args = lambda cap, out: [C.byref(model._c()), C.byref(cluster._c())] + arrays + [  # noqa: E731
+        1 if scoring == "measured" else 0, rc, memory.dp0_bytes_per_param, memory.headroom, threads, cap, out,
+        C.byref(n)]
+    _check(L.bfpp_rank_configs(*args(0, None)))
+    buf = (N.RankedConfigC * max(1, n.value))()
+    _check(L.bfpp_rank_configs(*args(n.value, buf)))
+    out = []
+    for r in buf[:n.value]:
+        c = r.config
+        cfg = ParallelConfig(n_dp=c.n_dp, n_tp=c.n_tp, n_pp=c.n_pp, n_mb=c.n_mb, s_mb=c.s_mb, n_loop=c.n_loop,
+                             dp_variant=DpVariant(c.dp_variant), schedule=Schedule(c.schedule))
+        t = r.timing
+        out.append(RankedConfig(cfg, r.score, r.memory_bytes, r.bubble,
+                                TimingModel(t.t_fwd_stage, t.bwd_ratio, t.t_pp_transfer, t.pp_latency,
+                                            t.t_dp_reduce_stage, t.t_dp_reconstruct_stage)))
+    return out
+
+
 def param_count(model: ModelSpec) -> int:
     return 12 * model.n_layers * model.s_hidden * model.s_hidden
 

@@ -75,3 +75,53 @@ print(f"gemm alone {g_alone:.2f} ms ({flops_layer * LAYERS / g_alone / 1e9:.0f} 
       f"adam alone {a_alone:.2f} ms ({30.0 * n_param / a_alone / 1e6:.0f} GB/s)")
 print(f"together (adam x{k}): gemm {g_both:.2f} ms ({flops_layer * LAYERS / g_both / 1e9:.0f} TF/s), "
       f"adam {a_both:.2f} ms ({30.0 * n_param * k / a_both / 1e6:.0f} GB/s)")
+
+
+# ---- SM partition (green contexts): GEMM stream on N - k SMs, optimizer stream on k SMs ----
+def green_streams(k):
+    """Two CUDA streams confined to disjoint SM partitions of the current device (k SMs for the
+    second). Returns (big_stream, small_stream, n_big) or None when unsupported."""
+    from cuda.bindings import driver as d
+    dev = torch.cuda.current_device()
+    err, cudev = d.cuDeviceGet(dev)
+    err, res = d.cuDeviceGetDevResource(cudev, d.CUdevResourceType.CU_DEV_RESOURCE_TYPE_SM)
+    if err != d.CUresult.CUDA_SUCCESS:
+        return None
+    total = res.sm.smCount
+    # split off groups of k SMs: the first group goes to the optimizer, the remainder to the GEMMs
+    err, groups, n, rem = d.cuDevSmResourceSplitByCount(1, res, 0, k)
+    if err != d.CUresult.CUDA_SUCCESS:
+        print("split failed", err)
+        return None
+    out = []
+    for r in (rem, groups[0]):
+        err, desc = d.cuDevResourceGenerateDesc([r], 1)
+        err, gctx = d.cuGreenCtxCreate(desc, cudev, d.CUgreenCtxCreate_flags.CU_GREEN_CTX_DEFAULT_STREAM)
+        err, s = d.cuGreenCtxStreamCreate(gctx, d.CUstream_flags.CU_STREAM_NON_BLOCKING, 0)
+        out.append((int(s), r.sm.smCount))
+    print(f"partition: {out[0][1]} SMs (GEMM) + {out[1][1]} SMs (optimizer) of {total}")
+    return out
+
+
+if os.environ.get("GREEN_SPLIT"):
+    from paper_2211_05953_b200 import _native as NAT
+    for k in [int(x) for x in os.environ["GREEN_SPLIT"].split(",")]:
+        gs = green_streams(k)
+        if gs is None:
+            print("green contexts unavailable")
+            break
+        (sb, nb), (ss, ns) = gs
+        NAT.lib().bfpp_gemm_sm_limit(nb)
+        hi = torch.cuda.ExternalStream(sb)
+        lo = torch.cuda.ExternalStream(ss)
+        for _ in range(2):
+            timed(True, True, 1)
+        g_alone, _ = timed(True, False, 0)
+        _, a_alone = timed(False, True, 1)
+        kk = max(1, int(g_alone / a_alone))
+        g_both, a_both = timed(True, True, kk)
+        print(f"[{nb}+{ns} SMs] gemm alone {g_alone:.2f} ms ({flops_layer * LAYERS / g_alone / 1e9:.0f} TF/s); "
+              f"adam alone {a_alone:.2f} ms ({30.0 * n_param / a_alone / 1e6:.0f} GB/s); together (adam x{kk}): "
+              f"gemm {g_both:.2f} ms ({flops_layer * LAYERS / g_both / 1e9:.0f} TF/s), "
+              f"adam {a_both:.2f} ms ({30.0 * n_param * kk / a_both / 1e6:.0f} GB/s)")
+        NAT.lib().bfpp_gemm_sm_limit(0)

@@ -48,6 +48,11 @@ def ref():
             "ref_total_memory": (C.c_int, [M, Cf, C.c_double, C.POINTER(C.c_double)]),
             "ref_feasible": (C.c_int, [M, Cf, C.c_double, C.c_double, C.c_double, C.POINTER(C.c_int32)]),
             "ref_cluster_preset": (C.c_int, [C.c_char_p, C.POINTER(N.ClusterSpecC)]),
+            "ref_rank_configs": (C.c_int, [M, C.POINTER(N.ClusterSpecC), C.POINTER(C.c_int32), C.c_int64,
+                                           C.POINTER(C.c_int32), C.c_int64]
+                                 + [C.POINTER(C.c_int64), C.c_int64] * 5
+                                 + [C.c_int32, C.c_int64, C.POINTER(N.ParallelConfigC), C.POINTER(C.c_double),
+                                    C.POINTER(C.c_int64)]),
             "ref_timeline_text": (C.c_int, [P, T, C.c_int32, C.c_char_p, C.c_int64, C.POINTER(C.c_int64)]),
             "ref_time_schedule_path": (C.c_int, [M, Cf, T, C.c_int, C.POINTER(C.c_double),
                                                  C.POINTER(C.c_double), C.POINTER(C.c_int64)]),

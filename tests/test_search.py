@@ -1,0 +1,104 @@
+"""Configuration search: the reference's enumerate_configs + rank_configs in
+simulate mode (search.cpp:62-188) restated, checked against the compiled reference (same configs,
+same order, identical scores), and the "measured" scoring mode: candidates simulated with
+per-kind task costs measured at one configuration. Given the reference's own derived timing as
+the "measurement", measured scoring must reproduce the reference's ranking."""
+import ctypes as C
+
+import pytest
+
+import ref_oracle as R
+from paper_2211_05953_b200 import _native as N
+from paper_2211_05953_b200 import pipesim as ps
+
+S, V = ps.Schedule, ps.DpVariant
+needs_ref = pytest.mark.skipif(not R.available(), reason="oracle/_ref not built (needs /root/reference)")
+
+SPACES = {
+    "gpt6.7b_8gpu": (ps.ModelSpec(n_layers=32, s_hidden=4096, n_heads=32, s_seq=2048, s_voc=50304),
+                     dict(schedules=[1, 2, 3, 4], dp_variants=[0, 1, 2], n_pp=[1, 2, 4, 8], s_mb=[1, 2],
+                          n_mb=[2, 4, 8, 16, 32], n_loop=[1, 2, 4], batch_sizes=[16, 32, 64])),
+    "52b_8gpu": (ps.ModelSpec(n_layers=64, s_hidden=8192, n_heads=64, s_seq=1024, s_voc=30592),
+                 dict(schedules=[0, 1, 2, 3, 4], dp_variants=[0, 2], n_pp=[2, 4, 8], s_mb=[1],
+                      n_mb=[4, 8, 16], n_loop=[1, 2, 4, 8], batch_sizes=[16, 32])),
+}
+
+
+def _ref_rank(model, cluster, sp):
+    L = R.ref()
+    i32 = lambda xs: (C.c_int32 * len(xs))(*xs)  # noqa: E731
+    i64 = lambda xs: (C.c_int64 * len(xs))(*xs)  # noqa: E731
+    arrays = [i32(sp["schedules"]), len(sp["schedules"]), i32(sp["dp_variants"]), len(sp["dp_variants"])]
+    for k in ("n_pp", "s_mb", "n_mb", "n_loop", "batch_sizes"):
+        arrays += [i64(sp[k]), len(sp[k])]
+    n = C.c_int64()
+    assert L.ref_rank_configs(C.byref(model._c()), C.byref(cluster._c()), *arrays, 4, 0, None, None,
+                              C.byref(n)) == 0, L.ref_last_error()
+    cfgs = (N.ParallelConfigC * n.value)()
+    scores = (C.c_double * n.value)()
+    assert L.ref_rank_configs(C.byref(model._c()), C.byref(cluster._c()), *arrays, 4, n.value, cfgs, scores,
+                              C.byref(n)) == 0
+    key = lambda c: (c.n_dp, c.n_tp, c.n_pp, c.n_mb, c.s_mb, c.n_loop, c.dp_variant, c.schedule)  # noqa: E731
+    return [(key(c), s) for c, s in zip(cfgs, scores)]
+
+
+def _key(c: ps.ParallelConfig):
+    return (c.n_dp, c.n_tp, c.n_pp, c.n_mb, c.s_mb, c.n_loop, int(c.dp_variant), int(c.schedule))
+
+
+@needs_ref
+@pytest.mark.parametrize("name", list(SPACES))
+@pytest.mark.parametrize("cluster", ["a100", "b200"])
+def test_simulate_ranking_matches_reference(name, cluster):
+    model, sp = SPACES[name]
+    k = ps.cluster_preset(cluster)
+    if cluster == "a100":  # the reference's 32-GPU preset: search one 8-GPU node of it
+        k = ps.ClusterSpec(1, 8, k.peak_flops, k.bw_intra, k.bw_inter, k.pp_latency, k.mem_capacity,
+                           k.kernel_efficiency)
+    ours = ps.rank_configs(model, k, threads=4, **sp)
+    ref = _ref_rank(model, k, sp)
+    assert len(ours) == len(ref) and len(ref) > 5
+    assert [_key(r.config) for r in ours] == [c for c, _ in ref]
+    assert [r.score for r in ours] == [s for _, s in ref]
+
+
+@needs_ref
+@pytest.mark.parametrize("name", list(SPACES))
+def test_measured_scoring_reproduces_reference_given_its_timing(name):
+    """Rates taken from TimingModel::derive at one configuration carry to every other one (forward
+    time linear in layers per stage and s_mb, hand-off time in message bytes, DP time in stage
+    parameters), so measured scoring with them ranks exactly as the reference's simulate mode."""
+    model, sp = SPACES[name]
+    k = ps.cluster_preset("b200")
+    ref = _ref_rank(model, k, sp)
+    at = ps.ParallelConfig(n_dp=2, n_pp=4, n_loop=1, n_mb=8, dp_variant=V.DP0, schedule=S.OneFOneB)
+    ranked_sim = ps.rank_configs(model, k, threads=4, **sp)
+    base = next(r for r in ranked_sim if r.config.n_dp >= 2 and r.config.n_pp >= 2)
+    rates = ps.rates_from_timing(model, base.config, base.timing)
+    meas = ps.rank_configs(model, k, scoring="measured", rates=rates, threads=4, **sp)
+    assert len(meas) == len(ref)
+    for r, (c, s) in zip(meas, ref):
+        assert r.score == pytest.approx(s, rel=1e-9)
+    # ties broken identically up to the floating-point noise of the rate round trip
+    assert sorted(_key(r.config) for r in meas) == sorted(c for c, _ in ref)
+    del at
+
+
+def test_measured_rates_round_trip():
+    model, _ = SPACES["gpt6.7b_8gpu"]
+    c0 = ps.ParallelConfig(n_dp=2, n_pp=4, n_loop=2, n_mb=8, dp_variant=V.DP_FS, schedule=S.BreadthFirst)
+    t0 = ps.TimingModel(t_fwd_stage=0.012, bwd_ratio=2.1, t_pp_transfer=4e-5, pp_latency=5e-6,
+                        t_dp_reduce_stage=0.02, t_dp_reconstruct_stage=0.006)
+    r = ps.rates_from_timing(model, c0, t0)
+    # a config with stages half as deep and twice the micro-batch size has the same stage cost
+    c1 = ps.ParallelConfig(n_dp=2, n_pp=4, n_loop=4, n_mb=4, s_mb=2, dp_variant=V.DP_FS, schedule=S.BreadthFirst)
+    got = ps.rank_configs(model, ps.cluster_preset("b200"), schedules=[4], dp_variants=[2], n_pp=[4], s_mb=[2],
+                          n_mb=[4], n_loop=[4], batch_sizes=[16], scoring="measured", rates=r)
+    assert len(got) == 1 and got[0].config == c1
+    t1 = got[0].timing
+    assert t1.t_fwd_stage == pytest.approx(t0.t_fwd_stage) and t1.bwd_ratio == t0.bwd_ratio
+    assert t1.t_pp_transfer == pytest.approx(2 * t0.t_pp_transfer)
+    assert t1.t_dp_reduce_stage == pytest.approx(t0.t_dp_reduce_stage / 2)
+    with pytest.raises(ps.SpecError):
+        ps.rank_configs(model, ps.cluster_preset("b200"), schedules=[4], dp_variants=[2], n_pp=[4], s_mb=[1],
+                        n_mb=[8], n_loop=[2], batch_sizes=[16], scoring="measured")
