@@ -315,7 +315,7 @@ __device__ __forceinline__ void named_bar_sync(int id, int n) {
 }
 
 // -------------------------------------------------------------------------------------
-// Backward: one CTA per (128-key block, head, sample), 14 warps (448 threads). Every MMA is
+// Backward: one CTA per (128-key block, head, sample), 18 warps (576 threads). Every MMA is
 // 128 x 128 x 16 (an N = 64 MMA takes as long as N = 128); the elementwise work of a query block
 // is split into two 64-query halves h = A, B so dV_A / dK_A start while half B is computed:
 //   warp 0      TMA: K, V once; Q_i (2-stage ring) and dO_i per query block (one buffer per
@@ -325,14 +325,16 @@ __device__ __forceinline__ void named_bar_sync(int id, int n) {
 //                 for h: dV += P_h^T dO_h   (A = P_h^T read from TMEM, packed over S_h^T)
 //                        (h = B: dQ^T = K^T dS^T -> TMEM[128,256), lanes = head dims)
 //                        dK += dS_h^T Q_h   (A = dS^T from shared memory)
-//   warps 2..5  dQ drain: thread = head dim d; per 64 queries, each warp stages its 32 dims
-//               as a SWIZZLE_128B f32 box and adds it to the f32 dQ accumulator with one
-//               TMA reduce-add (cp.reduce.async.bulk.tensor)
-//   warps 6..9 (half A), 10..13 (half B): elementwise, thread = key row (TMEM lane):
-//               P^T = exp2(S^T*scale_log2 - lse) packed bf16 into TMEM, dS^T = P^T (dP^T - delta)
+//   warps 2..9  dQ drain, two per TMEM lane quadrant: thread = head dim d; a warp takes its 32
+//               dims x 64 queries out of TMEM at once (releasing the columns), then stages them as
+//               two SWIZZLE_128B [32 queries][32 dims] f32 boxes, each added to the f32 dQ
+//               accumulator with one TMA reduce-add (cp.reduce.async.bulk.tensor)
+//   warps 10..17: elementwise, two per TMEM lane quadrant (thread = key row), one per 64-query
+//               half h of each block, 16 queries at a time: P^T = exp2(S^T*scale_log2 - lse)
+//               packed bf16 into TMEM over the half's own S^T columns, dS^T = P^T (dP^T - delta)
 //               bf16 into shared memory (packed f32x2 arithmetic; the causal selects only on
 //               diagonal / partial blocks); finally dK, dV.
-// Shared memory: K, V, Q[2], dO, dS^T, dQ staging (4 x [64][32] f32) = 7 x 32 KB + lse/delta
+// Shared memory: K, V, Q[2], dO, dS^T, dQ staging (8 x [32][32] f32) = 7 x 32 KB + lse/delta
 // (exactly fits 227 KB; the dynamic shared window is 1024-byte aligned, checked at run time).
 struct BwdSmem {
     static constexpr int kK = 0, kV = kTile, kQ = 2 * kTile, kO = 4 * kTile, kS = 5 * kTile, kDQ = 6 * kTile;
@@ -342,16 +344,16 @@ struct BwdSmem {
 };
 static_assert(BwdSmem::kBytes <= 232448, "attention backward shared memory");
 
-// Elementwise core of the backward for 32 queries of one key row: rs = S^T, rd = dP^T (TMEM
-// words), nl / nd = -lse / -delta of the 32 queries (shared memory, broadcast), [lo, hi) = the
+// Elementwise core of the backward for N queries of one key row: rs = S^T, rd = dP^T (TMEM
+// words), nl / nd = -lse / -delta of the N queries (shared memory, broadcast), [lo, hi) = the
 // visible query range (MASK only) -> P^T and dS^T as packed bf16 pairs.
-template <bool MASK>
-__device__ __forceinline__ void bwd_elementwise32(const uint32_t (&rs)[32], const uint32_t (&rd)[32], const float* nl,
-                                                  const float* nd, float scale_log2, int q_base, int lo, int hi,
-                                                  uint32_t (&pw)[16], uint32_t (&dw)[16]) {
+template <bool MASK, int N>
+__device__ __forceinline__ void bwd_elementwise(const uint32_t (&rs)[N], const uint32_t (&rd)[N], const float* nl,
+                                                const float* nd, float scale_log2, int q_base, int lo, int hi,
+                                                uint32_t (&pw)[N / 2], uint32_t (&dw)[N / 2]) {
     const uint64_t sc = ptx::pack2(scale_log2, scale_log2);
 #pragma unroll
-    for (int j = 0; j < 32; j += 2) {
+    for (int j = 0; j < N; j += 2) {
         const float2 nl2 = *reinterpret_cast<const float2*>(nl + j);
         const float2 nd2 = *reinterpret_cast<const float2*>(nd + j);
         const float2 t = ptx::unpack2(ptx::ffma2(ptx::pack2(__uint_as_float(rs[j]), __uint_as_float(rs[j + 1])), sc,
@@ -372,7 +374,7 @@ __device__ __forceinline__ void bwd_elementwise32(const uint32_t (&rs)[32], cons
     }
 }
 
-__global__ void __launch_bounds__(448, 1)
+__global__ void __launch_bounds__(576, 1)
     attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
                         const __grid_constant__ CUtensorMap tm_dq, const float* __restrict__ lse,
                         const float* __restrict__ delta, __nv_bfloat16* __restrict__ dqkv, int S, int H, float scale,
@@ -409,7 +411,7 @@ __global__ void __launch_bounds__(448, 1)
         ptx::mbar_init(kv_full, 1);
         ptx::mbar_init(s_full, 1);
         ptx::mbar_init(dq_full, 1);
-        ptx::mbar_init(dq_empty, 4);
+        ptx::mbar_init(dq_empty, 8);
         for (int k = 0; k < 2; ++k) {
             ptx::mbar_init(&q_full[k], 1);
             ptx::mbar_init(&q_empty[k], 1);
@@ -494,11 +496,12 @@ __global__ void __launch_bounds__(448, 1)
                         const int kk = h * 4 + k4;
                         ptx::umma_f16_ts(t_dv, t_s + h * 64 + k4 * 8, mnmajor_desc(so, kk), id_kn, (it | kk) != 0);
                     }
-                    ptx::umma_commit(&o_empty[h]);  // dO rows of this half: read by dP^T and dV only
+                    ptx::umma_commit(&o_empty[h]);  // dO rows of this half: read by dP^T and dV only (the
+                                                    // refill overlaps the rest of the block)
                     if (h == 1) {
                         // dQ^T [d][q] = sum_key K[key][d] dS[q][key]: A = K (MN-major over d),
                         // B = dS^T tile (MN-major over q), K-step = 16 keys; before dK_B so the
-                        // drain runs under it
+                        // drain overlaps dK_B and the next S^T
 #pragma unroll
                         for (int kk = 0; kk < BKV / 16; ++kk)
                             ptx::umma_f16(t_dp, mnmajor_desc(sk, kk), mnmajor_desc(sds, kk), id_nn, kk != 0);
@@ -515,57 +518,52 @@ __global__ void __launch_bounds__(448, 1)
                 ATRACE(1, it, 11);
             }
         }
-    } else if (warp < 6) {
-        // ===== dQ drain: thread = head dim d (TMEM lane); warp q4 owns dims q4*32..q4*32+31 =====
-        const int q4 = warp & 3;
+    } else if (warp < 10) {
+        // ===== dQ drain: thread = head dim d (TMEM lane); warp (q4, dh) owns dims q4*32..+31 of
+        // queries 64dh..64dh+63 and stages them as two [32 queries][32 dims] f32 boxes =====
+        const int q4 = warp & 3, dh = (warp - 2) >> 2;
         const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
-        uint8_t* box_ptr = sm + BwdSmem::kDQ + q4 * 8192;  // [64 queries][32 dims] f32, SWIZZLE_128B
+        uint8_t* box_ptr = sm + BwdSmem::kDQ + (warp - 2) * 4096;  // [32 queries][32 dims] f32, SWIZZLE_128B
         const uint32_t box = ptx::smem_u32(box_ptr);
         const uint32_t col = static_cast<uint32_t>(lane & 3) * 4;
         for (int it = 0; it < n_it; ++it) {
-            const int q0 = (i0 + it) * BQ;
+            const int q0 = (i0 + it) * BQ + dh * 64;
             if (warp == 2 && lane == 0) ATRACE(2, it, 0);
             ptx::mbar_wait(dq_full, it & 1);
             if (warp == 2 && lane == 0) ATRACE(2, it, 1);
             ptx::tc_fence_after();
-#pragma unroll 1
-            for (int h = 0; h < 2; ++h) {  // 64 queries per staged box
-                uint32_t v[2][32];
-                ptx::tmem_ld_32x32b_x32(t_dp + lane_off + h * 64, v[0]);
-                ptx::tmem_ld_32x32b_x32(t_dp + lane_off + h * 64 + 32, v[1]);
-                ptx::tmem_ld_wait();
-                if (h == 1) {  // all of dQ^T has left TMEM: the next dP^T may overwrite it
-                    ptx::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(dq_empty);
-                }
+            uint32_t v[2][32];
+            ptx::tmem_ld_32x32b_x32(t_dp + lane_off + dh * 64, v[0]);
+            ptx::tmem_ld_32x32b_x32(t_dp + lane_off + dh * 64 + 32, v[1]);
+            ptx::tmem_ld_wait();
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(dq_empty);  // this warp's share of dQ^T is in registers
+#pragma unroll
+            for (int c2 = 0; c2 < 2; ++c2) {
                 if (lane == 0) ptx::bulk_wait_read<0>();  // the previous reduce has read the box
                 __syncwarp();
 #pragma unroll
-                for (int c2 = 0; c2 < 2; ++c2)
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const int ql = c2 * 32 + j;  // row of the box
-                        ptx::st_shared_f32(box + ql * 128 + ((((lane >> 2) ^ ql) & 7) << 4) + col,
-                                           __uint_as_float(v[c2][j]) * scale);
-                    }
+                for (int j = 0; j < 32; ++j)  // row j of the box = query q0 + 32 c2 + j
+                    ptx::st_shared_f32(box + j * 128 + ((((lane >> 2) ^ j) & 7) << 4) + col,
+                                       __uint_as_float(v[c2][j]) * scale);
                 ptx::fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
-                    ptx::tma_reduce_add_2d(&tm_dq, box_ptr, head * D + q4 * 32, row0 + q0 + h * 64);
+                    ptx::tma_reduce_add_2d(&tm_dq, box_ptr, head * D + q4 * 32, row0 + q0 + c2 * 32);
                     ptx::bulk_commit();
-                    if (warp == 2) ATRACE(2, it, 2 + h);
+                    if (warp == 2) ATRACE(2, it, 2 + c2);
                 }
             }
         }
         if (lane == 0) ptx::bulk_wait<0>();
     } else {
-        // ===== elementwise: thread = key row r, query half h of every 128-query block =====
-        const int q4 = warp & 3, h = (warp - 6) >> 2;
+        // ===== elementwise: thread = key row r, query half h (64 queries) of every block =====
+        const int q4 = warp & 3, h = (warp - 10) >> 2;
         const int r = q4 * 32 + lane;
         const int key = kb * BKV + r;
         const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
-        const int e = threadIdx.x - (6 + 4 * h) * 32;  // 0..127 within the half: lse (< 64) or delta
+        const int e = threadIdx.x - (10 + 4 * h) * 32;  // 0..127 within the half: lse (< 64) or delta
         const uint32_t sds_base = ptx::smem_u32(sm + BwdSmem::kS);
         const int64_t stat_base = (static_cast<int64_t>(b) * H + head) * S;
         const float* stat = e < 64 ? lse : delta;
@@ -585,12 +583,12 @@ __global__ void __launch_bounds__(448, 1)
                 const int q = qh + BQ + eq;
                 nxt = q < S ? stat[stat_base + q] : 0.f;
             }
-            if (lane == 0 && (warp == 6 || warp == 10)) ATRACE(3 + h, it, 0);
+            if (lane == 0 && (warp == 10 || warp == 14)) ATRACE(3 + h, it, 0);
             named_bar_sync(1 + h, 128);
-            if (lane == 0 && (warp == 6 || warp == 10)) ATRACE(3 + h, it, 1);
+            if (lane == 0 && (warp == 10 || warp == 14)) ATRACE(3 + h, it, 1);
             // s_full(i) also orders after every MMA of block i-1 (the readers of dS^T)
             ptx::mbar_wait(s_full, it & 1);
-            if (lane == 0 && (warp == 6 || warp == 10)) ATRACE(3 + h, it, 2);
+            if (lane == 0 && (warp == 10 || warp == 14)) ATRACE(3 + h, it, 2);
             ptx::tc_fence_after();
             const bool mask = (i == i0) || (i * BQ + BQ > S) || (kb * BKV + BKV > S);
             // valid queries of this thread's key row: key <= q < S, as a [lo, hi) range of the
@@ -599,23 +597,23 @@ __global__ void __launch_bounds__(448, 1)
             const float* Lp = reinterpret_cast<const float*>(sm + BwdSmem::kStat + h * 1024 + (it & 1) * 512);
             const float* Dp = Lp + 64;
 #pragma unroll 1
-            for (int cc = 0; cc < 2; ++cc) {
-                uint32_t rs[32], rd[32];
-                ptx::tmem_ld_32x32b_x32(t_s + lane_off + h * 64 + cc * 32, rs);
-                ptx::tmem_ld_32x32b_x32(t_dp + lane_off + h * 64 + cc * 32, rd);
+            for (int sub = 0; sub < 4; ++sub) {
+                const int qc = sub * 16;  // first query of the 16 within the half
+                uint32_t rs[16], rd[16];
+                ptx::tmem_ld_32x32b_x16(t_s + lane_off + h * 64 + qc, rs);
+                ptx::tmem_ld_32x32b_x16(t_dp + lane_off + h * 64 + qc, rd);
                 ptx::tmem_ld_wait();
-                uint32_t pw[16], dw[16];
+                uint32_t pw[8], dw[8];
                 if (mask)  // warp-uniform: only diagonal / partial blocks pay for the selects
-                    bwd_elementwise32<true>(rs, rd, Lp + cc * 32, Dp + cc * 32, scale_log2, cc * 32, lo, hi, pw, dw);
+                    bwd_elementwise<true, 16>(rs, rd, Lp + qc, Dp + qc, scale_log2, qc, lo, hi, pw, dw);
                 else
-                    bwd_elementwise32<false>(rs, rd, Lp + cc * 32, Dp + cc * 32, scale_log2, cc * 32, lo, hi, pw, dw);
-                // P^T in place of S^T: the half's 64 queries pack into columns 64h + [0, 32), all of
-                // which this warp has already read
-                ptx::tmem_st_32x32b_x16(t_s + lane_off + h * 64 + cc * 16, pw);
-                // dS^T row r of the [2 q-halves][128 keys][128 B] SW128 tile
+                    bwd_elementwise<false, 16>(rs, rd, Lp + qc, Dp + qc, scale_log2, qc, lo, hi, pw, dw);
+                // P^T packed over this half's S^T columns 64h + [8 sub, 8 sub + 8): all read already
+                ptx::tmem_st_32x32b_x8(t_s + lane_off + h * 64 + sub * 8, pw);
+                // dS^T row r of the [2 q-halves][128 keys][128 B] SW128 tile: 16-byte chunks qc / 8 + {0, 1}
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int ch = cc * 4 + u;
+                for (int u = 0; u < 2; ++u) {
+                    const int ch = qc / 8 + u;
                     const uint32_t off = h * (kTile / 2) + r * 128 + ((ch ^ (r & 7)) << 4);
                     ptx::st_shared_v4(sds_base + off, dw[4 * u], dw[4 * u + 1], dw[4 * u + 2], dw[4 * u + 3]);
                 }
@@ -625,7 +623,7 @@ __global__ void __launch_bounds__(448, 1)
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&p_full[h]);
-            if (lane == 0 && (warp == 6 || warp == 10)) ATRACE(3 + h, it, 3);
+            if (lane == 0 && (warp == 10 || warp == 14)) ATRACE(3 + h, it, 3);
         }
         // dK (scaled) and dV: every MMA has completed once the last block's q_empty commit fires
         // (its previous phase, block n-3, completed before s_full of block n-1)
@@ -637,15 +635,15 @@ __global__ void __launch_bounds__(448, 1)
         __nv_bfloat16* dkr = dqkv + static_cast<int64_t>(row0 + key) * 3 * HD + HD + head * D;
         __nv_bfloat16* dvr = dqkv + static_cast<int64_t>(row0 + key) * 3 * HD + 2 * HD + head * D;
 #pragma unroll 1
-        for (int cc = 0; cc < 2; ++cc) {
-            const int c0 = h * 64 + cc * 32;
-            uint32_t rk[32], rv[32];
-            ptx::tmem_ld_32x32b_x32(t_dk + lane_off + c0, rk);
-            ptx::tmem_ld_32x32b_x32(t_dv + lane_off + c0, rv);
+        for (int sub = 0; sub < 4; ++sub) {
+            const int c0 = h * 64 + sub * 16;
+            uint32_t rk[16], rv[16];
+            ptx::tmem_ld_32x32b_x16(t_dk + lane_off + c0, rk);
+            ptx::tmem_ld_32x32b_x16(t_dv + lane_off + c0, rv);
             ptx::tmem_ld_wait();
             if (key >= S) continue;
 #pragma unroll
-            for (int j = 0; j < 32; j += 8) {
+            for (int j = 0; j < 16; j += 8) {
                 uint4 ok, ov;
                 uint32_t* wk = reinterpret_cast<uint32_t*>(&ok);
                 uint32_t* wv = reinterpret_cast<uint32_t*>(&ov);
@@ -684,8 +682,8 @@ void attention_bwd_tc(const void* qkv, const void* dout, const float* lse, const
     dim3 grid(heads, (seq + BKV - 1) / BKV, batch);
     if (heads > 1 && seq > BKV) count_variant(KV_ATTN_BWD_MULTI);
     const float scale = 1.f / sqrtf(static_cast<float>(head_dim));
-    const CUtensorMap tdq = make_tma_2d(dq_acc, HD, T, HD, 64, true);
-    attn_bwd_tc_kernel<<<grid, 448, BwdSmem::kBytes, st>>>(tq, to64, tdq, lse, delta,
+    const CUtensorMap tdq = make_tma_2d(dq_acc, HD, T, HD, 32, true);  // [32 queries][32 dims] boxes
+    attn_bwd_tc_kernel<<<grid, 576, BwdSmem::kBytes, st>>>(tq, to64, tdq, lse, delta,
                                                              static_cast<__nv_bfloat16*>(dqkv), seq, heads, scale,
                                                              scale * kLog2e);
 }
