@@ -340,6 +340,7 @@ def main():
     measured_timing = None
     sim_bubble = None
     replay_bubble = None
+    task_replay_bubble = None
     peak_layers = None
     _progress('timeline')
     if not args.no_timeline:
@@ -359,6 +360,10 @@ def main():
         # the same graph simulated with the measured per-kind task durations
         mtm = ps.measured_timing_model(ex.graph, tl)
         replay_bubble = ps.bubble_fraction(ps.simulate(ex.graph, mtm))
+        # the same graph replayed with every task's own measured duration: the bubble a zero-overhead
+        # executor would show with these task times (measured - this = executor overhead)
+        task_replay_bubble = ps.bubble_fraction(
+            ps.simulate_durations(ex.graph, [e.end - e.start for e in tl.events]))
         mspec = ps.ModelSpec(n_layers=cfg.n_layers, s_hidden=cfg.s_hidden, n_heads=cfg.n_heads, s_seq=cfg.s_seq,
                              s_voc=cfg.s_voc)
         measured_timing = {"timing_model": dataclasses.asdict(mtm),
@@ -438,6 +443,7 @@ def main():
                     "model_flops_per_token": fpt, "eq11_tflops_per_gpu": eq11 / 1e12},
             "bubble_fraction": {"measured": bubble, "eq7": sim_bubble,
                                 "simulated_with_measured_timing": replay_bubble,
+                                "simulated_with_measured_task_durations": task_replay_bubble,
                                 "peak_inflight_layers_measured": peak_layers},
             "loss": loss_val,
             "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clocks, "roofline": roofline,

@@ -142,6 +142,9 @@ void bfpp_graph_destroy(bfpp_graph* g);
 
 /* replaces simulate (simulate.hpp:28, simulate.cpp:41-158) */
 int bfpp_simulate(const bfpp_graph* g, const bfpp_timing_model* t, bfpp_timeline** out);
+/* the same list scheduler with one duration per task id (durations[n_tasks]): replays a measured
+ * timeline's own task times with zero executor overhead (new; no reference counterpart) */
+int bfpp_simulate_durations(const bfpp_graph* g, const double* durations, bfpp_timeline** out);
 int64_t bfpp_timeline_n_events(const bfpp_timeline* tl);
 int64_t bfpp_timeline_n_devices(const bfpp_timeline* tl);
 double bfpp_timeline_makespan(const bfpp_timeline* tl);

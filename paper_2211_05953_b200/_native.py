@@ -82,6 +82,7 @@ _PROTOS = {
     "bfpp_graph_programs": (C.c_int, [_P, _I32P, _I32P]),
     "bfpp_graph_destroy": (None, [_P]),
     "bfpp_simulate": (C.c_int, [_P, C.POINTER(TimingModelC), C.POINTER(_P)]),
+    "bfpp_simulate_durations": (C.c_int, [_P, _DP, C.POINTER(_P)]),
     "bfpp_timeline_n_events": (C.c_int64, [_P]),
     "bfpp_timeline_n_devices": (C.c_int64, [_P]),
     "bfpp_timeline_makespan": (C.c_double, [_P]),

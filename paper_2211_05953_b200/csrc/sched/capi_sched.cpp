@@ -184,6 +184,14 @@ int bfpp_graph_programs(const bfpp_graph* g, int32_t* offsets, int32_t* ids) {
 
 void bfpp_graph_destroy(bfpp_graph* g) { delete g; }
 
+int bfpp_simulate_durations(const bfpp_graph* g, const double* durations, bfpp_timeline** out) {
+    *out = nullptr;
+    return guarded([&] {
+        std::vector<double> d(durations, durations + g->g.tasks.size());
+        *out = new bfpp_timeline{simulate_durations(g->g, d)};
+    });
+}
+
 int bfpp_simulate(const bfpp_graph* g, const bfpp_timing_model* t, bfpp_timeline** out) {
     *out = nullptr;
     return guarded([&] {

@@ -108,6 +108,7 @@ StagePlacement place_stages(const ModelSpec& m, const ParallelConfig& c);
 TaskGraph build_tasks(const ModelSpec& m, const ParallelConfig& c, const StagePlacement& pl);
 TaskGraph build_accumulation_tasks(const ModelSpec& m, DpVariant v, AccumulationOrder o, i64 n_mb);
 Timeline simulate(const TaskGraph& g, const TimingModel& t);
+Timeline simulate_durations(const TaskGraph& g, const std::vector<double>& durations);
 double bubble_fraction(const Timeline& tl);
 std::vector<i64> peak_inflight(const Timeline& tl, const TaskGraph& g, i64 layers_per_stage);
 // A measured timeline: events from per-task intervals, lane busy time summed

@@ -8,6 +8,7 @@
 // (bubble_fraction, peak_inflight; ref simulate.cpp:160-191) are applied to the
 // executor's *measured* timelines.
 #include <algorithm>
+#include <cmath>
 #include <functional>
 #include <queue>
 #include <set>
@@ -28,8 +29,9 @@ static double duration(const Task& t, const TimingModel& tm) {
     return 0.0;
 }
 
-Timeline simulate(const TaskGraph& g, const TimingModel& tm) {
-    tm.validate();
+namespace {
+template <class Dur>
+Timeline simulate_impl(const TaskGraph& g, Dur&& duration_of) {
     const size_t n = g.tasks.size();
     const size_t nd = static_cast<size_t>(g.n_devices);
     Timeline tl;
@@ -63,7 +65,7 @@ Timeline simulate(const TaskGraph& g, const TimingModel& tm) {
         return true;
     };
     auto launch = [&](const Task& t, double now) {
-        const double dur = duration(t, tm);
+        const double dur = duration_of(t);
         tl.events[static_cast<size_t>(t.id)] = {t.id, now, now + dur};
         free_at[lane_slot(t.device, t.lane)] = now + dur;
         tl.lane_busy[static_cast<size_t>(t.device)][static_cast<int>(t.lane)] += dur;
@@ -122,6 +124,21 @@ Timeline simulate(const TaskGraph& g, const TimingModel& tm) {
         tl.makespan = std::max(tl.makespan, now);
     }
     return tl;
+}
+}  // namespace
+
+Timeline simulate(const TaskGraph& g, const TimingModel& tm) {
+    tm.validate();
+    return simulate_impl(g, [&](const Task& t) { return duration(t, tm); });
+}
+
+// The same list scheduler with one duration per task (e.g. every task's measured duration): the
+// makespan an executor with zero overhead would reach with those task times.
+Timeline simulate_durations(const TaskGraph& g, const std::vector<double>& dur) {
+    if (dur.size() != g.tasks.size()) throw SpecError("simulate_durations: one duration per task expected");
+    for (double d : dur)
+        if (!(d >= 0.0) || !std::isfinite(d)) throw SpecError("simulate_durations: durations must be finite and >= 0");
+    return simulate_impl(g, [&](const Task& t) { return dur[static_cast<size_t>(t.id)]; });
 }
 
 Timeline timeline_from_intervals(const TaskGraph& g, const double* start, const double* end) {

@@ -338,6 +338,17 @@ def simulate(graph: TaskGraph, timing: TimingModel) -> Timeline:
     return Timeline(h.value)
 
 
+def simulate_durations(graph: TaskGraph, durations) -> Timeline:
+    """simulate() with one duration per task (e.g. a measured timeline's own task times)."""
+    durations = list(durations)
+    if len(durations) != len(graph.tasks):
+        raise SpecError("error[invalid-spec]: simulate_durations: one duration per task expected")
+    d = (C.c_double * len(graph.tasks))(*[float(x) for x in durations])
+    h = C.c_void_p()
+    _check(N.lib().bfpp_simulate_durations(graph.handle, d, C.byref(h)))
+    return Timeline(h.value)
+
+
 def simulate_config(model: ModelSpec, config: ParallelConfig, timing: TimingModel) -> Timeline:
     return simulate(build_tasks(model, config, place_stages(model, config)), timing)
 

@@ -102,3 +102,24 @@ def test_measured_rates_round_trip():
     with pytest.raises(ps.SpecError):
         ps.rank_configs(model, ps.cluster_preset("b200"), schedules=[4], dp_variants=[2], n_pp=[4], s_mb=[1],
                         n_mb=[8], n_loop=[2], batch_sizes=[16], scoring="measured")
+
+
+def test_simulate_durations_replays_simulate():
+    """simulate_durations with each task's simulated duration reproduces simulate() exactly, and a
+    uniformly slower task set stretches the makespan proportionally."""
+    m = ps.ModelSpec(n_layers=16, s_hidden=256, n_heads=2, s_seq=128, s_voc=1000)
+    for sched, dv in ((S.BreadthFirst, V.DP_FS), (S.DepthFirst, V.DP0), (S.OneFOneB, V.DP_PS)):
+        loops = 2 if sched in (S.BreadthFirst, S.DepthFirst) else 1
+        c = ps.ParallelConfig(n_dp=2, n_pp=4, n_loop=loops, n_mb=8, dp_variant=dv, schedule=sched)
+        g = ps.build_tasks(m, c)
+        tm = ps.TimingModel(t_fwd_stage=1.0, bwd_ratio=2.0, t_pp_transfer=0.125, t_dp_reduce_stage=0.5,
+                            t_dp_reconstruct_stage=0.25)
+        a = ps.simulate(g, tm)
+        dur = [e.end - e.start for e in a.events]
+        b = ps.simulate_durations(g, dur)
+        assert [(e.start, e.end) for e in a.events] == [(e.start, e.end) for e in b.events]
+        assert ps.simulate_durations(g, [2 * x for x in dur]).makespan == 2 * a.makespan
+    with pytest.raises(ps.SpecError):
+        ps.simulate_durations(g, dur[:-1])
+    with pytest.raises(ps.SpecError):
+        ps.simulate_durations(g, [-1.0] + dur[1:])
