@@ -23,6 +23,7 @@
 #include <map>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 
 #include "gemm.hpp"
 #include "sm100_ptx.cuh"
@@ -44,9 +45,30 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
+namespace {
+CUtensorMap encode_tma_2d(const void* ptr, int64_t inner, int64_t rows, int64_t ld, int box_rows, bool f32);
+}  // namespace
+
 // 2-D tensor map over a row-major [rows][ld] matrix with `inner` valid columns;
 // box = {128 B of inner, box_rows}, SWIZZLE_128B, OOB loads -> zero, OOB stores dropped.
+// Cached by (address, shape, box): the executor's buffers are persistent, so every launch of a step
+// after the first reuses its descriptors instead of encoding ~3 per GEMM launch on the host.
 CUtensorMap make_tma_2d(const void* ptr, int64_t inner, int64_t rows, int64_t ld, int box_rows, bool f32) {
+    using Key = std::tuple<const void*, int64_t, int64_t, int64_t, int, bool>;
+    static std::mutex mu;
+    static std::map<Key, CUtensorMap> cache;
+    const Key k{ptr, inner, rows, ld, box_rows, f32};
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(k);
+    if (it != cache.end()) return it->second;
+    if (cache.size() >= 8192) cache.clear();  // bounded (tests allocate many short-lived buffers)
+    const CUtensorMap m = encode_tma_2d(ptr, inner, rows, ld, box_rows, f32);
+    cache.emplace(k, m);
+    return m;
+}
+
+namespace {
+CUtensorMap encode_tma_2d(const void* ptr, int64_t inner, int64_t rows, int64_t ld, int box_rows, bool f32) {
     CUtensorMap m;
     const int esz = f32 ? 4 : 2;
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(rows)};
@@ -60,6 +82,7 @@ CUtensorMap make_tma_2d(const void* ptr, int64_t inner, int64_t rows, int64_t ld
     if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
     return m;
 }
+}  // namespace
 
 
 namespace {

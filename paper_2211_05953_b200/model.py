@@ -29,6 +29,8 @@ PRESETS = {
     "gpt-13b-l40": (40, 5120, 40, 2048, 50304),
     "gpt-13b-l32": (32, 5760, 45, 2048, 50304),
     "52b": (64, 8192, 64, 1024, 50304),
+    # the 52B layer shape at a depth 4 B200s can hold (BASELINE configs[4] needs 8: PP4 x DP2)
+    "52b-l16": (16, 8192, 64, 1024, 50304),
 }
 
 
