@@ -1178,8 +1178,8 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
                 CK(cudaMemsetAsync(G_ + L.wte, 0, static_cast<size_t>(V * h) * 4, st));
                 CK(cudaMemsetAsync(G_ + L.wpe, 0, static_cast<size_t>(m_.s_seq * h) * 4, st));
             }
-            if (L.first)
-                K(K_MISC, 2 * Th2, 1, st, [&] {
+            if (L.first)  // iota, radix sort (1-2 launches), per-token and per-position sums
+                K(K_MISC, 2 * Th2, 4, st, [&] {
                     embed_bwd(I.inputs + t.micro_batch * T, g, G_ + L.wte, G_ + L.wpe, static_cast<int>(T), S,
                               static_cast<int>(h), st);
                 });

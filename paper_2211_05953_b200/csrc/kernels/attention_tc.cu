@@ -287,6 +287,238 @@ __global__ void __launch_bounds__(192, 1)
     if (warp == 1) ptx::tmem_dealloc<512>(tmem);
 }
 
+// -------------------------------------------------------------------------------------
+// Forward, two query tiles per CTA (adjacent 128-query blocks 2p, 2p+1 of one head), sharing every
+// K / V tile; 10 warps:
+//   warp 0      TMA: Q0, Q1 once, K_j and V_j through 2-stage rings
+//   warp 1      MMA issuer: S_t,0 for both tiles, then per key tile j and tile t:
+//                 O_t += P_t,j V_j (A = P read from TMEM over S_t), then S_t,j+1 = Q_t K_j+1^T
+//   warps 2..5  softmax of tile 0, warps 6..9 softmax of tile 1 (thread = query row): while one
+//               tile's softmax runs, the tensor pipe works on the other tile (ping-pong)
+// TMEM: O0 [0,128), O1 [128,256), S0/P0 [256,384), S1/P1 [384,512). S_t,j+1 is issued after PV_t,j,
+// so when softmax t sees S_t,j+1 the previous PV has completed and O_t may be rescaled at once.
+struct Fwd2Smem {
+    static constexpr int kQ = 0;               // [2 tiles]
+    static constexpr int kK = kQ + 2 * kTile;  // 2 stages
+    static constexpr int kV = kK + 2 * kTile;  // 2 stages
+    static constexpr int kBar = kV + 2 * kTile;
+    static constexpr int kBytes = kBar + 256 + 1024;
+};
+
+__global__ void __launch_bounds__(320, 1)
+    attn_fwd_tc2_kernel(const __grid_constant__ CUtensorMap tm_qkv, __nv_bfloat16* __restrict__ o,
+                        float* __restrict__ lse, int S, int H, float scale_log2) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + Fwd2Smem::kBar);
+    uint64_t* q_full = bar + 0;
+    uint64_t* k_full = bar + 1;   // [2]
+    uint64_t* k_empty = bar + 3;  // [2]
+    uint64_t* v_full = bar + 5;   // [2]
+    uint64_t* v_empty = bar + 7;  // [2]
+    uint64_t* s_full = bar + 9;   // [tile]
+    uint64_t* p_full = bar + 11;  // [tile]
+    uint64_t* o_done = bar + 13;  // [tile] PV_t,j complete
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+
+    // grid (H, query-block pairs, B), longest pairs first
+    const int n_qb = (S + BQ - 1) / BQ;
+    const int n_pairs = (n_qb + 1) / 2;
+    const int pr = n_pairs - 1 - blockIdx.y;
+    const int head = blockIdx.x, b = blockIdx.z;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int HD = H * D;
+    const int row0 = b * S;
+    const int n_tq = 2 * pr + 1 < n_qb ? 2 : 1;  // query tiles of this CTA
+    auto tiles_of = [&](int t) { return (min((2 * pr + t + 1) * BQ, S) + BKV - 1) / BKV; };
+    const int n_max = tiles_of(n_tq - 1);
+
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch(&tm_qkv);
+        ptx::mbar_init(q_full, 1);
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(&k_full[i], 1);
+            ptx::mbar_init(&k_empty[i], 1);
+            ptx::mbar_init(&v_full[i], 1);
+            ptx::mbar_init(&v_empty[i], 1);
+            ptx::mbar_init(&s_full[i], 1);
+            ptx::mbar_init(&p_full[i], 4);
+            ptx::mbar_init(&o_done[i], 1);
+        }
+        ptx::fence_barrier_init();
+    }
+    if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            const int qcol = head * D, kcol = HD + head * D, vcol = 2 * HD + head * D;
+            ptx::mbar_expect_tx(q_full, n_tq * kTile);
+            for (int t = 0; t < n_tq; ++t)
+                for (int h2 = 0; h2 < 2; ++h2)
+                    ptx::tma_load_2d(sm + Fwd2Smem::kQ + t * kTile + h2 * (kTile / 2), &tm_qkv, q_full,
+                                     qcol + 64 * h2, row0 + (2 * pr + t) * BQ);
+            for (int j = 0; j < n_max; ++j) {
+                const int st = j & 1;
+                const uint32_t ph = (j >> 1) & 1;
+                ptx::mbar_wait(&k_empty[st], ph ^ 1);
+                ptx::mbar_expect_tx(&k_full[st], kTile);
+                for (int h2 = 0; h2 < 2; ++h2)
+                    ptx::tma_load_2d(sm + Fwd2Smem::kK + st * kTile + h2 * (kTile / 2), &tm_qkv, &k_full[st],
+                                     kcol + 64 * h2, row0 + j * BKV);
+                ptx::mbar_wait(&v_empty[st], ph ^ 1);
+                ptx::mbar_expect_tx(&v_full[st], kTile);
+                for (int h2 = 0; h2 < 2; ++h2)
+                    ptx::tma_load_2d(sm + Fwd2Smem::kV + st * kTile + h2 * (kTile / 2), &tm_qkv, &v_full[st],
+                                     vcol + 64 * h2, row0 + j * BKV);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(128, 128, 0, 0);   // Q K^T: both K-major
+            constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(128, 128, 0, 1);  // P V: V is MN-major
+            ptx::mbar_wait(q_full, 0);
+            auto issue_s = [&](int t, int j) {
+                const int st = j & 1;
+                ptx::mbar_wait(&k_full[st], (j >> 1) & 1);
+                ptx::tc_fence_after();
+                const uint32_t sq = ptx::smem_u32(sm + Fwd2Smem::kQ + t * kTile);
+                const uint32_t sk = ptx::smem_u32(sm + Fwd2Smem::kK + st * kTile);
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk)
+                    ptx::umma_f16(tmem + 256 + t * 128, kmajor_desc(sq, kk), kmajor_desc(sk, kk), idesc_s, kk != 0);
+                ptx::umma_commit(&s_full[t]);
+            };
+            for (int t = 0; t < n_tq; ++t) issue_s(t, 0);
+            for (int j = 0; j < n_max; ++j) {
+                const int st = j & 1;
+                for (int t = 0; t < n_tq; ++t) {
+                    const int nt = tiles_of(t);
+                    if (j >= nt) continue;
+                    ptx::mbar_wait(&p_full[t], j & 1);
+                    ptx::mbar_wait(&v_full[st], (j >> 1) & 1);
+                    ptx::tc_fence_after();
+                    const uint32_t sv = ptx::smem_u32(sm + Fwd2Smem::kV + st * kTile);
+#pragma unroll
+                    for (int kk = 0; kk < BKV / 16; ++kk)  // P: 16 keys = 8 packed columns per K-step
+                        ptx::umma_f16_ts(tmem + t * 128, tmem + 256 + t * 128 + kk * 8, mnmajor_desc(sv, kk),
+                                         idesc_pv, (j | kk) != 0);
+                    ptx::umma_commit(&o_done[t]);
+                    if (j + 1 < nt) issue_s(t, j + 1);
+                }
+                ptx::umma_commit(&k_empty[st]);
+                ptx::umma_commit(&v_empty[st]);
+            }
+        }
+    } else {
+        // ===== softmax warps: tile t = (warp - 2) / 4, thread = query row =====
+        const int t = (warp - 2) >> 2;
+        const int q4 = warp & 3;
+        const int r = q4 * 32 + lane;
+        const int qb = 2 * pr + t;
+        const int qrow = qb * BQ + r;
+        const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
+        const uint32_t t_o = tmem + t * 128, t_s = tmem + 256 + t * 128;
+        if (t < n_tq) {
+            const int n_tiles = tiles_of(t);
+            float m_used = -INFINITY, l = 0.f;
+            for (int j = 0; j < n_tiles; ++j) {
+                ptx::mbar_wait(&s_full[t], j & 1);
+                ptx::tc_fence_after();
+                float s[128];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t rr[32];
+                    ptx::tmem_ld_32x32b_x32(t_s + lane_off + c * 32, rr);
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(rr[i]);
+                }
+                const int k0 = j * BKV;
+                const bool diag = k0 + BKV - 1 > qb * BQ || k0 + BKV > S;
+                const int lim = diag ? min(qrow + 1, S) - k0 : BKV;
+                float mx = -INFINITY;
+#pragma unroll
+                for (int i = 0; i < 128; ++i) {
+                    const float v = i < lim ? s[i] * scale_log2 : -INFINITY;
+                    s[i] = v;
+                    mx = fmaxf(mx, v);
+                }
+                // warp-uniform rescale (tcgen05.ld/st are .sync.aligned); O_t is stable: S_t,j was
+                // issued after PV_t,j-1 and s_full fired once every earlier MMA had completed
+                const bool mine = mx > m_used + kRescaleThreshold;
+                if (__any_sync(0xffffffffu, mine)) {
+                    const float alpha = mine ? (m_used == -INFINITY ? 0.f : ptx::ex2_fast(m_used - mx)) : 1.f;
+                    if (mine) m_used = mx;
+                    l *= alpha;
+                    if (j > 0) {
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            uint32_t rr[32];
+                            ptx::tmem_ld_32x32b_x32(t_o + lane_off + c * 32, rr);
+                            ptx::tmem_ld_wait();
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) rr[i] = __float_as_uint(__uint_as_float(rr[i]) * alpha);
+                            ptx::tmem_st_32x32b_x32(t_o + lane_off + c * 32, rr);
+                        }
+                    }
+                }
+                float sum = 0.f;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t w[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const float p0 = ptx::ex2_fast(s[c * 32 + 2 * i] - m_used);
+                        const float p1 = ptx::ex2_fast(s[c * 32 + 2 * i + 1] - m_used);
+                        sum += p0 + p1;
+                        __nv_bfloat162 hb = __floats2bfloat162_rn(p0, p1);
+                        w[i] = *reinterpret_cast<uint32_t*>(&hb);
+                    }
+                    ptx::tmem_st_32x32b_x16(t_s + lane_off + c * 16, w);
+                }
+                l += sum;
+                ptx::tmem_st_wait();
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&p_full[t]);
+            }
+            // epilogue: passing s_full_t(n-1) proved PV_t(n-2) done; wait for PV_t(n-1)
+            ptx::mbar_wait(&o_done[t], (n_tiles - 1) & 1);
+            ptx::tc_fence_after();
+            const float inv = 1.f / l;
+            __nv_bfloat16* orow = o + static_cast<int64_t>(row0 + qrow) * HD + head * D;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                uint32_t rr[32];
+                ptx::tmem_ld_32x32b_x32(t_o + lane_off + c * 32, rr);
+                ptx::tmem_ld_wait();
+                if (qrow < S) {
+#pragma unroll
+                    for (int i = 0; i < 32; i += 8) {
+                        uint4 pk;
+                        uint32_t* w = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            __nv_bfloat162 hb = __floats2bfloat162_rn(__uint_as_float(rr[i + 2 * u]) * inv,
+                                                                      __uint_as_float(rr[i + 2 * u + 1]) * inv);
+                            w[u] = *reinterpret_cast<uint32_t*>(&hb);
+                        }
+                        *reinterpret_cast<uint4*>(orow + c * 32 + i) = pk;
+                    }
+                }
+            }
+            if (qrow < S) lse[(static_cast<int64_t>(b) * H + head) * S + qrow] = m_used + __log2f(l);
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) ptx::tmem_dealloc<512>(tmem);
+}
+
 }  // namespace
 
 void attention_fwd_tc(const void* qkv, void* o, float* lse, int batch, int seq, int heads, int head_dim,
@@ -302,8 +534,21 @@ void attention_fwd_tc(const void* qkv, void* o, float* lse, int batch, int seq, 
     dim3 grid(heads, (seq + BQ - 1) / BQ, batch);
     if (heads > 1 && seq > BQ) count_variant(KV_ATTN_FWD_MULTI);
     const float scale_log2 = kLog2e / sqrtf(static_cast<float>(head_dim));
-    attn_fwd_tc_kernel<<<grid, 192, FwdSmem::kBytes, st>>>(tm, static_cast<__nv_bfloat16*>(o), lse, seq, heads,
-                                                           scale_log2);
+    static const bool one_tile = getenv("BFPP_ATTN_FWD") && atoi(getenv("BFPP_ATTN_FWD")) == 1;
+    if (one_tile) {
+        attn_fwd_tc_kernel<<<grid, 192, FwdSmem::kBytes, st>>>(tm, static_cast<__nv_bfloat16*>(o), lse, seq, heads,
+                                                               scale_log2);
+        return;
+    }
+    static bool cfg2 = false;
+    if (!cfg2) {
+        cudaFuncSetAttribute(attn_fwd_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2Smem::kBytes);
+        cfg2 = true;
+    }
+    const int n_qb = (seq + BQ - 1) / BQ;
+    dim3 grid2(heads, (n_qb + 1) / 2, batch);
+    attn_fwd_tc2_kernel<<<grid2, 320, Fwd2Smem::kBytes, st>>>(tm, static_cast<__nv_bfloat16*>(o), lse, seq, heads,
+                                                              scale_log2);
 }
 
 

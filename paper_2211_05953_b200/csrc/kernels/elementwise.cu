@@ -2,6 +2,7 @@
 // scatter-add bwd), fused softmax cross-entropy (loss + dlogits in place),
 // sharded Adam with bf16 emission, Philox normal init, reductions.
 // All use 128-bit vector accesses and grid sizes in multiples of the SM count.
+#include <cub/device/device_radix_sort.cuh>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <curand_kernel.h>
@@ -57,25 +58,58 @@ __global__ void embed_fwd_kernel(const int32_t* __restrict__ tok, const __nv_bfl
     }
 }
 
-__global__ void embed_bwd_kernel(const int32_t* __restrict__ tok, const __nv_bfloat16* __restrict__ dx,
-                                 float* __restrict__ dwte, float* __restrict__ dwpe, int T, int S, int h) {
-    const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x & 31;
-    if (row >= T) return;
-    const int id = tok[row], pos = row % S;
+// Embedding backward without atomics (bit-reproducible): the T (token, row) pairs are radix-sorted
+// by token (stable, so equal tokens keep row order), then one warp per distinct token adds that
+// token's rows of dx in row order to dwte[token], and one warp per position adds the s_mb samples of
+// that position to dwpe[pos]. dwte / dwpe hold the running sums (the executor zeroes them at the
+// start of a reduction unit).
+__global__ void iota_kernel(int32_t* __restrict__ v, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) v[i] = i;
+}
+
+__global__ void embed_wte_bwd_kernel(const int32_t* __restrict__ sk, const int32_t* __restrict__ sv,
+                                     const __nv_bfloat16* __restrict__ dx, float* __restrict__ dwte, int T, int h) {
+    const int i = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x & 31;
+    if (i >= T || (i > 0 && sk[i] == sk[i - 1])) return;  // segment heads only
+    const int id = sk[i];
+    int end = i + 1;
+    while (end < T && sk[end] == id) ++end;
     for (int c = lane * 8; c < h; c += 256) {
-        float a[8];
-        bf8_to_f(*reinterpret_cast<const uint4*>(dx + static_cast<int64_t>(row) * h + c), a);
-        float* pt = dwte + static_cast<int64_t>(id) * h + c;
-        float* pp = dwpe + static_cast<int64_t>(pos) * h + c;
+        float* dst = dwte + static_cast<int64_t>(id) * h + c;
+        float acc[8];
+        const float4 a0 = *reinterpret_cast<const float4*>(dst), a1 = *reinterpret_cast<const float4*>(dst + 4);
+        acc[0] = a0.x, acc[1] = a0.y, acc[2] = a0.z, acc[3] = a0.w, acc[4] = a1.x, acc[5] = a1.y, acc[6] = a1.z,
+        acc[7] = a1.w;
+        for (int k = i; k < end; ++k) {
+            float a[8];
+            bf8_to_f(*reinterpret_cast<const uint4*>(dx + static_cast<int64_t>(sv[k]) * h + c), a);
 #pragma unroll
-        for (int u = 0; u < 8; u += 4) {
-            asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(pt + u), "f"(a[u]), "f"(a[u + 1]),
-                         "f"(a[u + 2]), "f"(a[u + 3])
-                         : "memory");
-            asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(pp + u), "f"(a[u]), "f"(a[u + 1]),
-                         "f"(a[u + 2]), "f"(a[u + 3])
-                         : "memory");
+            for (int u = 0; u < 8; ++u) acc[u] += a[u];
         }
+        *reinterpret_cast<float4*>(dst) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        *reinterpret_cast<float4*>(dst + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
+    }
+}
+
+__global__ void embed_wpe_bwd_kernel(const __nv_bfloat16* __restrict__ dx, float* __restrict__ dwpe, int T, int S,
+                                     int h) {
+    const int pos = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x & 31;
+    if (pos >= S) return;
+    for (int c = lane * 8; c < h; c += 256) {
+        float* dst = dwpe + static_cast<int64_t>(pos) * h + c;
+        float acc[8];
+        const float4 a0 = *reinterpret_cast<const float4*>(dst), a1 = *reinterpret_cast<const float4*>(dst + 4);
+        acc[0] = a0.x, acc[1] = a0.y, acc[2] = a0.z, acc[3] = a0.w, acc[4] = a1.x, acc[5] = a1.y, acc[6] = a1.z,
+        acc[7] = a1.w;
+        for (int row = pos; row < T; row += S) {
+            float a[8];
+            bf8_to_f(*reinterpret_cast<const uint4*>(dx + static_cast<int64_t>(row) * h + c), a);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc[u] += a[u];
+        }
+        *reinterpret_cast<float4*>(dst) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        *reinterpret_cast<float4*>(dst + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
     }
 }
 
@@ -259,7 +293,32 @@ void embed_fwd(const int32_t* tok, const void* wte, const void* wpe, void* x, in
 }
 
 void embed_bwd(const int32_t* tok, const void* dx, float* dwte, float* dwpe, int T, int S, int h, cudaStream_t st) {
-    embed_bwd_kernel<<<(T + 7) / 8, 256, 0, st>>>(tok, static_cast<const __nv_bfloat16*>(dx), dwte, dwpe, T, S, h);
+    if (h % 8) throw std::runtime_error("embed_bwd: hidden size must be a multiple of 8");
+    // per-device workspace: row ids, sorted keys / values, radix-sort temporary storage
+    static thread_local void* ws[64] = {};
+    static thread_local size_t ws_bytes[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    size_t tmp = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, tok, static_cast<int32_t*>(nullptr), static_cast<int32_t*>(nullptr),
+                                    static_cast<int32_t*>(nullptr), T, 0, 32, st);
+    const size_t ids = (static_cast<size_t>(T) * 4 + 255) / 256 * 256;
+    const size_t need = 3 * ids + tmp;
+    if (need > ws_bytes[dev]) {
+        if (ws[dev]) cudaFree(ws[dev]);
+        if (cudaMalloc(&ws[dev], need) != cudaSuccess) throw std::runtime_error("embed_bwd: workspace allocation failed");
+        ws_bytes[dev] = need;
+    }
+    auto* base = static_cast<uint8_t*>(ws[dev]);
+    auto* rows = reinterpret_cast<int32_t*>(base);
+    auto* sk = reinterpret_cast<int32_t*>(base + ids);
+    auto* sv = reinterpret_cast<int32_t*>(base + 2 * ids);
+    iota_kernel<<<(T + 255) / 256, 256, 0, st>>>(rows, T);
+    if (cub::DeviceRadixSort::SortPairs(base + 3 * ids, tmp, tok, sk, rows, sv, T, 0, 32, st) != cudaSuccess)
+        throw std::runtime_error("embed_bwd: radix sort failed");
+    const auto* d = static_cast<const __nv_bfloat16*>(dx);
+    embed_wte_bwd_kernel<<<(T + 7) / 8, 256, 0, st>>>(sk, sv, d, dwte, T, h);
+    embed_wpe_bwd_kernel<<<(S + 7) / 8, 256, 0, st>>>(d, dwpe, T, S, h);
 }
 
 void softmax_xent(void* logits, int64_t ld, const int32_t* labels, float* row_loss, int T, int V, float grad_scale,

@@ -12,3 +12,8 @@ for k in gemm2_kernel attn_fwd_tc_kernel attn_bwd_tc_kernel ln_bwd_reg_kernel ad
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 20 -c 1 -o gpurun_out/full_$k -f $B \
     > gpurun_out/ncu_$k.log 2>&1; echo "$k rc=$?"
 done
+# GPT-6.7B on one B200 (no pipeline bubble: the per-GPU efficiency ceiling of the 6.7B shapes)
+for b in 1 2; do
+  timeout 600 python bench.py --model gpt-6.7b --loops 4 --beta $b --steps 5 --warmup 3 --no-e2e --no-cpu-baseline \
+    > gpurun_out/bench_6.7b_n1_b$b.json 2> gpurun_out/bench_6.7b_n1_b$b.err; echo "6.7b b$b rc=$?"
+done

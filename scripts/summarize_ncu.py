@@ -3,6 +3,8 @@ from a --csv --metrics log, and key metrics of --set full captures. Usage:
   python scripts/summarize_ncu.py launches.csv full_a.ncu-rep [full_b.ncu-rep ...] > summary.md"""
 import collections
 import csv
+import json
+import os
 import io
 import re
 import subprocess
@@ -32,6 +34,14 @@ def launch_list(path):
         a[1] += m.get("gpu__time_duration.sum", 0)
         a[2] += m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)
     tot = sum(v[1] for v in agg.values())
+    g = [v for n, v in agg.items() if n.startswith("gemm")]
+    if g and os.environ.get("GEMM_TRAFFIC_OUT"):  # per-launch GEMM DRAM bytes for bench.py's roofline.traffic
+        c, b = sum(v[0] for v in g), sum(v[2] for v in g)
+        with open(os.environ["GEMM_TRAFFIC_OUT"], "w") as f:
+            json.dump({"bytes_per_launch": int(b / c), "launches_in_list": c,
+                       "source": f"{path}: mean dram__bytes_read.sum + dram__bytes_write.sum over the GEMM kernel "
+                                 "launches of bench.py (GPT-1.3B, N=1; weight-gradient pairs are one grouped launch)"},
+                      f, indent=1)
     print("| kernel | launches | total ms | avg us | share | DRAM MB / launch |")
     print("|---|---|---|---|---|---|")
     for n, (c, t, b) in sorted(agg.items(), key=lambda x: -x[1][1]):
