@@ -202,6 +202,8 @@ int bfpp_gemm_bf16_pair(const bfpp_gemm_args* a, const bfpp_gemm_args* b, void* 
  * stream_k = 0 off (default), 1 forced, -1 auto (only when the last tile wave leaves pairs idle).
  * Defaults come from BFPP_GEMM_MODE / BFPP_GEMM_BN2 / BFPP_GEMM_SK. */
 int bfpp_gemm_config(int32_t mode, int32_t bn2, int32_t stream_k);
+/* attention forward: query tiles per CTA (0 auto, 1, 2 = two tiles sharing K/V, ping-pong softmax) */
+int bfpp_attention_config(int32_t fwd_tiles);
 /* persistent GEMM grids use at most n SMs (0 = all): for streams confined to an SM partition */
 int bfpp_gemm_sm_limit(int32_t n);
 /* Process-wide launch counters per kernel variant (0 1-CTA GEMM, 1 2-CTA GEMM, 2 grouped 2-CTA

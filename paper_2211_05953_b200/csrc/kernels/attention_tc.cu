@@ -521,6 +521,8 @@ __global__ void __launch_bounds__(320, 1)
 
 }  // namespace
 
+int attn_fwd_tiles = 0;  // query tiles per forward CTA: 0 auto, 1, 2 (tests / benchmarks)
+
 void attention_fwd_tc(const void* qkv, void* o, float* lse, int batch, int seq, int heads, int head_dim,
                       cudaStream_t st) {
     if (head_dim != D) throw std::runtime_error("attention: head_dim must be 128");
@@ -534,7 +536,15 @@ void attention_fwd_tc(const void* qkv, void* o, float* lse, int batch, int seq, 
     dim3 grid(heads, (seq + BQ - 1) / BQ, batch);
     if (heads > 1 && seq > BQ) count_variant(KV_ATTN_FWD_MULTI);
     const float scale_log2 = kLog2e / sqrtf(static_cast<float>(head_dim));
-    static const bool one_tile = getenv("BFPP_ATTN_FWD") && atoi(getenv("BFPP_ATTN_FWD")) == 1;
+    // two query tiles per CTA halve the CTA count; with fewer than ~2 waves of pairs the causal
+    // imbalance (the longest pair has 2x the key tiles of the longest single block) outweighs the
+    // ping-pong (measured: 1x2048x16 heads 28.9 vs 46.4 us; 4x2048x32 218 vs 208 us; 1x4096x16 90
+    // vs 87 us). BFPP_ATTN_FWD=1 / 2 forces one / two tiles.
+    const int n_qb = (seq + BQ - 1) / BQ;
+    const int64_t pair_ctas = static_cast<int64_t>(heads) * batch * ((n_qb + 1) / 2);
+    static const int env = getenv("BFPP_ATTN_FWD") ? atoi(getenv("BFPP_ATTN_FWD")) : 0;
+    const int force = attn_fwd_tiles ? attn_fwd_tiles : env;
+    const bool one_tile = force == 1 || (force != 2 && pair_ctas < 256);
     if (one_tile) {
         attn_fwd_tc_kernel<<<grid, 192, FwdSmem::kBytes, st>>>(tm, static_cast<__nv_bfloat16*>(o), lse, seq, heads,
                                                                scale_log2);
@@ -545,7 +555,6 @@ void attention_fwd_tc(const void* qkv, void* o, float* lse, int batch, int seq, 
         cudaFuncSetAttribute(attn_fwd_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2Smem::kBytes);
         cfg2 = true;
     }
-    const int n_qb = (seq + BQ - 1) / BQ;
     dim3 grid2(heads, (n_qb + 1) / 2, batch);
     attn_fwd_tc2_kernel<<<grid2, 320, Fwd2Smem::kBytes, st>>>(tm, static_cast<__nv_bfloat16*>(o), lse, seq, heads,
                                                               scale_log2);

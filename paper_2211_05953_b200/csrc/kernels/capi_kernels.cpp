@@ -44,6 +44,13 @@ int bfpp_gemm_config(int32_t mode, int32_t bn2, int32_t stream_k) {
     });
 }
 
+int bfpp_attention_config(int32_t fwd_tiles) {
+    return guarded([&] {
+        if (fwd_tiles < 0 || fwd_tiles > 2) throw SpecError("attention_config: fwd_tiles must be 0, 1 or 2");
+        bfpp::attn_fwd_tiles = fwd_tiles;
+    });
+}
+
 int bfpp_gemm_sm_limit(int32_t n) {
     return guarded([&] {
         if (n < 0) throw SpecError("gemm_sm_limit: must be >= 0 (0 = all SMs)");

@@ -8,6 +8,8 @@ namespace bfpp {
 
 // attention.cu — causal MHA, head_dim 128; qkv [B*S][3*H*128], o [B*S][H*128], lse [B*H][S] (log2 domain)
 void attention_fwd(const void* qkv, void* o, float* lse, int batch, int seq, int heads, int head_dim, cudaStream_t st);
+// query tiles per forward CTA: 0 auto (two when there are >= 256 tile pairs), 1, 2
+extern int attn_fwd_tiles;
 // tcgen05/TMEM version of attention_fwd (attention_tc.cu); same inputs/outputs
 void attention_fwd_tc(const void* qkv, void* o, float* lse, int batch, int seq, int heads, int head_dim,
                       cudaStream_t st);

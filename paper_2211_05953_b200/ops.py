@@ -78,6 +78,11 @@ def gemm_pair(first: dict, second: dict):
     return ox, oy
 
 
+def attention_config(fwd_tiles: int = 0):
+    """Query tiles per attention-forward CTA: 0 auto, 1, 2."""
+    _check(_nat.lib().bfpp_attention_config(fwd_tiles))
+
+
 def gemm_config(mode: int = -1, bn2: int = 0, stream_k: int = -1):
     """Process-wide GEMM variant selection (tests / benchmarks): mode -1 auto, 1 one-CTA, 2 two-CTA;
     bn2 = two-CTA tile width (0 default 256, 128); stream_k -1 auto, 0 off, 1 forced."""

@@ -28,9 +28,12 @@ def _ref_attention(qkv, B, S, H, D=128):
     return torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True)  # [B,H,S,D]
 
 
-@pytest.mark.parametrize("B,S,H", [(1, 128, 2), (2, 256, 3), (1, 2048, 2), (1, 64, 4), (1, 200, 2)])
-def test_attention_fwd_bwd(cuda_device, B, S, H):
+@pytest.mark.parametrize("fwd_tiles", [1, 2])
+@pytest.mark.parametrize("B,S,H", [(1, 128, 2), (2, 256, 3), (1, 2048, 2), (1, 64, 4), (1, 200, 2), (2, 384, 2)])
+def test_attention_fwd_bwd(cuda_device, B, S, H, fwd_tiles, request):
     ops = _ops()
+    ops.attention_config(fwd_tiles)  # one query tile per CTA, or two (ping-pong, odd block counts too)
+    request.addfinalizer(lambda: ops.attention_config(0))
     D = 128
     torch.manual_seed(B * 1000 + S + H)
     qkv = torch.randn(B * S, 3 * H * D, device="cuda").bfloat16()
