@@ -6,6 +6,14 @@
       --n-mb 1 --steps 5 [--trace t.json] [--gantt g.svg]
   (N > 1 ranks: python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 -m paper_2211_05953_b200 execute ...)
 
+  python -m paper_2211_05953_b200 search --model gpt-6.7b --cluster b200 --batch 8 16 \
+      [--scoring measured --rates-from bench_line.json] [--top 20]
+
+`search` ranks the feasible configurations of a search space like the reference's `rank_configs`
+(search.cpp:136-188; simulate scoring = TimingModel::derive), or with per-kind task costs
+measured on B200s (`--scoring measured`: the `measured_timing.rates` of a bench.py JSON line, or
+--rates f,b,pp,lat,red,rec), printing one CSV row per configuration; exit 3 when nothing is
+feasible (the reference's empty-result code).
 `simulate` prints the reference's summary lines (makespan, bubble, peak in-flight layers, lane busy
 times; report.cpp:214-232) for the analytic timing model; `execute` runs the same task graph on the local B200(s),
 prints the measured step time, tokens/s, the measured bubble fraction and the bubble of the
@@ -28,7 +36,7 @@ VARIANTS = {"dp0": ps.DpVariant.DP0, "dp_ps": ps.DpVariant.DP_PS, "dp_fs": ps.Dp
 
 def _args(argv):
     ap = argparse.ArgumentParser(prog="python -m paper_2211_05953_b200")
-    ap.add_argument("command", choices=["simulate", "execute"])
+    ap.add_argument("command", choices=["simulate", "execute", "search"])
     ap.add_argument("--model", default="gpt-1.3b", choices=sorted(PRESETS))
     ap.add_argument("--schedule", default="breadth_first", choices=sorted(SCHEDULES))
     ap.add_argument("--dp-variant", default="dp_fs", choices=sorted(VARIANTS))
@@ -45,6 +53,21 @@ def _args(argv):
     ap.add_argument("--t-reconstruct", type=float, default=0.0)
     ap.add_argument("--trace", help="write the (simulated / measured) timeline as Chrome trace JSON")
     ap.add_argument("--gantt", help="write the timeline as an SVG Gantt chart")
+    # search
+    ap.add_argument("--cluster", default="b200", help="search: cluster preset (a100, v100-dgx1, b200)")
+    ap.add_argument("--gpus", type=int, default=None, help="search: GPUs per node (overrides the preset)")
+    ap.add_argument("--schedules", nargs="+", default=["gpipe", "1f1b", "depth_first", "breadth_first"])
+    ap.add_argument("--variants", nargs="+", default=["dp0", "dp_ps", "dp_fs"])
+    ap.add_argument("--pp-choices", type=int, nargs="+", default=[1, 2, 4, 8])
+    ap.add_argument("--loop-choices", type=int, nargs="+", default=[1, 2, 4])
+    ap.add_argument("--mb-choices", type=int, nargs="+", default=[1, 2, 4, 8, 16, 32])
+    ap.add_argument("--smb-choices", type=int, nargs="+", default=[1])
+    ap.add_argument("--batch", type=int, nargs="+", default=[8, 16])
+    ap.add_argument("--scoring", default="simulate", choices=["simulate", "measured"])
+    ap.add_argument("--rates-from", help="search: bench.py JSON line(s); the last measured_timing.rates is used")
+    ap.add_argument("--rates", type=float, nargs=6, help="search: fwd_layer_seq bwd_ratio pp_s_per_byte "
+                                                          "pp_latency reduce_s_per_param reconstruct_s_per_param")
+    ap.add_argument("--top", type=int, default=0, help="search: print only the best N per batch size")
     return ap.parse_args(argv)
 
 
@@ -80,6 +103,8 @@ def main(argv=None) -> int:
             _write(a.trace, ps.chrome_trace_json(tl, graph))
             _write(a.gantt, ps.gantt_svg(tl, graph))
             return 0
+        if a.command == "search":
+            return _search(a, model)
         return _execute(a, cfg, model, config)
     except ps.SpecError as e:
         print(e, file=sys.stderr)
@@ -87,6 +112,48 @@ def main(argv=None) -> int:
     except ps.SimError as e:
         print(e, file=sys.stderr)
         return 4
+
+
+def _search(a, model) -> int:
+    import json
+    k = ps.cluster_preset(a.cluster)
+    if a.gpus:
+        k = ps.ClusterSpec(1, a.gpus, k.peak_flops, k.bw_intra, k.bw_inter, k.pp_latency, k.mem_capacity,
+                           k.kernel_efficiency)
+    rates = None
+    if a.scoring == "measured":
+        if a.rates:
+            rates = ps.MeasuredRates(*a.rates)
+        elif a.rates_from:
+            for line in open(a.rates_from):
+                line = line.strip()
+                if line.startswith("{") and '"measured_timing"' in line:
+                    mt = json.loads(line).get("measured_timing")
+                    if mt:
+                        rates = ps.MeasuredRates(**mt["rates"])
+        if rates is None:
+            raise ps.SpecError("error[invalid-spec]: search: measured scoring needs --rates or --rates-from "
+                               "with a measured_timing line")
+    ranked = ps.rank_configs(model, k, schedules=[int(SCHEDULES[x]) for x in a.schedules],
+                             dp_variants=[int(VARIANTS[x]) for x in a.variants], n_pp=a.pp_choices,
+                             s_mb=a.smb_choices, n_mb=a.mb_choices, n_loop=a.loop_choices, batch_sizes=a.batch,
+                             scoring=a.scoring, rates=rates)
+    if not ranked:
+        print("pipesim: error[empty-result]: every configuration of the search space is infeasible", file=sys.stderr)
+        return 3
+    names = {v: n for n, v in SCHEDULES.items()}
+    print("rank,batch,schedule,dp_variant,n_pp,n_loop,n_dp,n_mb,s_mb,flops_per_gpu,tokens_per_second_per_gpu,"
+          "bubble,memory_bytes")
+    shown = {}
+    for i, r in enumerate(ranked, 1):
+        c = r.config
+        if a.top and shown.get(c.batch_size(), 0) >= a.top:
+            continue
+        shown[c.batch_size()] = shown.get(c.batch_size(), 0) + 1
+        tok = r.score / ps.compute_per_gpu(model, c) * c.batch_size() * model.s_seq / k.n_gpu()
+        print(f"{i},{c.batch_size()},{names[c.schedule]},{c.dp_variant.name},{c.n_pp},{c.n_loop},{c.n_dp},{c.n_mb},"
+              f"{c.s_mb},{r.score:.6e},{tok:.1f},{r.bubble:.6f},{r.memory_bytes:.0f}")
+    return 0
 
 
 def _execute(a, cfg, model, config) -> int:

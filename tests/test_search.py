@@ -123,3 +123,23 @@ def test_simulate_durations_replays_simulate():
         ps.simulate_durations(g, dur[:-1])
     with pytest.raises(ps.SpecError):
         ps.simulate_durations(g, [-1.0] + dur[1:])
+
+
+def test_cli_search(tmp_path, capsys):
+    """`python -m paper_2211_05953_b200 search`: simulate ranking, measured ranking from a bench line,
+    and the reference's empty-result exit code."""
+    import json
+    from paper_2211_05953_b200.__main__ import main
+    assert main(["search", "--model", "gpt-6.7b", "--batch", "16", "--top", "3"]) == 0
+    rows = capsys.readouterr().out.strip().splitlines()
+    assert rows[0].startswith("rank,batch,schedule") and len(rows) == 4
+    line = {"measured_timing": {"rates": {"fwd_layer_seq": 7.7e-4, "bwd_ratio": 2.2, "pp_s_per_byte": 2.5e-12,
+                                          "pp_latency": 0.0, "reduce_s_per_param": 2.7e-13,
+                                          "reconstruct_s_per_param": 3.3e-12}}}
+    f = tmp_path / "bench.jsonl"
+    f.write_text("noise\n" + json.dumps(line) + "\n")
+    assert main(["search", "--model", "gpt-6.7b", "--batch", "8", "--scoring", "measured", "--rates-from", str(f)]) == 0
+    out = capsys.readouterr().out.strip().splitlines()
+    assert len(out) > 5 and float(out[1].split(",")[10]) >= float(out[-1].split(",")[10])
+    assert main(["search", "--model", "gpt-6.7b", "--scoring", "measured"]) == 2
+    assert main(["search", "--model", "52b", "--gpus", "2", "--batch", "1"]) == 3
