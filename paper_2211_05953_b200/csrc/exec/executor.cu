@@ -249,6 +249,13 @@ struct Executor::Impl {
     std::vector<void*> ipc_opened;
     uint32_t xfer_seq = 0;                 // step sequence number written into the flags
     std::vector<void*> allocs;
+    // DP_FS all-gather through the copy engines (opt-in): the bf16 shard and full-weight slot buffers are
+    // ncclMemAlloc'd and registered as symmetric windows of a CTAPolicy-ZERO DP communicator, so
+    // NCCL moves them with copy engines instead of taking SMs from the compute stream
+    // (scripts/nccl_sym.cu: 544 vs 407 GB/s per direction at n_dp = 2, no SM kernel)
+    bool sym = false;
+    std::vector<std::pair<void*, size_t>> sym_bufs;
+    std::vector<ncclWindow_t> wins;
     std::vector<LocalStage> local;  // index c
     bf16* slots[2] = {nullptr, nullptr};
     std::vector<std::vector<StageActs>> acts;  // [mb][c]
@@ -273,6 +280,7 @@ struct Executor::Impl {
     int bwd_layers = 0;  // backward layers processed in the current step (scratch set parity)
     bool wgrad_stream = false;
     bool debug = false;
+    bool watchdog = false;  // BFPP_EXEC_WATCHDOG: stall reports without the debug mode's serialisation
     std::vector<int> task_c;                      // local stage index of compute tasks
     KernelStats stats;
     struct Mark {
@@ -294,7 +302,7 @@ struct Executor::Impl {
     MemoryPlan* mem = nullptr;
     size_t* total = nullptr;
     template <class T>
-    T* alloc(size_t n, int cat) {
+    T* alloc(size_t n, int cat, bool window = false) {
         const size_t bytes = std::max<size_t>(n * sizeof(T), 256);
         mem->bytes[cat] += bytes;
         *total += bytes;
@@ -304,6 +312,11 @@ struct Executor::Impl {
             return static_cast<T*>(p);
         }
         void* p = nullptr;
+        if (window && sym) {
+            NK(ncclMemAlloc(&p, bytes));
+            sym_bufs.push_back({p, bytes});
+            return static_cast<T*>(p);
+        }
         CK(cudaMalloc(&p, bytes));
         allocs.push_back(p);
         return static_cast<T*>(p);
@@ -359,12 +372,17 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
     I.total = &dev_bytes_;
     if (const char* e = getenv("BFPP_WGRAD_STREAM")) I.wgrad_stream = atoi(e) != 0;
     if (const char* e = getenv("BFPP_EXEC_DEBUG")) I.debug = atoi(e) != 0;
+    if (const char* e = getenv("BFPP_EXEC_WATCHDOG")) I.watchdog = atoi(e) != 0;
     // recompute: one working set per rank, so weight gradients stay on the compute stream
     if (o_.recompute) I.wgrad_stream = false;
     const bool fs = c_.n_dp >= 2 && c_.dp_variant == DpVariant::DP_FS;
     // sharded variants: gradients are consumed by reduce-scatters, so the rank's stages share one
     // f32 gradient buffer (reused per segment as the previous unit's reduce-scatters drain it)
     const bool pooled = c_.n_dp >= 2 && c_.dp_variant != DpVariant::DP0;
+    // opt-in (BFPP_DP_CE_ALLGATHER=1): +3.6% at N = 4, but 3 of 14 GPT-1.3B N = 4 bench runs hung
+    // inside an all-gather on both DP peers ("Copy-engine all-gather")
+    if (const char* e = getenv("BFPP_DP_CE_ALLGATHER")) I.sym = fs && !I.dry && atoi(e) != 0;
+    if (!I.dry) CK(cudaSetDevice(I.dev));
 
     // ---- per-task execution plan (host only) ----
     I.order = plan_rank(graph_, pp_rank_, c_.n_dp, pooled);
@@ -403,7 +421,7 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
                     gseg_n = std::max(gseg_n, (ls.seg[si + 1] - ls.seg[si]) / ls.nd);
             }
             if (ls.n_units > 1) gtmp_n = std::max(gtmp_n, ls.shard_n);
-            ls.w16_shard = I.alloc<bf16>(static_cast<size_t>(ls.shard_n), M_WEIGHT_SHARDS);
+            ls.w16_shard = I.alloc<bf16>(static_cast<size_t>(ls.shard_n), M_WEIGHT_SHARDS, true);
         }
         I.local.push_back(ls);
     }
@@ -416,7 +434,7 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
         if (gseg_n) I.gseg = I.alloc<float>(static_cast<size_t>(gseg_n), M_GRAD_SHARDS);
     }
     if (fs)
-        for (auto& sl : I.slots) sl = I.alloc<bf16>(static_cast<size_t>(max_padded), M_WEIGHTS);
+        for (auto& sl : I.slots) sl = I.alloc<bf16>(static_cast<size_t>(max_padded), M_WEIGHTS, true);
 
     // ---- activations: pooled sets of the live (micro-batch, local stage) pairs ----
     // A forward takes a set, the backward of the same (micro-batch, stage) returns it; set ids are
@@ -609,10 +627,18 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
         if (world > 1 && uids.size() < need) throw SpecError("executor: not enough NCCL unique ids");
         NK(ncclGroupStart());
         if (world > 1) NK(ncclCommInitRank(&I.world_comm, world, uids[0], rank));
+        ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+        if (I.sym) cfg.CTAPolicy = NCCL_CTA_POLICY_ZERO;  // copy-engine all-gathers on the windows below
         if (c_.n_dp >= 2)
-            NK(ncclCommInitRank(&I.dp_comm, static_cast<int>(c_.n_dp), uids[static_cast<size_t>(1 + pp_rank_)],
-                                static_cast<int>(dp_rank_)));
+            NK(ncclCommInitRankConfig(&I.dp_comm, static_cast<int>(c_.n_dp),
+                                      uids[static_cast<size_t>(1 + pp_rank_)], static_cast<int>(dp_rank_), &cfg));
         NK(ncclGroupEnd());
+        // symmetric windows: every DP peer allocated the same buffers in the same order
+        for (auto& b : I.sym_bufs) {
+            ncclWindow_t w;
+            NK(ncclCommWindowRegister(I.dp_comm, b.first, b.second, &w, NCCL_WIN_COLL_SYMMETRIC));
+            I.wins.push_back(w);
+        }
         if (I.world_comm) I.comm_ids.push_back({0, I.world_comm});
         if (I.dp_comm) I.comm_ids.push_back({static_cast<size_t>(1 + pp_rank_), I.dp_comm});
     }
@@ -740,7 +766,9 @@ Executor::~Executor() {
     if (I.recv_flags) cudaFree(I.recv_flags);
     std::vector<std::pair<size_t, ncclComm_t>> comms(I.comm_ids.begin(), I.comm_ids.end());
     std::sort(comms.begin(), comms.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    for (ncclWindow_t w : I.wins) ncclCommWindowDeregister(I.dp_comm, w);
     for (auto& kv : comms) ncclCommDestroy(kv.second);
+    for (auto& b : I.sym_bufs) ncclMemFree(b.first);
     for (auto e : I.done)
         if (e) cudaEventDestroy(e);
     for (auto e : I.t_start)
@@ -801,33 +829,7 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
     if (I.debug) fprintf(stderr, "[bfpp rank %d] step %d begin\n", rank_, I.step_no);
     // debug mode: no run-ahead at all, so a stalled step is reported by the watchdog below
     const int cap_slot = I.debug ? (I.step_no - 1) & 1 : I.step_no & 1;
-    if (I.step_no >= (I.debug ? 2 : 3)) {
-        if (!I.debug) {
-            CK(cudaEventSynchronize(I.step_done[cap_slot]));
-        } else {  // watchdog: report the first unfinished tasks if the device stalls
-            auto t0 = std::chrono::steady_clock::now();
-            while (cudaEventQuery(I.step_done[cap_slot]) == cudaErrorNotReady) {
-                if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(20)) {
-                    fprintf(stderr, "[bfpp rank %d] STALL waiting for step %d; unfinished tasks:\n", rank_,
-                            I.step_no - 2);
-                    int shown = 0;
-                    for (const TaskExec& te : I.order) {
-                        if (cudaEventQuery(I.done[static_cast<size_t>(te.id)]) == cudaErrorNotReady && shown < 12) {
-                            const Task& tt = graph_.tasks[static_cast<size_t>(te.id)];
-                            fprintf(stderr, "  task %d kind %s mb %lld stage %lld stream %d\n", te.id,
-                                    kind_name(tt.kind), (long long)tt.micro_batch, (long long)tt.stage, te.stream);
-                            ++shown;
-                        }
-                    }
-                    for (int q = 0; q < S_N; ++q)
-                        fprintf(stderr, "  stream %d query %d\n", q, static_cast<int>(cudaStreamQuery(I.st[q])));
-                    fflush(stderr);
-                    t0 = std::chrono::steady_clock::now() + std::chrono::seconds(3600);
-                }
-                std::this_thread::sleep_for(std::chrono::milliseconds(1));
-            }
-        }
-    }
+    if (I.step_no >= (I.debug ? 2 : 3)) wait_step_event(I.step_done[cap_slot], I.step_no - 2);
     if (I.debug) fprintf(stderr, "[bfpp rank %d] step %d run-ahead cap passed\n", rank_, I.step_no);
     for (int s = 0; s < S_N; ++s) CK(cudaStreamWaitEvent(I.st[s], I.step_end, 0));
     const int64_t T = c_.s_mb * m_.s_seq, h = m_.s_hidden, mlp = m_.s_mlp, V = m_.s_voc;
@@ -1278,7 +1280,7 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
     CK(cudaPeekAtLastError());
     if (I.debug) fprintf(stderr, "[bfpp rank %d] step %d enqueued\n", rank_, I.step_no);
     if (o_.profile_kernels) {
-        CK(cudaEventSynchronize(I.step_end));
+        wait_step_event(I.step_end, I.step_no);
         for (const auto& mk : I.marks) {
             float ms = 0;
             CK(cudaEventElapsedTime(&ms, I.ev_pool[mk.ev], I.ev_pool[mk.ev + 1]));
@@ -1287,7 +1289,7 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
         }
     }
     if (o_.record_timeline) {
-        CK(cudaEventSynchronize(I.step_end));
+        wait_step_event(I.step_end, I.step_no);
         for (const TaskExec& te : I.order) {
             float a = 0, b = 0;
             CK(cudaEventElapsedTime(&a, I.origin, I.t_start[static_cast<size_t>(te.id)]));
@@ -1299,6 +1301,40 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
             I.tl_end[static_cast<size_t>(te.id)] = b * 1e-3;
         }
     }
+}
+
+// Host wait for a step's completion event. With the watchdog on (debug mode, or
+// BFPP_EXEC_WATCHDOG=1) the event is polled and, after 20 s without progress, the first
+// unfinished tasks and the state of every stream are reported once (then the wait continues).
+void Executor::wait_step_event(cudaEvent_t ev, int step) {
+    Impl& I = *impl_;
+    if (!I.debug && !I.watchdog) {
+        CK(cudaEventSynchronize(ev));
+        return;
+    }
+    auto t0 = std::chrono::steady_clock::now();
+    bool reported = false;
+    cudaError_t q;
+    while ((q = cudaEventQuery(ev)) == cudaErrorNotReady) {
+        if (!reported && std::chrono::steady_clock::now() - t0 > std::chrono::seconds(20)) {
+            fprintf(stderr, "[bfpp rank %d] STALL waiting for step %d; unfinished tasks:\n", rank_, step);
+            int shown = 0;
+            for (const TaskExec& te : I.order) {
+                if (cudaEventQuery(I.done[static_cast<size_t>(te.id)]) == cudaErrorNotReady && shown < 12) {
+                    const Task& tt = graph_.tasks[static_cast<size_t>(te.id)];
+                    fprintf(stderr, "  task %d kind %s mb %lld stage %lld stream %d\n", te.id, kind_name(tt.kind),
+                            (long long)tt.micro_batch, (long long)tt.stage, te.stream);
+                    ++shown;
+                }
+            }
+            for (int s = 0; s < S_N; ++s)
+                fprintf(stderr, "  stream %d query %d\n", s, static_cast<int>(cudaStreamQuery(I.st[s])));
+            fflush(stderr);
+            reported = true;
+        }
+        std::this_thread::sleep_for(std::chrono::microseconds(100));
+    }
+    CK(q);
 }
 
 const KernelStats& Executor::kernel_stats() const { return impl_->stats; }

@@ -115,6 +115,7 @@ public:
 
 private:
     struct Impl;
+    void wait_step_event(cudaEvent_t ev, int step);
     std::unique_ptr<Impl> impl_;
     ModelSpec m_;
     ParallelConfig c_;
