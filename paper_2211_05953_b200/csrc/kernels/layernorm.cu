@@ -1,18 +1,26 @@
-// LayerNorm forward/backward (HBM-bound). One warp per row, 8 rows per 256-thread
-// block, 128-bit vector accesses, f32 statistics via warp shuffles; two passes per
-// row (the second pass re-reads the row from L1) so no per-thread row arrays are
-// held in registers at any width. The parameter gradients are a separate
-// two-level column reduction over 8-row chunks (coalesced, deterministic).
+// LayerNorm forward/backward (HBM-bound), bf16 rows, f32 statistics.
 //   fwd: y = (x - mean) * rstd * gamma + beta       (bf16 in/out; mean/rstd f32 saved)
 //   bwd: dx = rstd * (g - mean(g) - xhat * mean(g * xhat)) [+ dres],  g = dy * gamma
 //        dgamma += sum_rows dy * xhat, dbeta += sum_rows dy   (f32, accumulated across calls)
+// Dispatch by row width:
+//   backward, width <= 8192: bulk-staged kernel (cp.async.bulk rows into shared memory, column
+//     partials per block) + one deterministic partial-sum kernel;
+//   forward, width <= 4096: register-resident rows (one warp per row, or two for > 2048);
+//     forward 4096 < width <= 8192: bulk-staged kernel;
+//   wider rows: generic two-pass kernels (the row re-read from L1) with a two-level column
+//     reduction for the parameter gradients. No atomics in any gradient path except the
+//     generic column sum.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
+#include <set>
 #include <stdexcept>
 #include <type_traits>
 
 #include "kernels.hpp"
+#include "sm100_ptx.cuh"
 
 namespace bfpp {
 namespace {
@@ -586,6 +594,279 @@ bool ln_dispatch_wide(int width, F&& f) {
     return false;
 }
 
+using namespace ptx;
+
+// ---- bulk-staged variants (scripts/ln_bench.py, backward at 2048 x 2048: 13.6 vs 16.3 us; at
+// 2048 x 8192: 44 vs 101 us): a block's R rows (and gamma / beta) are fetched with one-shot
+// cp.async.bulk copies into shared memory, completing on one mbarrier, so every load of the block
+// is in flight at once with no register cost; two or more blocks per SM then overlap one block's
+// arithmetic with the next block's loads. W = 8 / R warps per row.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ uint4 lds16(const __nv_bfloat16* p) { return *reinterpret_cast<const uint4*>(p); }
+
+// the rows [r0, r0 + nr) of each of the n_src tensors, then the n_vec width-vectors, issued by warp 0
+__device__ __forceinline__ void bulk_rows(uint64_t* bar, const __nv_bfloat16* const* src, __nv_bfloat16* const* dst,
+                                          int n_src, const __nv_bfloat16* const* vsrc, __nv_bfloat16* const* vdst,
+                                          int n_vec, int64_t r0, int nr, int width) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t rb = static_cast<uint32_t>(width) * 2;
+    if (lane == 0) mbar_expect_tx(bar, rb * static_cast<uint32_t>(n_src * nr + n_vec));
+    __syncwarp();
+    for (int i = lane; i < n_src * nr + n_vec; i += 32) {
+        if (i < n_src * nr) {
+            const int t = i / nr, r = i % nr;
+            bulk_g2s(dst[t] + static_cast<int64_t>(r) * width, src[t] + (r0 + r) * width, rb, bar);
+        } else {
+            bulk_g2s(vdst[i - n_src * nr], vsrc[i - n_src * nr], rb, bar);
+        }
+    }
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) ln_fwd_bulk_kernel(const __nv_bfloat16* __restrict__ x,
+                                                          const __nv_bfloat16* __restrict__ gamma,
+                                                          const __nv_bfloat16* __restrict__ beta,
+                                                          __nv_bfloat16* __restrict__ y, float* __restrict__ mean_out,
+                                                          float* __restrict__ rstd_out, int rows, int width, float eps) {
+    constexpr int W = 8 / R;
+    extern __shared__ __align__(128) uint8_t ln_smem[];
+    __nv_bfloat16* sx = reinterpret_cast<__nv_bfloat16*>(ln_smem);
+    __nv_bfloat16* sg = sx + R * width;
+    __nv_bfloat16* sb = sg + width;
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ float st[R][W];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * R;
+    const int nr = min(R, static_cast<int>(rows - r0));
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const __nv_bfloat16* src[1] = {x};
+        __nv_bfloat16* dst[1] = {sx};
+        const __nv_bfloat16* vs[2] = {gamma, beta};
+        __nv_bfloat16* vd[2] = {sg, sb};
+        bulk_rows(&bar, src, dst, 1, vs, vd, 2, r0, nr, width);
+    }
+    mbar_wait(&bar, 0);
+    const int ri = warp / W, part = warp % W;
+    const bool valid = ri < nr;
+    const __nv_bfloat16* xr = sx + ri * width;
+    float s = 0.f;
+    if (valid)
+        for (int c = (part * 32 + lane) * 8; c < width; c += W * 256) {
+            float v[8];
+            unpack8(lds16(xr + c), v);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s += v[u];
+        }
+    s = warp_sum(s);
+    if constexpr (W > 1) {
+        if (lane == 0) st[ri][part] = s;
+        __syncthreads();
+        s = 0.f;
+#pragma unroll
+        for (int w = 0; w < W; ++w) s += st[ri][w];
+        __syncthreads();
+    }
+    const float mean = s / width;
+    float q = 0.f;
+    if (valid)
+        for (int c = (part * 32 + lane) * 8; c < width; c += W * 256) {
+            float v[8];
+            unpack8(lds16(xr + c), v);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) q += (v[u] - mean) * (v[u] - mean);
+        }
+    q = warp_sum(q);
+    if constexpr (W > 1) {
+        if (lane == 0) st[ri][part] = q;
+        __syncthreads();
+        q = 0.f;
+#pragma unroll
+        for (int w = 0; w < W; ++w) q += st[ri][w];
+    }
+    const float rstd = rsqrtf(q / width + eps);
+    if (!valid) return;
+    __nv_bfloat16* yr = y + (r0 + ri) * width;
+    for (int c = (part * 32 + lane) * 8; c < width; c += W * 256) {
+        float v[8], g[8], b[8];
+        unpack8(lds16(xr + c), v);
+        unpack8(lds16(sg + c), g);
+        unpack8(lds16(sb + c), b);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = (v[u] - mean) * rstd * g[u] + b[u];
+        store8(yr + c, v);
+    }
+    if (lane == 0 && part == 0) {
+        mean_out[r0 + ri] = mean;
+        rstd_out[r0 + ri] = rstd;
+    }
+}
+
+// dx of R-row groups (block-strided loop, one group staged at a time), and the block's column
+// partials ws[block][0..width) = sum dy * xhat, ws[block][width..2 width) = sum dy accumulated
+// in registers across its groups (C 2048-column slices per thread) and written once, so the
+// partial traffic is gridDim.x (<= 2 per SM) rows, not one per group
+template <int R, int C, bool RES>
+__global__ void __launch_bounds__(256) ln_bwd_bulk_kernel(const __nv_bfloat16* __restrict__ dy,
+                                                          const __nv_bfloat16* __restrict__ x,
+                                                          const __nv_bfloat16* __restrict__ gamma,
+                                                          const float* __restrict__ mean,
+                                                          const float* __restrict__ rstd,
+                                                          const __nv_bfloat16* __restrict__ dres,
+                                                          __nv_bfloat16* __restrict__ dx, float* __restrict__ ws,
+                                                          int rows, int width) {
+    constexpr int W = 8 / R;
+    extern __shared__ __align__(128) uint8_t ln_smem[];
+    __nv_bfloat16* sx = reinterpret_cast<__nv_bfloat16*>(ln_smem);
+    __nv_bfloat16* sd = sx + R * width;
+    __nv_bfloat16* sg = sd + R * width;
+    __nv_bfloat16* sr = sg + width;  // RES only
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ float s_mu[R], s_rs[R];
+    __shared__ float st[R][W][2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ri = warp / W, part = warp % W;
+    const int n_groups = (rows + R - 1) / R;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        fence_barrier_init();
+    }
+    float pg[C][8] = {}, pb[C][8] = {};
+    int it = 0;
+    for (int grp = blockIdx.x; grp < n_groups; grp += gridDim.x, ++it) {
+        const int64_t r0 = static_cast<int64_t>(grp) * R;
+        const int nr = min(R, static_cast<int>(rows - r0));
+        __syncthreads();  // the previous group's rows and statistics are no longer read
+        if (threadIdx.x < R) {
+            const bool v = static_cast<int>(threadIdx.x) < nr;
+            s_mu[threadIdx.x] = v ? mean[r0 + threadIdx.x] : 0.f;
+            s_rs[threadIdx.x] = v ? rstd[r0 + threadIdx.x] : 0.f;
+        }
+        if (warp == 0) {
+            const __nv_bfloat16* src[3] = {x, dy, dres};
+            __nv_bfloat16* dst[3] = {sx, sd, sr};
+            const __nv_bfloat16* vs[1] = {gamma};
+            __nv_bfloat16* vd[1] = {sg};
+            bulk_rows(&bar, src, dst, RES ? 3 : 2, vs, vd, it == 0 ? 1 : 0, r0, nr, width);
+        }
+        __syncthreads();  // s_mu / s_rs
+        mbar_wait(&bar, it & 1);
+        const bool valid = ri < nr;
+        const float mu = s_mu[ri], rs = s_rs[ri];
+        const __nv_bfloat16* xr = sx + ri * width;
+        const __nv_bfloat16* dr = sd + ri * width;
+        float s1 = 0.f, s2 = 0.f;
+        if (valid)
+            for (int c = (part * 32 + lane) * 8; c < width; c += W * 256) {
+                float xv[8], dv[8], g[8];
+                unpack8(lds16(xr + c), xv);
+                unpack8(lds16(dr + c), dv);
+                unpack8(lds16(sg + c), g);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const float gd = dv[u] * g[u];
+                    s1 += gd;
+                    s2 += gd * (xv[u] - mu) * rs;
+                }
+            }
+        s1 = warp_sum(s1);
+        s2 = warp_sum(s2);
+        if constexpr (W > 1) {
+            if (lane == 0) {
+                st[ri][part][0] = s1;
+                st[ri][part][1] = s2;
+            }
+            __syncthreads();
+            s1 = s2 = 0.f;
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                s1 += st[ri][w][0];
+                s2 += st[ri][w][1];
+            }
+        }
+        const float m1 = s1 / width, m2 = s2 / width;
+        if (valid) {
+            __nv_bfloat16* dxr = dx + (r0 + ri) * width;
+            for (int c = (part * 32 + lane) * 8; c < width; c += W * 256) {
+                float xv[8], dv[8], g[8], r[8];
+                unpack8(lds16(xr + c), xv);
+                unpack8(lds16(dr + c), dv);
+                unpack8(lds16(sg + c), g);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) r[u] = rs * (dv[u] * g[u] - m1 - (xv[u] - mu) * rs * m2);
+                if constexpr (RES) {
+                    float rv[8];
+                    unpack8(lds16(sr + ri * width + c), rv);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) r[u] += rv[u];
+                }
+                store8(dxr + c, r);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+            const int c = k * 2048 + threadIdx.x * 8;
+            if (c >= width) continue;
+            for (int r = 0; r < nr; ++r) {
+                float xv[8], dv[8];
+                unpack8(lds16(sx + r * width + c), xv);
+                unpack8(lds16(sd + r * width + c), dv);
+                const float m = s_mu[r], q = s_rs[r];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    pg[k][u] += dv[u] * (xv[u] - m) * q;
+                    pb[k][u] += dv[u];
+                }
+            }
+        }
+    }
+    float* wout = ws + static_cast<int64_t>(blockIdx.x) * 2 * width;
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+        const int c = k * 2048 + threadIdx.x * 8;
+        if (c >= width) continue;
+        *reinterpret_cast<float4*>(wout + c) = make_float4(pg[k][0], pg[k][1], pg[k][2], pg[k][3]);
+        *reinterpret_cast<float4*>(wout + c + 4) = make_float4(pg[k][4], pg[k][5], pg[k][6], pg[k][7]);
+        *reinterpret_cast<float4*>(wout + width + c) = make_float4(pb[k][0], pb[k][1], pb[k][2], pb[k][3]);
+        *reinterpret_cast<float4*>(wout + width + c + 4) = make_float4(pb[k][4], pb[k][5], pb[k][6], pb[k][7]);
+    }
+}
+
+// rows per block of the bulk kernels (8 / R warps per row); 0 = row too wide for them
+int ln_bulk_rows(int width) {
+    static const int mode = [] {
+        const char* e = getenv("BFPP_LN_BULK");  // A/B switch: 0 = register-resident kernels
+        return e ? atoi(e) : 1;
+    }();
+    if (!mode) return 0;
+    return width <= 2048 ? 8 : width <= 4096 ? 4 : width <= 8192 ? 2 : 0;
+}
+template <typename F>
+void ln_bulk_dispatch(int R, F&& f) {
+    switch (R) {
+        case 8: f(std::integral_constant<int, 8>{}); break;
+        case 4: f(std::integral_constant<int, 4>{}); break;
+        case 2: f(std::integral_constant<int, 2>{}); break;
+        default: f(std::integral_constant<int, 2>{}); break;
+    }
+}
+// raise a kernel's dynamic shared-memory limit once (host calls come from one thread per device)
+template <class K>
+void ln_smem_optin(K kernel) {
+    static std::set<const void*> done;
+    if (done.insert(reinterpret_cast<const void*>(kernel)).second)
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+}
+
 float* ln_workspace(size_t bytes) {
     // one workspace per device (the executor runs every LayerNorm backward on one stream)
     static thread_local float* ws[64] = {};
@@ -605,6 +886,19 @@ float* ln_workspace(size_t bytes) {
 void layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, float* mean, float* rstd, int rows,
                    int width, float eps, cudaStream_t st) {
     if (width % 8) throw std::runtime_error("layernorm: width must be a multiple of 8");
+    // forward: the register-resident kernels are as fast up to 4096 columns (scripts/ln_bench.py:
+    // 5.1 vs 5.3 us at 2048 x 2048); the bulk kernel takes the wider rows (11.0 vs 14.8 us at 5120)
+    if (const int R = width > 4096 ? ln_bulk_rows(width) : 0) {
+        ln_bulk_dispatch(R, [&](auto r) {
+            constexpr int RR = decltype(r)::value;
+            const size_t smem = static_cast<size_t>(RR + 2) * width * 2;
+            ln_smem_optin(ln_fwd_bulk_kernel<RR>);
+            ln_fwd_bulk_kernel<RR><<<(rows + RR - 1) / RR, 256, smem, st>>>(
+                static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(gamma),
+                static_cast<const __nv_bfloat16*>(beta), static_cast<__nv_bfloat16*>(y), mean, rstd, rows, width, eps);
+        });
+        return;
+    }
     const bool wide = ln_dispatch_wide(width, [&](auto w) {
         constexpr int W = decltype(w)::value;
         using Sh = MwShape<W>;
@@ -625,7 +919,7 @@ void layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, 
                                                   static_cast<__nv_bfloat16*>(y), mean, rstd, rows, width, eps);
 }
 
-int layernorm_bwd_launches(int width) { return width <= 4096 ? 2 : 3; }
+int layernorm_bwd_launches(int width) { return ln_bulk_rows(width) || width <= 4096 ? 2 : 3; }
 
 void layernorm_bwd(const void* dy, const void* x, const void* gamma, const float* mean, const float* rstd,
                    const void* dres, void* dx, float* dgamma, float* dbeta, int rows, int width, cudaStream_t st,
@@ -633,6 +927,27 @@ void layernorm_bwd(const void* dy, const void* x, const void* gamma, const float
     if (width % 8) throw std::runtime_error("layernorm: width must be a multiple of 8");
     auto DY = static_cast<const __nv_bfloat16*>(dy);
     auto X = static_cast<const __nv_bfloat16*>(x);
+    if (const int R = ln_bulk_rows(width)) {
+        int dev = 0, n_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+        const int parts = std::min((rows + R - 1) / R, 2 * n_sm);  // two resident blocks per SM
+        float* part = ln_workspace(static_cast<size_t>(parts) * 2 * width * sizeof(float));
+        ln_bulk_dispatch(R, [&](auto r) {
+            constexpr int RR = decltype(r)::value, CC = 8 / RR;
+            auto launch = [&](auto kernel, int n_src) {
+                const size_t smem = static_cast<size_t>(n_src * RR + 1) * width * 2;
+                ln_smem_optin(kernel);
+                kernel<<<parts, 256, smem, st>>>(DY, X, static_cast<const __nv_bfloat16*>(gamma), mean, rstd,
+                                                 static_cast<const __nv_bfloat16*>(dres),
+                                                 static_cast<__nv_bfloat16*>(dx), part, rows, width);
+            };
+            if (dres) launch(ln_bwd_bulk_kernel<RR, CC, true>, 3);
+            else launch(ln_bwd_bulk_kernel<RR, CC, false>, 2);
+        });
+        ln_partsum_kernel<<<(2 * width + 63) / 64, 256, 0, st>>>(part, parts, width, dgamma, dbeta, accumulate);
+        return;
+    }
     {
         int parts = 0;
         const bool wide = ln_dispatch_wide(width, [&](auto w) {

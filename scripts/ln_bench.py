@@ -31,7 +31,7 @@ def bench(fn, iters=10, reps=20):
     return ts[len(ts) // 2] * 1e3 / reps
 
 
-for rows, width in [(2048, 2048), (2048, 4096), (4096, 4096), (2048, 5120)]:
+for rows, width in [(2048, 2048), (8192, 2048), (2048, 4096), (4096, 4096), (2048, 5120), (2048, 8192)]:
     x = torch.randn(rows, width, device="cuda").bfloat16()
     g = torch.ones(width, device="cuda").bfloat16()
     b = torch.zeros(width, device="cuda").bfloat16()
