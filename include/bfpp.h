@@ -202,6 +202,10 @@ int bfpp_gemm_bf16_pair(const bfpp_gemm_args* a, const bfpp_gemm_args* b, void* 
  * stream_k = 0 off (default), 1 forced, -1 auto (only when the last tile wave leaves pairs idle).
  * Defaults come from BFPP_GEMM_MODE / BFPP_GEMM_BN2 / BFPP_GEMM_SK. */
 int bfpp_gemm_config(int32_t mode, int32_t bn2, int32_t stream_k);
+/* tile schedule of the persistent 2-CTA GEMM: 0 static (tile t, t + pairs, ...; default), 1 dynamic
+ * (a pair's later tiles come from a per-stream device counter, so a pair that starts late or runs
+ * slow takes fewer tiles; CUDA-graph captures always use the static schedule). BFPP_GEMM_DYN. */
+int bfpp_gemm_schedule(int32_t dynamic);
 /* attention forward: query tiles per CTA (0 auto, 1, 2 = two tiles sharing K/V, ping-pong softmax) */
 int bfpp_attention_config(int32_t fwd_tiles);
 /* persistent GEMM grids use at most n SMs (0 = all): for streams confined to an SM partition */

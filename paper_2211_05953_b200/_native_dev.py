@@ -21,6 +21,7 @@ class GemmArgsC(C.Structure):
 PROTOS: dict = {
     "bfpp_gemm_bf16": (C.c_int, [C.POINTER(GemmArgsC), _P]),
     "bfpp_gemm_config": (C.c_int, [C.c_int32, C.c_int32, C.c_int32]),
+    "bfpp_gemm_schedule": (C.c_int, [C.c_int32]),
     "bfpp_gemm_sm_limit": (C.c_int, [C.c_int32]),
     "bfpp_attention_config": (C.c_int, [C.c_int32]),
     "bfpp_gemm_bf16_pair": (C.c_int, [C.POINTER(GemmArgsC), C.POINTER(GemmArgsC), _P]),

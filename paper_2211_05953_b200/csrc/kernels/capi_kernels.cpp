@@ -44,6 +44,13 @@ int bfpp_gemm_config(int32_t mode, int32_t bn2, int32_t stream_k) {
     });
 }
 
+int bfpp_gemm_schedule(int32_t dynamic) {
+    return guarded([&] {
+        if (dynamic != 0 && dynamic != 1) throw SpecError("gemm_schedule: dynamic must be 0 or 1");
+        bfpp::gemm_dyn = dynamic;
+    });
+}
+
 int bfpp_attention_config(int32_t fwd_tiles) {
     return guarded([&] {
         if (fwd_tiles < 0 || fwd_tiles > 2) throw SpecError("attention_config: fwd_tiles must be 0, 1 or 2");

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 #include <curand_kernel.h>
 
+#include <cstdlib>
 #include <stdexcept>
 
 #include "kernels.hpp"
@@ -338,7 +339,12 @@ void adam_update(float* p, float* m, float* v, float* g, void* w16, int64_t n, f
         return true;
     }();
     (void)once;
-    const int64_t blocks = (n / 4 + kAdamThreads - 1) / kAdamThreads;
+    static const int64_t grid_cap = [] {  // experiment knob: grid-stride over at most this many blocks
+        const char* e = getenv("BFPP_ADAM_GRID");
+        return e ? static_cast<int64_t>(atoll(e)) : int64_t{0};
+    }();
+    int64_t blocks = (n / 4 + kAdamThreads - 1) / kAdamThreads;
+    if (grid_cap > 0 && blocks > grid_cap) blocks = grid_cap;
     adam_kernel<<<static_cast<unsigned>(blocks > 0 ? blocks : 1), kAdamThreads, 0, st>>>(
         p, m, v, g, static_cast<__nv_bfloat16*>(w16), n, lr, b1, b2, eps, wd, bc1, bc2, zero_grad);
 }

@@ -44,6 +44,7 @@ extern int gemm_pair;  // grouped pair launches (default 1; BFPP_GEMM_PAIR=0 dis
 extern int gemm_bn2;   // 2-CTA pair-tile width: 0 default (256), 128 opt-in
 extern int gemm_pdl;   // programmatic dependent launch of the GEMM kernels (default 0, BFPP_GEMM_PDL=1)
 extern int gemm_sk;    // stream-K in the 2-CTA kernel: -1 auto, 0 off, 1 forced (BFPP_GEMM_SK)
+extern int gemm_dyn;   // dynamic tile schedule in the 2-CTA kernel (default 0, BFPP_GEMM_DYN=1)
 
 // Host-side launch counters per kernel variant (process-wide, reset by bfpp_kernel_variant_reset):
 // lets the composed-step parity tests assert which production paths actually ran.

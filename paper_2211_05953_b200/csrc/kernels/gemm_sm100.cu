@@ -128,6 +128,10 @@ struct SkArgs {
     float* ws;    // [pair][cta][128][256] f32 partials (nullptr: data-parallel tiles)
     int* flags;   // [pair][cta] epoch of the last published partial
     int epoch;
+    // dynamic tile scheduler (data-parallel tiles): a pair's first tile is its index, every later
+    // tile is n_pairs + (atomicAdd(tctr, 1) - tbase); nullptr = static t += n_pairs schedule
+    unsigned long long* tctr;
+    unsigned long long tbase;
 };
 
 struct Seg {
@@ -497,6 +501,32 @@ struct Smem2 {
     static constexpr int kBytes = kBarOffset + 256 + 1024;
 };
 
+// Per-CTA timing probe (scripts/gemm_trace.cu builds this file with BFPP_GEMM_TRACE): start and
+// end (%globaltimer, ns), tiles drained and SM id of every CTA of the last gemm2 launch.
+#ifdef BFPP_GEMM_TRACE
+__device__ unsigned long long g_gemm_trace[512][4];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define GTRACE_START()                                             \
+    if (threadIdx.x == 64) {                                       \
+        unsigned smid;                                             \
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));          \
+        g_gemm_trace[blockIdx.x][0] = gtimer();                    \
+        g_gemm_trace[blockIdx.x][3] = smid;                        \
+    }
+#define GTRACE_END(n)                                              \
+    if (threadIdx.x == 64) {                                       \
+        g_gemm_trace[blockIdx.x][1] = gtimer();                    \
+        g_gemm_trace[blockIdx.x][2] = static_cast<unsigned long long>(n); \
+    }
+#else
+#define GTRACE_START()
+#define GTRACE_END(n)
+#endif
+
 template <int BN, int A_MN, int B_MN, bool SK, bool GROUP>
 __global__ void __maxnreg__(96)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -511,6 +541,11 @@ __global__ void __maxnreg__(96)
     uint64_t* tfull = empty + kStages2;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    // dynamic schedule: a 4-deep ring of tile indices the leader's producer fills for the pair
+    // (its own MMA and epilogue warps, the peer's producer and epilogue warps)
+    uint64_t* tq_full = tempty + 3;
+    uint64_t* tq_empty = tq_full + 4;
+    int* tq = reinterpret_cast<int*>(tq_empty + 4);
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
@@ -524,6 +559,7 @@ __global__ void __maxnreg__(96)
     const int num_tiles = tiles0 + (GROUP ? m_tiles1 * ((p2.N + BN - 1) / BN) : 0);
     const int nk = nk0;  // stream-K (never grouped) splits the first problem's k-blocks
     const bool use_sk = SK && !GROUP && BN == 256 && sk.ws != nullptr;  // stream-K instantiation only
+    const bool dyn = !use_sk && sk.tctr != nullptr;
     // problem of global tile t: tensor maps, shape, epilogue, tile index within the problem
     struct Prob {
         const CUtensorMap *A, *B, *D;
@@ -562,6 +598,10 @@ __global__ void __maxnreg__(96)
             ptx::mbar_init(&tfull[b], 1);
             ptx::mbar_init(&tempty[b], 2 * kEpiWarps);
         }
+        for (int b = 0; b < 4; ++b) {
+            ptx::mbar_init(&tq_full[b], 1);
+            ptx::mbar_init(&tq_empty[b], 2 * kEpiWarps + 2);  // both CTAs' epilogue warps, MMA, peer producer
+        }
         ptx::fence_barrier_init();
     }
     if (warp == 1) ptx::tmem_alloc_2sm<2 * BN>(tmem_slot);
@@ -572,6 +612,17 @@ __global__ void __maxnreg__(96)
     // PDL: everything above overlapped the previous kernel's tail; inputs/outputs are touched below
     ptx::griddep_wait();
     ptx::griddep_launch_dependents();
+    GTRACE_START();
+    // tile-ring consumer: index of ring entry i (every consumer reads every entry once, in order)
+    auto read_tile = [&](int i) -> int {
+        const int slot = i & 3;
+        ptx::mbar_wait_cluster(&tq_full[slot], (i >> 2) & 1);
+        const int t = *reinterpret_cast<volatile int*>(&tq[slot]);
+        // the slot is rewritten four tiles later; a release here would hold the MMA thread until
+        // its in-flight MMAs drain
+        ptx::mbar_arrive_cluster_relaxed(ptx::mapa_shared(ptx::smem_u32(&tq_empty[slot]), 0));
+        return t;
+    };
 
     if (warp == 0) {
         if (lane == 0) {
@@ -580,7 +631,37 @@ __global__ void __maxnreg__(96)
             uint32_t phase = 0;
             WorkIter wi(use_sk, pair, n_pairs, num_tiles, nk);
             Seg g;
-            while (wi.next(g)) {
+            int qi = 0;
+            unsigned long long fetched = 0;  // counter value drawn one tile ahead (latency hidden)
+            // leader: take the next tile (static first tile, then the shared counter) and publish
+            // it to both CTAs' rings; peer: read it from its own ring
+            auto next = [&](Seg& sg) -> bool {
+                if (!dyn) return wi.next(sg);
+                int t;
+                if (rank == 0) {
+                    if (qi == 0) {
+                        t = pair < num_tiles ? pair : num_tiles;
+                    } else {
+                        t = n_pairs + static_cast<int>(fetched - sk.tbase);
+                        if (t > num_tiles) t = num_tiles;
+                    }
+                    // draw the following tile now; its value is first used at the next call
+                    if (t < num_tiles) fetched = atomicAdd(sk.tctr, 1ull);
+                    const int slot = qi & 3;
+                    ptx::mbar_wait_cluster(&tq_empty[slot], ((qi >> 2) & 1) ^ 1);
+                    tq[slot] = t;
+                    ptx::st_shared_cluster_u32(ptx::mapa_shared(ptx::smem_u32(&tq[slot]), 1), static_cast<uint32_t>(t));
+                    ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tq_full[slot]), 0));
+                    ptx::mbar_arrive_cluster(ptx::mapa_shared(ptx::smem_u32(&tq_full[slot]), 1));
+                    ++qi;
+                } else {
+                    t = read_tile(qi++);
+                }
+                if (t >= num_tiles) return false;
+                sg = {t, 0, nk};
+                return true;
+            };
+            while (next(g)) {
                 const Prob pb = prob(g.tile);
                 if (!use_sk) g.kb1 = pb.nk;
                 const int t = pb.t;
@@ -621,7 +702,14 @@ __global__ void __maxnreg__(96)
             int it = 0;
             WorkIter wi(use_sk, pair, n_pairs, num_tiles, nk);
             Seg g;
-            for (; wi.next(g); ++it) {
+            auto next = [&](Seg& sg) -> bool {
+                if (!dyn) return wi.next(sg);
+                const int t = read_tile(it);
+                if (t >= num_tiles) return false;
+                sg = {t, 0, nk};
+                return true;
+            };
+            for (; next(g); ++it) {
                 if (!use_sk) g.kb1 = prob(g.tile).nk;
                 const int acc = it & 1;
                 const uint32_t acc_phase = (it >> 1) & 1;
@@ -660,7 +748,16 @@ __global__ void __maxnreg__(96)
         const int lr = q * 32 + lane;  // this thread's accumulator row within the CTA's 128 rows
         WorkIter wi(use_sk, pair, n_pairs, num_tiles, nk);
         Seg g;
-        for (; wi.next(g); ++it) {
+        auto next = [&](Seg& sg) -> bool {
+            if (!dyn) return wi.next(sg);
+            int t = 0;
+            if (lane == 0) t = read_tile(it);
+            t = __shfl_sync(0xffffffffu, t, 0);
+            if (t >= num_tiles) return false;
+            sg = {t, 0, nk};
+            return true;
+        };
+        for (; next(g); ++it) {
             const Prob pb = prob(g.tile);
             if (!use_sk) g.kb1 = pb.nk;
             const EpiArgs& ep_t = *pb.ep;
@@ -740,6 +837,7 @@ __global__ void __maxnreg__(96)
             }
         }
         if (lane == 0) ptx::bulk_wait<0>();
+        GTRACE_END(it);
     }
     ptx::tc_fence_before();
     ptx::cluster_sync();
@@ -809,6 +907,30 @@ SkWorkspace& sk_workspace(cudaStream_t st, int pairs) {
     return w;
 }
 
+// Dynamic-schedule tile counter, one per (device, stream): a launch that fetches draws exactly
+// `tiles` values from it (every pair's failing fetch included), so the host knows each launch's
+// base without resetting the counter. GEMMs of one stream run in order (PDL launches fetch only
+// after griddepcontrol.wait), so launches never interleave on a counter.
+struct TileCounter {
+    unsigned long long* ctr = nullptr;
+    unsigned long long next = 0;
+};
+TileCounter* tile_counter(cudaStream_t st) {
+    static std::map<std::pair<int, cudaStream_t>, TileCounter> all;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone)
+        return nullptr;  // a captured launch replays with a fixed base: static schedule
+    int dev = 0;
+    cudaGetDevice(&dev);
+    TileCounter& c = all[{dev, st}];
+    if (!c.ctr) {
+        if (cudaMalloc(&c.ctr, sizeof(unsigned long long)) != cudaSuccess)
+            throw std::runtime_error("gemm: tile counter allocation failed");
+        cudaMemset(c.ctr, 0, sizeof(unsigned long long));
+    }
+    return &c;
+}
+
 template <int BN, int A_MN, int B_MN>
 void launch2(const GemmArgs& g, cudaStream_t st, const GemmArgs* second = nullptr) {
     auto maps = [](const GemmArgs& a, CUtensorMap& ta, CUtensorMap& tb, CUtensorMap& td) {
@@ -845,7 +967,7 @@ void launch2(const GemmArgs& g, cudaStream_t st, const GemmArgs* second = nullpt
     if (second) tiles += static_cast<int>(((second->M + 255) / 256) * ((second->N + BN - 1) / BN));
     const int nk = static_cast<int>((g.K + BK - 1) / BK);
     int pairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
-    SkArgs sk{nullptr, nullptr, 0};
+    SkArgs sk{nullptr, nullptr, 0, nullptr, 0};
     {
         // stream-K when the data-parallel tile waves leave pairs idle and every pair's range is at
         // least half a tile (so a tile has at most two producers)
@@ -856,10 +978,21 @@ void launch2(const GemmArgs& g, cudaStream_t st, const GemmArgs* second = nullpt
         const bool want = !second && (gemm_sk == 1 || (gemm_sk < 0 && eff < 0.92));
         if (want && BN == 256 && total / all >= (nk + 1) / 2 && nk >= 2) {
             SkWorkspace& w = sk_workspace(st, all);
-            sk = SkArgs{w.ws, w.flags, ++w.epoch};
+            sk = SkArgs{w.ws, w.flags, ++w.epoch, nullptr, 0};
             pairs = all;
         }
     }
+    // dynamic tiles (opt-in) when a pair runs more than one tile: a pair that starts late (its SMs
+    // still busy with another stream's blocks) or runs slow takes fewer tiles. scripts/gemm_trace.py,
+    // 2048 x 8192 x 2048 launched while the optimizer saturates the GPU: 1224 vs 969 TF/s (one
+    // cluster of the static grid starts ~40 us late); alone 1425 vs 1535 TF/s (the tile ring costs
+    // ~1 us per tile); in the N = 1 step GEMMs 1006 vs 1037 TF/s, so static stays the default.
+    if (!sk.ws && gemm_dyn && tiles > pairs)
+        if (TileCounter* c = tile_counter(st)) {
+            sk.tctr = c->ctr;
+            sk.tbase = c->next;
+            c->next += static_cast<unsigned long long>(tiles);
+        }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * pairs);
     cfg.blockDim = dim3(kThreads);
@@ -894,6 +1027,7 @@ int gemm_sm_limit = 0;  // > 0: persistent grids sized to this many SMs (a green
 int gemm_pdl = 0;    // programmatic dependent launch (BFPP_GEMM_PDL=1): measured no gain in-step (optimizer co-running)
 int gemm_bn2 = 0;    // 2-CTA pair-tile width: 0 / 256 default, 128 opt-in (BFPP_GEMM_BN2; tests)
 int gemm_pair = 1;   // grouped launches of independent GEMM pairs (BFPP_GEMM_PAIR=0: two launches)
+int gemm_dyn = 0;    // dynamic tile schedule of the 2-CTA kernel (opt-in: BFPP_GEMM_DYN=1, bfpp_gemm_schedule)
 
 static bool env_read = false;
 
@@ -911,6 +1045,8 @@ static void read_env() {
     if (const char* e = getenv("BFPP_GEMM_PDL")) gemm_pdl = atoi(e);
     if (const char* e = getenv("BFPP_GEMM_SK")) gemm_sk = atoi(e);
     if (const char* e = getenv("BFPP_GEMM_PAIR")) gemm_pair = atoi(e);
+    if (const char* e = getenv("BFPP_GEMM_DYN")) gemm_dyn = atoi(e);
+    if (const char* e = getenv("BFPP_GEMM_SMS")) gemm_sm_limit = atoi(e);
     env_read = true;
 }
 

@@ -89,6 +89,11 @@ def gemm_config(mode: int = -1, bn2: int = 0, stream_k: int = -1):
     _check(_nat.lib().bfpp_gemm_config(mode, bn2, stream_k))
 
 
+def gemm_schedule(dynamic: bool = False):
+    """Tile schedule of the persistent 2-CTA GEMM: static (default) or dynamic (device tile counter)."""
+    _check(_nat.lib().bfpp_gemm_schedule(1 if dynamic else 0))
+
+
 def attention_fwd(qkv, batch, seq, heads, head_dim=128):
     T = batch * seq
     o = torch.empty(T, heads * head_dim, device=qkv.device, dtype=torch.bfloat16)

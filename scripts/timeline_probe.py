@@ -33,7 +33,7 @@ for t in ex.graph.tasks:
         rows.append((s[t.id], e[t.id], t.kind.name, t.stage, t.micro_batch, t.id))
 rows.sort()
 for a, b, k, st, mb, i in ([] if args.quiet else rows):
-    print(f"{a:8.3f} {b:8.3f} {b - a:7.3f}  {k:12s} stage {st} mb {mb} id {i}")
+    print(f"{a * 1e3:9.3f} {b * 1e3:9.3f} {(b - a) * 1e3:8.3f} ms  {k:12s} stage {st} mb {mb} id {i}")
 e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
 stream = torch.cuda.ExternalStream(ex.stream_handle)
 ex.set_flags(False, False)

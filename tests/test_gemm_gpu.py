@@ -20,17 +20,21 @@ def _close(got, ref, rtol):
     assert err <= rtol * scale, (err, scale)
 
 
-# (mode, bn2, stream_k): defaults (stream-K off); one-CTA tiles; two-CTA 256x128 and 256x256 pair tiles (forced),
-# data-parallel and stream-K (forced: a k-split wherever every pair gets >= half a tile)
-VARIANTS = [(-1, 0, 0), (-1, 0, -1), (1, 0, 0), (2, 128, 0), (2, 256, 0), (2, 256, 1)]
+# (mode, bn2, stream_k, dynamic): defaults (stream-K off); one-CTA tiles; two-CTA 256x128 and 256x256 pair
+# tiles (forced), data-parallel and stream-K (forced: a k-split wherever every pair gets >= half a tile);
+# the dynamic tile schedule (device counter + per-pair tile ring) with both pair-tile widths
+VARIANTS = [(-1, 0, 0, 0), (-1, 0, -1, 0), (1, 0, 0, 0), (2, 128, 0, 0), (2, 256, 0, 0), (2, 256, 1, 0),
+            (-1, 0, 0, 1), (2, 128, 0, 1)]
 
 
-@pytest.fixture(params=VARIANTS, ids=lambda v: f"mode{v[0]}-bn{v[1]}-sk{v[2]}")
+@pytest.fixture(params=VARIANTS, ids=lambda v: f"mode{v[0]}-bn{v[1]}-sk{v[2]}-dyn{v[3]}")
 def variant(request, cuda_device):
     ops = _ops()
-    ops.gemm_config(*request.param)
+    ops.gemm_config(*request.param[:3])
+    ops.gemm_schedule(bool(request.param[3]))
     yield request.param
     ops.gemm_config(-1, 0, 0)  # the library defaults
+    ops.gemm_schedule(False)
 
 
 @pytest.mark.parametrize("a_mn", [False, True])
@@ -94,9 +98,13 @@ def test_gemm_strided_views(cuda_device):
 @pytest.mark.parametrize("shapes", [((512, 768, 256), (768, 512, 384)), ((2048, 2048, 512), (6144, 2048, 512)),
                                     ((256, 8192, 128), (8192, 256, 128))])
 @pytest.mark.parametrize("epi", ["f32_acc", "bf16"])
-def test_gemm_pair_matches_separate_launches(cuda_device, shapes, epi):
-    """Grouped pair launch (one tile space) == two ordinary launches, bit for bit (same per-tile math)."""
+@pytest.mark.parametrize("dyn", [False, True], ids=["static", "dynamic"])
+def test_gemm_pair_matches_separate_launches(cuda_device, shapes, epi, dyn, request):
+    """Grouped pair launch (one tile space) == two ordinary launches, bit for bit (same per-tile math),
+    under the static and the dynamic tile schedule."""
     ops = _ops()
+    ops.gemm_schedule(dyn)
+    request.addfinalizer(lambda: ops.gemm_schedule(False))
     g = torch.Generator(device="cuda").manual_seed(11)
     probs = []
     for M, N, K in shapes:  # weight-gradient form: A = dY^T, B = X^T (both MN-major)
