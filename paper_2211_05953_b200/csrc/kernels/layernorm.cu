@@ -928,9 +928,11 @@ void layernorm_bwd(const void* dy, const void* x, const void* gamma, const float
     auto DY = static_cast<const __nv_bfloat16*>(dy);
     auto X = static_cast<const __nv_bfloat16*>(x);
     if (const int R = ln_bulk_rows(width)) {
-        int dev = 0, n_sm = 0;
+        static int sm_of[64] = {};  // SM count per device, queried once
+        int dev = 0;
         cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+        if (!sm_of[dev & 63]) cudaDeviceGetAttribute(&sm_of[dev & 63], cudaDevAttrMultiProcessorCount, dev);
+        const int n_sm = sm_of[dev & 63] > 0 ? sm_of[dev & 63] : 148;
         const int parts = std::min((rows + R - 1) / R, 2 * n_sm);  // two resident blocks per SM
         float* part = ln_workspace(static_cast<size_t>(parts) * 2 * width * sizeof(float));
         ln_bulk_dispatch(R, [&](auto r) {
