@@ -492,7 +492,10 @@ __global__ void __maxnreg__(96)
 // BN = 128 (each CTA stages 64 rows of B, 24 KB/stage, 7 stages): opt-in variant (see gemm_bf16).
 template <int BN>
 struct Smem2 {
-    static constexpr int kStages = BN == 256 ? 5 : 7;
+#ifndef BFPP_GEMM2_STAGES
+#define BFPP_GEMM2_STAGES 5  // experiments build other depths (scripts/gemm_stages.sh)
+#endif
+    static constexpr int kStages = BN == 256 ? BFPP_GEMM2_STAGES : 7;
     static constexpr int kABytes = 128 * BK * 2;
     static constexpr int kBBytes = (BN / 2) * BK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
