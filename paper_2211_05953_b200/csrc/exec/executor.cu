@@ -267,6 +267,13 @@ struct Executor::Impl {
     cudaEvent_t ev_opt[2] = {};  // segment-wise optimizer hand-off (compute, wgrad stream)
     std::vector<cudaEvent_t> rec_ev[2];  // DP_FS: per weight slot, one event per all-gathered segment
     std::vector<cudaEvent_t> done_g;  // per Bwd task: its gradients are complete (compute + wgrad streams)
+    // Deferred weight gradients: a backward whose input gradient goes to another device runs its
+    // data-gradient chain first and records done_dx, so the send (and the peer's backward) starts
+    // before this stage's weight-gradient GEMMs, which then fill the wait for the next task.
+    // Per-layer gradient scratch of one stage keeps the chain's outputs until those GEMMs run.
+    bool defer_wgrad = false;
+    std::vector<cudaEvent_t> done_dx;  // per deferring Bwd task: its input gradient is ready
+    std::vector<bf16*> dpre_d, dqkv_d, gmid_d, gout_d;  // [layer of the stage]
     float *dq_acc = nullptr, *delta = nullptr;
     int32_t *inputs = nullptr, *labels = nullptr;
     float *row_loss = nullptr, *loss_dev = nullptr, *loss_pinned = nullptr;
@@ -586,6 +593,15 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
         I.dpre_s[k] = I.alloc<bf16>(static_cast<size_t>(T * mlp), M_SCRATCH);
         I.dqkv_s[k] = I.alloc<bf16>(3 * Th, M_SCRATCH);
     }
+    I.defer_wgrad = p_ >= 2 && !I.wgrad_stream && !o_.recompute;
+    if (const char* e = getenv("BFPP_DEFER_WGRAD")) I.defer_wgrad = I.defer_wgrad && atoi(e) != 0;  // A/B switch
+    if (I.defer_wgrad)
+        for (i64 j = 0; j < pl_.layers_per_stage; ++j) {
+            I.dpre_d.push_back(I.alloc<bf16>(static_cast<size_t>(T * mlp), M_SCRATCH));
+            I.dqkv_d.push_back(I.alloc<bf16>(3 * Th, M_SCRATCH));
+            I.gmid_d.push_back(I.alloc<bf16>(Th, M_SCRATCH));
+            I.gout_d.push_back(I.alloc<bf16>(Th, M_SCRATCH));
+        }
     I.dq_acc = I.alloc<float>(Th, M_SCRATCH);
     I.delta = I.alloc<float>(static_cast<size_t>(T * H), M_SCRATCH);
     I.inputs = I.alloc<int32_t>(static_cast<size_t>(c_.n_mb * T), M_SCRATCH);
@@ -723,6 +739,7 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
     const size_t n = graph_.tasks.size();
     I.done.assign(n, nullptr);
     I.done_g.assign(n, nullptr);
+    I.done_dx.assign(n, nullptr);
     I.t_start.assign(n, nullptr);
     I.t_end.assign(n, nullptr);
     I.task_c.assign(n, -1);
@@ -734,6 +751,8 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
         CK(cudaEventCreateWithFlags(&I.done[static_cast<size_t>(te.id)], cudaEventDisableTiming));
         if (t.kind == TaskKind::Bwd)
             CK(cudaEventCreateWithFlags(&I.done_g[static_cast<size_t>(te.id)], cudaEventDisableTiming));
+        if (t.kind == TaskKind::Bwd && I.defer_wgrad && t.stage > 0 && pl_.device_of(t.stage - 1) != pp_rank_)
+            CK(cudaEventCreateWithFlags(&I.done_dx[static_cast<size_t>(te.id)], cudaEventDisableTiming));
     }
     set_flags(o.record_timeline, o.profile_kernels);
     CK(cudaEventCreate(&I.origin));
@@ -779,6 +798,8 @@ Executor::~Executor() {
     for (auto& evs : I.rec_ev)
         for (auto e : evs)
             if (e) cudaEventDestroy(e);
+    for (auto e : I.done_dx)
+        if (e) cudaEventDestroy(e);
     for (auto e : I.done_g)
         if (e) cudaEventDestroy(e);
     for (auto& ls : I.local)
@@ -1024,9 +1045,13 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
                 seg_wait = true;
                 continue;
             }
-            // gradient consumers (Reduce) need the wgrad stream's half of a backward task too
+            // gradient consumers (Reduce) need the wgrad stream's half of a backward task too; a
+            // send of a deferring backward needs only its data-gradient chain
             const bool grads = dk == TaskKind::Bwd && t.kind == TaskKind::Reduce;
-            CK(cudaStreamWaitEvent(st, grads ? I.done_g[static_cast<size_t>(d)] : I.done[static_cast<size_t>(d)], 0));
+            cudaEvent_t ev = grads ? I.done_g[static_cast<size_t>(d)] : I.done[static_cast<size_t>(d)];
+            if (t.kind == TaskKind::Transfer && dk == TaskKind::Bwd && I.done_dx[static_cast<size_t>(d)])
+                ev = I.done_dx[static_cast<size_t>(d)];
+            CK(cudaStreamWaitEvent(st, ev, 0));
         }
         // wait for the all-gather of the weight segment that holds stage-vector offset `off`
         auto need_weights = [&](const LocalStage& ls, int64_t off) {
@@ -1089,6 +1114,15 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
             const bool early = te.unit_end_bwd && ls.w16_shard != nullptr && ls.seg.size() > 2;
             const bool guard = te.first_in_unit && I.gbuf != nullptr;
             const size_t nl = L.layers.size();
+            // deferred weight gradients: chain first, then (after done_dx) the weight-gradient GEMMs
+            // and the per-segment optimizer / reduce-scatter work in the original order
+            const bool defer = I.done_dx[static_cast<size_t>(te.id)] != nullptr;
+            struct LaterLayer {
+                size_t li;
+                const bf16 *g, *dpre, *gmid, *dqkv;
+            };
+            std::vector<LaterLayer> later;
+            bool head_later = false;
             // end of layer li's parameters in the stage vector (the last layer of a non-last stage
             // runs to the padded end; n_dp == 1 here for the optimizer segments, so shard = stage)
             auto layer_end = [&](size_t li) -> int64_t {
@@ -1117,13 +1151,17 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
                 G(st, T, h, V, a.logits, V, 0, W + L.head, h, 1, I.tmp_h, h, GEMM_EPI_BF16);
                 CK(cudaEventRecord(I.ev_a[0], st));  // logits/lnf are persistent; only ordering matters
                 CK(cudaStreamWaitEvent(ws, I.ev_a[0], 0));
-                G(ws, V, h, T, a.logits, V, 1, a.lnf, h, 1, G_ + L.head, h, GEMM_EPI_F32, nullptr, 0, nullptr, 0, acc);
+                if (defer)
+                    head_later = true;
+                else
+                    G(ws, V, h, T, a.logits, V, 1, a.lnf, h, 1, G_ + L.head, h, GEMM_EPI_F32, nullptr, 0, nullptr, 0,
+                      acc);
                 wait_wgrad_latest();  // g_head was last read by an earlier layer's wgrad
                 LNB(st, I.tmp_h, a.out, W + L.lnf_g, a.muf, a.rsf, nullptr, I.g_head, G_ + L.lnf_g, G_ + L.lnf_b,
                     acc);
                 g = I.g_head;
-                if (seg_opt) adam_segment(ls, st, ws, L.lnf_g, ls.shard_n);
-                if (early) early_segment(ls, st, ws, L.lnf_g, te.reduce_first_unit, te.last_unit_bwd);
+                if (!defer && seg_opt) adam_segment(ls, st, ws, L.lnf_g, ls.shard_n);
+                if (!defer && early) early_segment(ls, st, ws, L.lnf_g, te.reduce_first_unit, te.last_unit_bwd);
             } else {
                 g = a.gin;
             }
@@ -1146,15 +1184,17 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
                     G(st, T, mlp, h, x.ln2, h, 0, W + P.fc1, h, 0, x.act, mlp, GEMM_EPI_GELU, nullptr, 0, x.pre, mlp);
                 }
                 if (guard) guard_grads(ls, st, ws, P.ln1_g, layer_end(li));
-                bf16 *gmid = I.gmid_s[k], *dpre = I.dpre_s[k], *dqkv = I.dqkv_s[k];
-                bf16* gnext = (li == 0 && !L.first) ? a.gout : I.gout_s[k];
+                bf16 *gmid = defer ? I.gmid_d[li] : I.gmid_s[k], *dpre = defer ? I.dpre_d[li] : I.dpre_s[k],
+                     *dqkv = defer ? I.dqkv_d[li] : I.dqkv_s[k];
+                bf16* gnext = (li == 0 && !L.first) ? a.gout : (defer ? I.gout_d[li] : I.gout_s[k]);
                 // MLP: x_out = x_mid + gelu(ln2 W1^T) W2^T
                 G(st, T, mlp, h, g, h, 0, W + P.fc2, mlp, 1, dpre, mlp, GEMM_EPI_DGELU, x.pre, mlp);
                 CK(cudaEventRecord(I.ev_a[k], st));
                 CK(cudaStreamWaitEvent(ws, I.ev_a[k], 0));
                 // weight gradients of fc2 and fc1: independent, one grouped launch
-                G2(ws, {h, mlp, T, g, h, 1, x.act, mlp, 1, G_ + P.fc2, mlp},
-                   {mlp, h, T, dpre, mlp, 1, x.ln2, h, 1, G_ + P.fc1, h}, acc);
+                if (!defer)
+                    G2(ws, {h, mlp, T, g, h, 1, x.act, mlp, 1, G_ + P.fc2, mlp},
+                       {mlp, h, T, dpre, mlp, 1, x.ln2, h, 1, G_ + P.fc1, h}, acc);
                 G(st, T, h, mlp, dpre, mlp, 0, W + P.fc1, h, 1, I.tmp_h, h, GEMM_EPI_BF16);
                 LNB(st, I.tmp_h, x.x_mid, W + P.ln2_g, x.mu2, x.rs2, g, gmid, G_ + P.ln2_g, G_ + P.ln2_b, acc);
                 // attention: x_mid = x_in + attn(ln1 Wqkv^T) Wo^T
@@ -1164,16 +1204,39 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
                 });
                 CK(cudaEventRecord(I.ev_b[k], st));
                 CK(cudaStreamWaitEvent(ws, I.ev_b[k], 0));
-                G2(ws, {h, h, T, gmid, h, 1, x.o, h, 1, G_ + P.o, h}, {3 * h, h, T, dqkv, 3 * h, 1, x.ln1, h, 1, G_ + P.qkv, h},
-                   acc);
+                if (defer)
+                    later.push_back({li, g, dpre, gmid, dqkv});
+                else
+                    G2(ws, {h, h, T, gmid, h, 1, x.o, h, 1, G_ + P.o, h},
+                       {3 * h, h, T, dqkv, 3 * h, 1, x.ln1, h, 1, G_ + P.qkv, h}, acc);
                 CK(cudaEventRecord(I.ev_wg[k], ws));
                 G(st, T, h, 3 * h, dqkv, 3 * h, 0, W + P.qkv, h, 1, I.tmp_h, h, GEMM_EPI_BF16);
                 // gnext (set k) was last read as g_in by the wgrad of layer lc-1
                 if (gnext == I.gout_s[k] && lc >= 1) CK(cudaStreamWaitEvent(st, I.ev_wg[(lc - 1) & 1], 0));
                 LNB(st, I.tmp_h, x.x_in, W + P.ln1_g, x.mu1, x.rs1, gmid, gnext, G_ + P.ln1_g, G_ + P.ln1_b, acc);
                 g = gnext;
-                if (seg_opt) adam_segment(ls, st, ws, P.ln1_g, layer_end(li));
-                if (early) early_segment(ls, st, ws, P.ln1_g, te.reduce_first_unit, te.last_unit_bwd);
+                if (!defer && seg_opt) adam_segment(ls, st, ws, P.ln1_g, layer_end(li));
+                if (!defer && early) early_segment(ls, st, ws, P.ln1_g, te.reduce_first_unit, te.last_unit_bwd);
+            }
+            if (defer) {
+                // the input gradient (a.gout) is final: the send may start; then the weight gradients
+                CK(cudaEventRecord(I.done_dx[static_cast<size_t>(te.id)], st));
+                if (head_later) {
+                    G(ws, V, h, T, a.logits, V, 1, a.lnf, h, 1, G_ + L.head, h, GEMM_EPI_F32, nullptr, 0, nullptr, 0,
+                      acc);
+                    if (seg_opt) adam_segment(ls, st, ws, L.lnf_g, ls.shard_n);
+                    if (early) early_segment(ls, st, ws, L.lnf_g, te.reduce_first_unit, te.last_unit_bwd);
+                }
+                for (const LaterLayer& d : later) {
+                    const LayerParams& P = L.layers[d.li];
+                    const LayerActs& x = a.layers[d.li];
+                    G2(ws, {h, mlp, T, d.g, h, 1, x.act, mlp, 1, G_ + P.fc2, mlp},
+                       {mlp, h, T, d.dpre, mlp, 1, x.ln2, h, 1, G_ + P.fc1, h}, acc);
+                    G2(ws, {h, h, T, d.gmid, h, 1, x.o, h, 1, G_ + P.o, h},
+                       {3 * h, h, T, d.dqkv, 3 * h, 1, x.ln1, h, 1, G_ + P.qkv, h}, acc);
+                    if (seg_opt) adam_segment(ls, st, ws, P.ln1_g, layer_end(d.li));
+                    if (early) early_segment(ls, st, ws, P.ln1_g, te.reduce_first_unit, te.last_unit_bwd);
+                }
             }
             if (L.first && guard) guard_grads(ls, st, ws, 0, L.layers[0].ln1_g);
             if (L.first && acc == 0) {  // scatter-added gradients need a zeroed start
