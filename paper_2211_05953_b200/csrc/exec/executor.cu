@@ -272,6 +272,14 @@ struct Executor::Impl {
     // before this stage's weight-gradient GEMMs, which then fill the wait for the next task.
     // Per-layer gradient scratch of one stage keeps the chain's outputs until those GEMMs run.
     bool defer_wgrad = false;
+    // Lazy token-embedding update (n_dp == 1, stage 0 on this rank): step k's Adam of the wte table
+    // runs at the start of step k + 1 — the rows of step k + 1's tokens first, on the compute stream
+    // before the lookup, every other row on the DP stream beside the forward — instead of in the
+    // step's tail. Each row is still updated once per step with step k's gradient and moments.
+    bool lazy_wte = false, wte_pending = false, wte_armed = false;
+    int wte_step = 0;
+    int32_t *wte_mark = nullptr, *wte_list = nullptr, *wte_count = nullptr;
+    cudaEvent_t ev_wte_mark = nullptr, ev_wte_done = nullptr;
     std::vector<cudaEvent_t> done_dx;  // per deferring Bwd task: its input gradient is ready
     std::vector<bf16*> dpre_d, dqkv_d, gmid_d, gout_d;  // [layer of the stage]
     float *dq_acc = nullptr, *delta = nullptr;
@@ -593,6 +601,13 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
         I.dpre_s[k] = I.alloc<bf16>(static_cast<size_t>(T * mlp), M_SCRATCH);
         I.dqkv_s[k] = I.alloc<bf16>(3 * Th, M_SCRATCH);
     }
+    I.lazy_wte = c_.n_dp == 1 && !o_.skip_optimizer && pl_.device_of(0) == pp_rank_;
+    if (const char* e = getenv("BFPP_LAZY_WTE")) I.lazy_wte = I.lazy_wte && atoi(e) != 0;  // A/B switch
+    if (I.lazy_wte) {
+        I.wte_mark = I.alloc<int32_t>(static_cast<size_t>(V), M_SCRATCH);
+        I.wte_list = I.alloc<int32_t>(static_cast<size_t>(c_.n_mb * T), M_SCRATCH);
+        I.wte_count = I.alloc<int32_t>(1, M_SCRATCH);
+    }
     I.defer_wgrad = p_ >= 2 && !I.wgrad_stream && !o_.recompute;
     if (const char* e = getenv("BFPP_DEFER_WGRAD")) I.defer_wgrad = I.defer_wgrad && atoi(e) != 0;  // A/B switch
     if (I.defer_wgrad)
@@ -756,6 +771,10 @@ Executor::Executor(const ModelSpec& m, const ParallelConfig& c, const ExecOption
     }
     set_flags(o.record_timeline, o.profile_kernels);
     CK(cudaEventCreate(&I.origin));
+    if (I.lazy_wte) {
+        CK(cudaEventCreateWithFlags(&I.ev_wte_mark, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&I.ev_wte_done, cudaEventDisableTiming));
+    }
     CK(cudaEventCreateWithFlags(&I.step_end, cudaEventDisableTiming));
     for (auto& e : I.step_done) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming | cudaEventBlockingSync));
     for (auto& e : I.stream_end) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -809,6 +828,8 @@ Executor::~Executor() {
         for (cudaEvent_t e : {I.ev_a[k], I.ev_b[k], I.ev_wg[k], I.ev_opt[k]})
             if (e) cudaEventDestroy(e);
     if (I.origin) cudaEventDestroy(I.origin);
+    for (cudaEvent_t e : {I.ev_wte_mark, I.ev_wte_done})
+        if (e) cudaEventDestroy(e);
     if (I.step_end) cudaEventDestroy(I.step_end);
     for (auto e : I.step_done)
         if (e) cudaEventDestroy(e);
@@ -1070,6 +1091,26 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
             const LocalStage& lsw = I.local[static_cast<size_t>(cidx)];
             const int32_t* inp = I.inputs + t.micro_batch * T;
             if (L.first) need_weights(lsw, L.wte);
+            if (L.first && I.wte_pending) {
+                // the previous step's table update: this step's token rows now, the rest beside the forward
+                LocalStage& l0 = I.local[static_cast<size_t>(cidx)];
+                const int ntok = static_cast<int>(c_.n_mb * T);
+                const int64_t base = L.wte;
+                auto rows = [&](int listed, cudaStream_t s2) {
+                    adam_rows(l0.master + base, l0.m + base, l0.v + base, l0.grad + base, l0.w16 + base, V,
+                              static_cast<int>(h), I.wte_mark, I.wte_list, I.wte_count, ntok, listed, o_.lr, o_.beta1,
+                              o_.beta2, o_.eps, o_.weight_decay, I.wte_step, s2);
+                };
+                K(K_MISC, 8.0 * ntok, 1, st,
+                  [&] { mark_rows(I.inputs, ntok, I.wte_mark, I.wte_list, I.wte_count, V, st); });
+                K(K_ADAM, 30.0 * static_cast<double>(ntok) * h, 1, st, [&] { rows(1, st); });
+                CK(cudaEventRecord(I.ev_wte_mark, st));
+                CK(cudaStreamWaitEvent(ds, I.ev_wte_mark, 0));
+                K(K_ADAM, 30.0 * static_cast<double>(V * h), 1, ds, [&] { rows(0, ds); });
+                CK(cudaEventRecord(I.ev_wte_done, ds));
+                I.wte_pending = false;
+                I.wte_armed = true;
+            }
             if (L.first)
                 K(K_MISC, 3 * Th2, 1, st, [&] {
                     embed_fwd(inp, W + L.wte, W + L.wpe, a.in, static_cast<int>(T), S, static_cast<int>(h), st);
@@ -1239,6 +1280,10 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
                 }
             }
             if (L.first && guard) guard_grads(ls, st, ws, 0, L.layers[0].ln1_g);
+            if (L.first && I.wte_armed) {  // the lazy table update still reads the previous gradient
+                CK(cudaStreamWaitEvent(st, I.ev_wte_done, 0));
+                I.wte_armed = false;
+            }
             if (L.first && acc == 0) {  // scatter-added gradients need a zeroed start
                 CK(cudaMemsetAsync(G_ + L.wte, 0, static_cast<size_t>(V * h) * 4, st));
                 CK(cudaMemsetAsync(G_ + L.wpe, 0, static_cast<size_t>(m_.s_seq * h) * 4, st));
@@ -1252,7 +1297,15 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
             CK(cudaEventRecord(I.done[static_cast<size_t>(te.id)], st));
             CK(cudaStreamWaitEvent(ws, I.done[static_cast<size_t>(te.id)], 0));
             CK(cudaEventRecord(I.done_g[static_cast<size_t>(te.id)], ws));
-            if (seg_opt && L.first) adam_segment(ls, st, ws, 0, L.layers[0].ln1_g);  // embeddings
+            if (seg_opt && L.first) {  // embeddings (the token table lazily, at the next step's start)
+                if (I.lazy_wte) {
+                    adam_segment(ls, st, ws, L.wpe, L.layers[0].ln1_g);
+                    I.wte_pending = true;
+                    I.wte_step = I.step_no;
+                } else {
+                    adam_segment(ls, st, ws, 0, L.layers[0].ln1_g);
+                }
+            }
             break;
         }
         case TaskKind::Transfer: {
@@ -1461,6 +1514,7 @@ void Executor::set_params(i64 stage, const float* host, int64_t n) {
     Impl& I = *impl_;
     CK(cudaSetDevice(I.dev));
     sync();
+    I.wte_pending = I.wte_armed = false;  // the optimizer restarts: no deferred update carries over
     cudaStream_t cs = I.st[S_COMPUTE];
     LocalStage& ls = find_local(I.local, stage);
     const StageLayout& L = layouts_[static_cast<size_t>(stage)];
@@ -1490,9 +1544,27 @@ void Executor::set_params(i64 stage, const float* host, int64_t n) {
     I.step_no = 0;
 }
 
+// Completes a pending lazy token-table update (all rows, the pending step's bias corrections) so
+// the parameters read back are those after the last step.
+void Executor::flush_lazy_updates() {
+    Impl& I = *impl_;
+    if (!I.wte_pending) return;
+    CK(cudaSetDevice(I.dev));
+    for (LocalStage& ls : I.local) {
+        const StageLayout& L = layouts_[static_cast<size_t>(ls.stage)];
+        if (!L.first) continue;
+        const int64_t base = L.wte, n = L.wpe - L.wte;
+        adam_update(ls.master + base, ls.m + base, ls.v + base, ls.grad + base, ls.w16 + base, n, o_.lr, o_.beta1,
+                    o_.beta2, o_.eps, o_.weight_decay, I.wte_step, 0, I.st[S_COMPUTE]);
+    }
+    I.wte_pending = false;
+    CK(cudaStreamSynchronize(I.st[S_COMPUTE]));
+}
+
 void Executor::get_params(i64 stage, float* host, int64_t n, int64_t* lo, int64_t* hi) {
     Impl& I = *impl_;
     sync();
+    flush_lazy_updates();
     CK(cudaDeviceSynchronize());
     LocalStage& ls = find_local(I.local, stage);
     const StageLayout& L = layouts_[static_cast<size_t>(stage)];
@@ -1522,6 +1594,7 @@ void Executor::get_grads(i64 stage, float* host, int64_t n, int64_t* lo, int64_t
 void Executor::get_weights16(i64 stage, uint16_t* host, int64_t n, int64_t* lo, int64_t* hi) {
     Impl& I = *impl_;
     sync();
+    flush_lazy_updates();
     CK(cudaDeviceSynchronize());
     LocalStage& ls = find_local(I.local, stage);
     const StageLayout& L = layouts_[static_cast<size_t>(stage)];

@@ -101,6 +101,8 @@ public:
     const StageLayout& layout(i64 stage) const { return layouts_[static_cast<size_t>(stage)]; }
     void set_params(i64 stage, const float* host, int64_t n);
     void get_params(i64 stage, float* host, int64_t n, int64_t* lo, int64_t* hi);
+    // completes deferred optimizer work (the lazy token-table update) before parameters are read
+    void flush_lazy_updates();
     void get_grads(i64 stage, float* host, int64_t n, int64_t* lo, int64_t* hi);
     void zero_grads();
     // bf16 compute weights: resident copy (full) or this rank's all-gather source shard (DP_FS)

@@ -247,6 +247,67 @@ __global__ void __launch_bounds__(kAdamThreads) adam_kernel(float* __restrict__ 
     }
 }
 
+// ---- row-wise Adam over an embedding table [rows][h] (h % 4 == 0), same math as adam_kernel ----
+// The next step's token rows are updated first (list pass, before the embedding lookup) and every
+// other row afterwards (masked pass, off the critical path); each row is updated exactly once.
+__device__ __forceinline__ void adam_group(float* p, float* m, float* v, const float* g, __nv_bfloat16* w16,
+                                           int64_t i, float lr, float b1, float b2, float eps, float wd, float bc1,
+                                           float bc2, uint64_t pol) {
+    float4 P = ld4_stream(reinterpret_cast<const float4*>(p) + i, pol);
+    float4 M = ld4_stream(reinterpret_cast<const float4*>(m) + i, pol);
+    float4 Vv = ld4_stream(reinterpret_cast<const float4*>(v) + i, pol);
+    const float4 G = ld4_stream(reinterpret_cast<const float4*>(g) + i, pol);
+    float* pp = &P.x;
+    float* mm = &M.x;
+    float* vv = &Vv.x;
+    const float* gg = &G.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        mm[k] = b1 * mm[k] + (1.f - b1) * gg[k];
+        vv[k] = b2 * vv[k] + (1.f - b2) * gg[k] * gg[k];
+        pp[k] -= lr * (__fdividef(mm[k] * bc1, sqrtf(vv[k] * bc2) + eps) + wd * pp[k]);
+    }
+    st4_stream(reinterpret_cast<float4*>(p) + i, P, pol);
+    st4_stream(reinterpret_cast<float4*>(m) + i, M, pol);
+    st4_stream(reinterpret_cast<float4*>(v) + i, Vv, pol);
+    __nv_bfloat162 lo = __floats2bfloat162_rn(P.x, P.y), hi = __floats2bfloat162_rn(P.z, P.w);
+    uint2 o;
+    o.x = *reinterpret_cast<uint32_t*>(&lo);
+    o.y = *reinterpret_cast<uint32_t*>(&hi);
+    st2_stream(reinterpret_cast<uint2*>(w16) + i, o, pol);
+}
+
+// mark[tok] = 1 for every token; the first marker of a row appends it to list (order irrelevant:
+// rows are independent)
+__global__ void mark_rows_kernel(const int32_t* __restrict__ tok, int n, int32_t* __restrict__ mark,
+                                 int32_t* __restrict__ list, int32_t* __restrict__ count) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int r = tok[i];
+    if (atomicExch(&mark[r], 1) == 0) list[atomicAdd(count, 1)] = r;
+}
+
+__global__ void __launch_bounds__(256) adam_rows_list_kernel(float* p, float* m, float* v, const float* g,
+                                                             __nv_bfloat16* w16, const int32_t* __restrict__ list,
+                                                             const int32_t* __restrict__ count, int max_rows, int h4,
+                                                             float lr, float b1, float b2, float eps, float wd,
+                                                             float bc1, float bc2) {
+    const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int li = static_cast<int>(idx / h4);
+    if (li >= max_rows || li >= *count) return;
+    const int64_t i = static_cast<int64_t>(list[li]) * h4 + idx % h4;
+    adam_group(p, m, v, g, w16, i, lr, b1, b2, eps, wd, bc1, bc2, evict_first_policy());
+}
+
+__global__ void __launch_bounds__(256) adam_rows_unmarked_kernel(float* p, float* m, float* v, const float* g,
+                                                                 __nv_bfloat16* w16, const int32_t* __restrict__ mark,
+                                                                 int64_t rows, int h4, float lr, float b1, float b2,
+                                                                 float eps, float wd, float bc1, float bc2) {
+    // one float4 per thread and short-lived blocks, like adam_kernel (it runs beside the GEMMs)
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < rows * h4 && !mark[i / h4]) adam_group(p, m, v, g, w16, i, lr, b1, b2, eps, wd, bc1, bc2, evict_first_policy());
+}
+
 __global__ void init_normal_kernel(float* __restrict__ p, __nv_bfloat16* __restrict__ w16, int64_t n, float mean,
                                    float std, uint64_t seed, uint64_t offset) {
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x * 4;
@@ -347,6 +408,32 @@ void adam_update(float* p, float* m, float* v, float* g, void* w16, int64_t n, f
     if (grid_cap > 0 && blocks > grid_cap) blocks = grid_cap;
     adam_kernel<<<static_cast<unsigned>(blocks > 0 ? blocks : 1), kAdamThreads, 0, st>>>(
         p, m, v, g, static_cast<__nv_bfloat16*>(w16), n, lr, b1, b2, eps, wd, bc1, bc2, zero_grad);
+}
+
+void mark_rows(const int32_t* tok, int n, int32_t* mark, int32_t* list, int32_t* count, int64_t rows,
+               cudaStream_t st) {
+    cudaMemsetAsync(mark, 0, static_cast<size_t>(rows) * 4, st);
+    cudaMemsetAsync(count, 0, 4, st);
+    mark_rows_kernel<<<(n + 255) / 256, 256, 0, st>>>(tok, n, mark, list, count);
+}
+
+void adam_rows(float* p, float* m, float* v, const float* g, void* w16, int64_t rows, int h, const int32_t* mark,
+               const int32_t* list, const int32_t* count, int max_rows, int listed, float lr, float b1, float b2,
+               float eps, float wd, int step, cudaStream_t st) {
+    if (h % 4) throw std::runtime_error("adam_rows: row width must be a multiple of 4");
+    const float bc1 = 1.f / (1.f - powf(b1, static_cast<float>(step)));
+    const float bc2 = 1.f / (1.f - powf(b2, static_cast<float>(step)));
+    const int h4 = h / 4;
+    auto* w = static_cast<__nv_bfloat16*>(w16);
+    if (listed) {
+        const int64_t n = static_cast<int64_t>(max_rows) * h4;
+        adam_rows_list_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(
+            p, m, v, g, w, list, count, max_rows, h4, lr, b1, b2, eps, wd, bc1, bc2);
+    } else {
+        const int64_t n = rows * h4;
+        adam_rows_unmarked_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(p, m, v, g, w, mark, rows, h4,
+                                                                                        lr, b1, b2, eps, wd, bc1, bc2);
+    }
 }
 
 void init_normal(float* p, void* w16, int64_t n, float mean, float std, uint64_t seed, uint64_t offset,

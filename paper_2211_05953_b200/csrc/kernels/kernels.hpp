@@ -35,6 +35,14 @@ void softmax_xent(void* logits, int64_t ld, const int32_t* labels, float* row_lo
                   cudaStream_t st);
 void adam_update(float* p, float* m, float* v, float* g, void* w16, int64_t n, float lr, float b1, float b2,
                  float eps, float wd, int step, int zero_grad, cudaStream_t st);
+// Row-wise Adam over an embedding table (same math as adam_update): mark_rows marks the rows of
+// `tok` in mark[rows] and lists them once each; adam_rows updates the listed rows (listed = 1) or
+// every unmarked row (listed = 0)
+void mark_rows(const int32_t* tok, int n, int32_t* mark, int32_t* list, int32_t* count, int64_t rows,
+               cudaStream_t st);
+void adam_rows(float* p, float* m, float* v, const float* g, void* w16, int64_t rows, int h, const int32_t* mark,
+               const int32_t* list, const int32_t* count, int max_rows, int listed, float lr, float b1, float b2,
+               float eps, float wd, int step, cudaStream_t st);
 void init_normal(float* p, void* w16, int64_t n, float mean, float std, uint64_t seed, uint64_t offset,
                  cudaStream_t st);
 void f32_to_bf16(const float* src, void* dst, int64_t n, cudaStream_t st);
