@@ -276,7 +276,7 @@ struct Executor::Impl {
     // runs at the start of step k + 1 — the rows of step k + 1's tokens first, on the compute stream
     // before the lookup, every other row on the DP stream beside the forward — instead of in the
     // step's tail. Each row is still updated once per step with step k's gradient and moments.
-    bool lazy_wte = false, wte_pending = false, wte_armed = false;
+    bool lazy_wte = false, wte_pending = false, wte_armed = false, wte_rest = false;
     int wte_step = 0;
     int32_t *wte_mark = nullptr, *wte_list = nullptr, *wte_count = nullptr;
     cudaEvent_t ev_wte_mark = nullptr, ev_wte_done = nullptr;
@@ -1105,10 +1105,8 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
                   [&] { mark_rows(I.inputs, ntok, I.wte_mark, I.wte_list, I.wte_count, V, st); });
                 K(K_ADAM, 30.0 * static_cast<double>(ntok) * h, 1, st, [&] { rows(1, st); });
                 CK(cudaEventRecord(I.ev_wte_mark, st));
-                CK(cudaStreamWaitEvent(ds, I.ev_wte_mark, 0));
-                K(K_ADAM, 30.0 * static_cast<double>(V * h), 1, ds, [&] { rows(0, ds); });
-                CK(cudaEventRecord(I.ev_wte_done, ds));
                 I.wte_pending = false;
+                I.wte_rest = true;  // the other rows: issued with the step's first backward (below)
                 I.wte_armed = true;
             }
             if (L.first)
@@ -1144,6 +1142,25 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
             LocalStage& ls = I.local[static_cast<size_t>(cidx)];
             const bf16* W = weights(te, cidx);
             float* G_ = ls.grad;
+            if (I.wte_rest) {
+                // the lazy table update's other rows go on the DP stream at the start of the backward,
+                // where it is idle until the first layer's gradients exist, instead of beside the
+                // forward (which has no optimizer work to hide behind)
+                I.wte_rest = false;
+                for (LocalStage& l0 : I.local) {
+                    const StageLayout& L0 = layouts_[static_cast<size_t>(l0.stage)];
+                    if (!L0.first) continue;
+                    const int64_t base = L0.wte;
+                    CK(cudaStreamWaitEvent(ds, I.ev_wte_mark, 0));
+                    K(K_ADAM, 30.0 * static_cast<double>(V * h), 1, ds, [&] {
+                        adam_rows(l0.master + base, l0.m + base, l0.v + base, l0.grad + base, l0.w16 + base, V,
+                                  static_cast<int>(h), I.wte_mark, I.wte_list, I.wte_count,
+                                  static_cast<int>(c_.n_mb * T), 0, o_.lr, o_.beta1, o_.beta2, o_.eps,
+                                  o_.weight_decay, I.wte_step, ds);
+                    });
+                    CK(cudaEventRecord(I.ev_wte_done, ds));
+                }
+            }
             // weight-gradient GEMMs: same stream by default (measured faster at T = 2048, where two
             // persistent GEMM grids only interleave at CTA granularity); BFPP_WGRAD_STREAM=1 runs
             // them on a separate stream overlapping the data-gradient chain
@@ -1514,7 +1531,7 @@ void Executor::set_params(i64 stage, const float* host, int64_t n) {
     Impl& I = *impl_;
     CK(cudaSetDevice(I.dev));
     sync();
-    I.wte_pending = I.wte_armed = false;  // the optimizer restarts: no deferred update carries over
+    I.wte_pending = I.wte_armed = I.wte_rest = false;  // the optimizer restarts: no deferred update carries over
     cudaStream_t cs = I.st[S_COMPUTE];
     LocalStage& ls = find_local(I.local, stage);
     const StageLayout& L = layouts_[static_cast<size_t>(stage)];
