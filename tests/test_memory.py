@@ -144,3 +144,36 @@ def test_reference_model_vs_executor_plan():
     ours = max(p["total"] for p in _per_rank(cfg, c, recompute=True))
     assert ours > 10 * ref.total_bytes
     assert ps.feasible(m, c, ps.cluster_preset("b200"))
+
+
+def test_deferred_wgrad_and_lazy_table_scratch(monkeypatch):
+    """The per-layer gradient scratch of deferred weight gradients (n_pp >= 2: dpre, dqkv, gmid, gout
+    per layer of a stage) and the lazy token-table update's row marks / list (n_dp = 1, the rank of
+    stage 0) are in the plan, with exactly these sizes; the A/B switches remove them."""
+    cfg = GPTConfig.preset("gpt-1.3b")
+    T, h, mlp, V = cfg.s_seq, cfg.s_hidden, cfg.s_mlp, cfg.s_voc
+    c = ps.ParallelConfig(n_pp=2, n_loop=4, n_mb=2, schedule=S.BreadthFirst)
+    lps = cfg.n_layers // (c.n_pp * c.n_loop)
+
+    def rnd(n):  # the executor's allocator rounds each buffer up to >= 256 bytes
+        return max(n, 256)
+
+    defer_bytes = lps * (rnd(2 * T * mlp) + rnd(2 * 3 * T * h) + 2 * rnd(2 * T * h))
+    lazy_bytes = rnd(4 * V) + rnd(4 * c.n_mb * T) + rnd(4)
+    base = {}
+    for defer in ("1", "0"):
+        for lazy in ("1", "0"):
+            monkeypatch.setenv("BFPP_DEFER_WGRAD", defer)
+            monkeypatch.setenv("BFPP_LAZY_WTE", lazy)
+            base[defer, lazy] = [memory_plan(cfg, c, r)["scratch"] for r in range(2)]
+    for r in range(2):
+        assert base["1", "0"][r] - base["0", "0"][r] == defer_bytes
+        lazy_here = lazy_bytes if r == 0 else 0  # stage 0 lives on rank 0
+        assert base["0", "1"][r] - base["0", "0"][r] == lazy_here
+        assert base["1", "1"][r] - base["0", "0"][r] == defer_bytes + lazy_here
+    # recompute keeps one working set per rank: no deferral scratch
+    monkeypatch.setenv("BFPP_DEFER_WGRAD", "1")
+    monkeypatch.setenv("BFPP_LAZY_WTE", "0")
+    rc = memory_plan(cfg, c, 1, recompute=True)["scratch"]
+    monkeypatch.setenv("BFPP_DEFER_WGRAD", "0")
+    assert memory_plan(cfg, c, 1, recompute=True)["scratch"] == rc
