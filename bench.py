@@ -452,6 +452,12 @@ def main():
             "memory": memory_report(ex, cfg, config, args.recompute, mem_used),
             "comm": comm,
             "measured_timing": measured_timing,
+            "executor_options": {
+                "defer_wgrad": pp >= 2 and not args.recompute and os.environ.get("BFPP_DEFER_WGRAD", "1") != "0"
+                and os.environ.get("BFPP_WGRAD_STREAM", "0") == "0",
+                "lazy_token_table_update": dp == 1 and os.environ.get("BFPP_LAZY_WTE", "1") != "0",
+                "gemm_tile_schedule": "dynamic" if os.environ.get("BFPP_GEMM_DYN") == "1" else "static",
+                "dp_copy_engine_allgather": dp >= 2 and os.environ.get("BFPP_DP_CE_ALLGATHER") == "1"},
         }
         print(json.dumps(line), flush=True)
     ex.close()
