@@ -667,7 +667,6 @@ __global__ void __maxnreg__(96)
             while (next(g)) {
                 const Prob pb = prob(g.tile);
                 if (!use_sk) g.kb1 = pb.nk;
-                const int t = pb.t;
                 const int m0 = pb.mi * 256 + 128 * rank, n0 = pb.ni * BN + (BN / 2) * rank;
                 for (int kb = g.kb0; kb < g.kb1; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
