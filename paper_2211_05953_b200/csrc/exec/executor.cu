@@ -1151,6 +1151,9 @@ void Executor::step(const int32_t* tokens, bool on_host, float* loss_host, float
                     const StageLayout& L0 = layouts_[static_cast<size_t>(l0.stage)];
                     if (!L0.first) continue;
                     const int64_t base = L0.wte;
+                    // device order, not host order: the DP stream waits for the compute stream to
+                    // reach this backward (after every forward of the step, and after the row marks)
+                    CK(cudaEventRecord(I.ev_wte_mark, st));
                     CK(cudaStreamWaitEvent(ds, I.ev_wte_mark, 0));
                     K(K_ADAM, 30.0 * static_cast<double>(V * h), 1, ds, [&] {
                         adam_rows(l0.master + base, l0.m + base, l0.v + base, l0.grad + base, l0.w16 + base, V,
