@@ -350,42 +350,35 @@ __global__ void __launch_bounds__(256, 1) ln_bwd_reg_kernel(const __nv_bfloat16*
     }
 }
 
-// dgamma/dbeta (=, or += when accumulating) = column sums of the n_part block partials:
-// 8 warps split the partials, each lane owns 2 adjacent columns (64 per block), then a
-// shared-memory sum across the warps. Deterministic, no atomics, no memsets.
-__global__ void __launch_bounds__(256) ln_partsum_kernel(const float* __restrict__ ws, int n_part, int width,
-                                                         float* __restrict__ dgamma, float* __restrict__ dbeta,
-                                                         int accumulate) {
-    __shared__ float2 red[8][32];
+// dgamma/dbeta (=, or += when accumulating) = column sums of the n_part block partials: 32
+// columns per block (one per lane, 128-byte rows per warp access), 16 warps split the partials
+// and a fixed-order shared-memory sum combines them. Deterministic, no atomics, no memsets.
+constexpr int kPartsumWarps = 16;
+__global__ void __launch_bounds__(kPartsumWarps * 32) ln_partsum_kernel(const float* __restrict__ ws, int n_part,
+                                                                        int width, float* __restrict__ dgamma,
+                                                                        float* __restrict__ dbeta, int accumulate) {
+    __shared__ float red[kPartsumWarps][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int c = blockIdx.x * 64 + lane * 2;  // column in [0, 2 width)
-    float2 s = make_float2(0.f, 0.f);
+    const int c = blockIdx.x * 32 + lane;  // column in [0, 2 width)
+    float s = 0.f;
     if (c < 2 * width) {
 #pragma unroll 8
-        for (int b = warp; b < n_part; b += 8) {
-            const float2 v = *reinterpret_cast<const float2*>(ws + static_cast<int64_t>(b) * 2 * width + c);
-            s.x += v.x;
-            s.y += v.y;
-        }
+        for (int b = warp; b < n_part; b += kPartsumWarps) s += ws[static_cast<int64_t>(b) * 2 * width + c];
     }
     red[warp][lane] = s;
     __syncthreads();
     if (warp == 0 && c < 2 * width) {
-        float2 t = red[0][lane];
+        float t = red[0][lane];
 #pragma unroll
-        for (int w = 1; w < 8; ++w) {
-            t.x += red[w][lane].x;
-            t.y += red[w][lane].y;
-        }
+        for (int w = 1; w < kPartsumWarps; ++w) t += red[w][lane];
         float* dst = c < width ? dgamma + c : dbeta + (c - width);
-        if (accumulate) {
-            dst[0] += t.x;
-            dst[1] += t.y;
-        } else {
-            dst[0] = t.x;
-            dst[1] = t.y;
-        }
+        *dst = accumulate ? *dst + t : t;
     }
+}
+void launch_partsum(const float* ws, int n_part, int width, float* dgamma, float* dbeta, int accumulate,
+                    cudaStream_t st) {
+    ln_partsum_kernel<<<(2 * width + 31) / 32, kPartsumWarps * 32, 0, st>>>(ws, n_part, width, dgamma, dbeta,
+                                                                          accumulate);
 }
 
 // chunks of 8 elements per lane: NCH = 1, 2, 4, 8, 12, 16, 20, 24 (width <= 256 NCH), up to MAX
@@ -947,7 +940,7 @@ void layernorm_bwd(const void* dy, const void* x, const void* gamma, const float
             if (dres) launch(ln_bwd_bulk_kernel<RR, CC, true>, 3);
             else launch(ln_bwd_bulk_kernel<RR, CC, false>, 2);
         });
-        ln_partsum_kernel<<<(2 * width + 63) / 64, 256, 0, st>>>(part, parts, width, dgamma, dbeta, accumulate);
+        launch_partsum(part, parts, width, dgamma, dbeta, accumulate, st);
         return;
     }
     {
@@ -960,7 +953,7 @@ void layernorm_bwd(const void* dy, const void* x, const void* gamma, const float
             ln_bwd_mw_kernel<W><<<parts, Sh::kThreads, 0, st>>>(
                 DY, X, static_cast<const __nv_bfloat16*>(gamma), mean, rstd, static_cast<const __nv_bfloat16*>(dres),
                 static_cast<__nv_bfloat16*>(dx), part, rows, width);
-            ln_partsum_kernel<<<(2 * width + 63) / 64, 256, 0, st>>>(part, parts, width, dgamma, dbeta, accumulate);
+            launch_partsum(part, parts, width, dgamma, dbeta, accumulate, st);
         });
         if (wide) return;
     }
@@ -973,7 +966,7 @@ void layernorm_bwd(const void* dy, const void* x, const void* gamma, const float
                 static_cast<__nv_bfloat16*>(dx), part, rows, width);
         });  // x and dy both register-resident: up to 16 chunks per lane without spills
         if (done) {
-            ln_partsum_kernel<<<(2 * width + 63) / 64, 256, 0, st>>>(part, blocks, width, dgamma, dbeta, accumulate);
+            launch_partsum(part, blocks, width, dgamma, dbeta, accumulate, st);
             return;
         }
     }
