@@ -22,29 +22,42 @@ constexpr int D = 128;  // head dim
 
 // delta_i = sum_d dO[i,d] * O[i,d]: half a warp per (token, head), 16-byte loads (8 bf16 per lane).
 __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
-                                     float* __restrict__ delta, int S, int H, int T) {
-    const int pair = (blockIdx.x * blockDim.x + threadIdx.x) >> 4, l16 = threadIdx.x & 15;
-    const bool ok = pair < T * H;
-    float s = 0.f;
-    if (ok) {
-        const int row = pair / H, head = pair % H;
-        const int64_t off = static_cast<int64_t>(row) * H * D + head * D + l16 * 8;
-        const uint4 a = __ldg(reinterpret_cast<const uint4*>(o + off));
-        const uint4 c = __ldg(reinterpret_cast<const uint4*>(dout + off));
-        const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
-        const __nv_bfloat162* c2 = reinterpret_cast<const __nv_bfloat162*>(&c);
+                                     float* __restrict__ delta, float* __restrict__ dq_acc, int S, int H, int T) {
+    // a half-warp per two (token, head) pairs: all four 16-byte loads in flight before the math;
+    // the same threads zero the pairs' dQ accumulator rows (no separate memset)
+    const int base = ((blockIdx.x * blockDim.x + threadIdx.x) >> 4) * 2, l16 = threadIdx.x & 15;
+    uint4 a[2], c[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int pair = base + k;
+        if (pair < T * H) {
+            const int64_t off = static_cast<int64_t>(pair) * D + l16 * 8;  // [T][H][D] = pair * D
+            a[k] = __ldg(reinterpret_cast<const uint4*>(o + off));
+            c[k] = __ldg(reinterpret_cast<const uint4*>(dout + off));
+            __stcs(reinterpret_cast<float4*>(dq_acc + off), make_float4(0.f, 0.f, 0.f, 0.f));
+            __stcs(reinterpret_cast<float4*>(dq_acc + off + 4), make_float4(0.f, 0.f, 0.f, 0.f));
+        } else {
+            a[k] = c[k] = make_uint4(0, 0, 0, 0);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a[k]);
+        const __nv_bfloat162* c2 = reinterpret_cast<const __nv_bfloat162*>(&c[k]);
+        float s = 0.f;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const float2 x = __bfloat1622float2(a2[i]), y = __bfloat1622float2(c2[i]);
             s += x.x * y.x + x.y * y.y;
         }
-    }
 #pragma unroll
-    for (int k = 8; k; k >>= 1) s += __shfl_xor_sync(0xffffffff, s, k);
-    if (ok && l16 == 0) {
-        const int row = pair / H, head = pair % H;
-        const int b = row / S, q = row % S;
-        delta[(static_cast<int64_t>(b) * H + head) * S + q] = s;
+        for (int m = 8; m; m >>= 1) s += __shfl_xor_sync(0xffffffff, s, m);
+        const int pair = base + k;
+        if (pair < T * H && l16 == 0) {
+            const int row = pair / H, head = pair % H;
+            const int bb = row / S, q = row % S;
+            delta[(static_cast<int64_t>(bb) * H + head) * S + q] = s;
+        }
     }
 }
 
@@ -74,11 +87,10 @@ void attention_bwd(const void* qkv, const void* o, const void* dout, const float
     if (head_dim != D) throw std::runtime_error("attention: head_dim must be 128");
     const int T = batch * seq;
     const int64_t n = static_cast<int64_t>(T) * heads * head_dim;
-    if (cudaMemsetAsync(dq_acc, 0, static_cast<size_t>(n) * sizeof(float), st) != cudaSuccess)
-        throw std::runtime_error("attention: dQ accumulator memset failed");
     const int pairs = T * heads;
-    attn_bwd_prep_kernel<<<(pairs + 15) / 16, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(o),
-                                                            static_cast<const __nv_bfloat16*>(dout), delta, seq, heads, T);
+    attn_bwd_prep_kernel<<<(pairs + 31) / 32, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(o),
+                                                            static_cast<const __nv_bfloat16*>(dout), delta, dq_acc,
+                                                            seq, heads, T);
     attention_bwd_tc(qkv, dout, lse, delta, dq_acc, dqkv, batch, seq, heads, head_dim, st);
     attn_dq_convert_kernel<<<static_cast<unsigned>((n / 8 + 255) / 256), 256, 0, st>>>(
         dq_acc, static_cast<__nv_bfloat16*>(dqkv), T, heads * head_dim);
